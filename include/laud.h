@@ -1,0 +1,154 @@
+/* laud.h — C-ABI of the B200 LAUDNet dynamic-inference path.
+ *
+ * One shared library (paper_2308_15949_b200/_laud.so, sm_100a) behind the
+ * Python operator surface of the reference's `dynlat.reference`.  Plain
+ * pointers and sizes only; every device pointer is caller-allocated CUDA
+ * memory, every call is stream-ordered and asynchronous (no host sync, no
+ * allocation on the hot path), `stream` is a cudaStream_t (NULL = legacy).
+ *
+ * Layout: activations NHWC bfloat16 with a per-pixel channel stride `ld`
+ * (multiple of 8, channels zero-padded); weights packed bf16
+ * [c_out][k*k taps][kpad(c_in)] (kpad = c_in rounded up to 64, zero filled);
+ * folded-BN scale/bias fp32 [c_out] (NULL = 1 / 0); masks uint8 per cell,
+ * active-cell and active-pixel lists int32 row-major (n, i, j) linear index.
+ *
+ * Status codes map onto the reference's exception classes
+ * (`pkg/src/dynlat/errors.py:8-29`); the Python layer re-raises them.
+ */
+#ifndef LAUD_H_
+#define LAUD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAUD_OK 0
+#define LAUD_ERR_GRANULARITY 1 /* GranularityMismatch (reference.py:171-172, 304-305) */
+#define LAUD_ERR_MASK_SHAPE 2  /* MaskShapeMismatch (reference.py:307-310, 332-335)  */
+#define LAUD_ERR_SHAPE 3       /* ShapeMismatch (reference.py:36-37, 54-67)           */
+#define LAUD_ERR_UNSUPPORTED 4 /* ShapeMismatch: channel skipping with groups != 1 (reference.py:405-406) */
+#define LAUD_ERR_CUDA 5        /* launch / runtime failure                            */
+#define LAUD_ERR_ARG 6         /* ValueError: bad argument                            */
+
+#define LAUD_PARADIGM_SPATIAL 0
+#define LAUD_PARADIGM_CHANNEL 1
+#define LAUD_PARADIGM_LAYER 2
+#define LAUD_PARADIGM_STATIC 3
+
+/* Library identity and the calling thread's last error message. */
+const char* laud_version(void);
+const char* laud_last_error(void);
+/* Number of kernels this library launched since load (diagnostics / bench). */
+uint64_t laud_launch_count(void);
+
+/* Bytes of look-back scratch for a compaction over `items` elements.  Must be
+ * zeroed once after allocation; the kernels restore it to zero. */
+size_t laud_scan_workspace_bytes(int items);
+/* fp32 partial sums the spatial masker needs for this geometry. */
+size_t laud_masker_partial_floats(int n, int h, int w, int c, int s, int stride);
+
+/* Spatial (and layer, s*stride = H) masker — replaces
+ * `spatial_masker_forward` + `build_gather_plan` (reference.py:156-186, 133-135)
+ * with the fused-masker identity of reference.py:244-253: decision per cell of
+ * the OUTPUT grid = mean over the (s*stride)^2 input window of x.wdiff + bias
+ * >= 0 (x bf16, or fp32 when x_f32).  Writes coarse[n*(H/(s*st))*(W/(s*st))], the row-major list of active
+ * cells and its device-side count. */
+int laud_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c, int s,
+                        int stride, const float* wdiff, float bias, uint8_t* coarse,
+                        int* cell_list, int* cell_count, float* partial, void* scan,
+                        void* stream);
+
+/* Active-cell list from a caller-supplied coarse mask (argwhere order). */
+int laud_cells_from_mask(const uint8_t* coarse, int cells, int* cell_list, int* cell_count,
+                         void* scan, void* stream);
+
+/* conv1 work set: input pixels covered by an active cell's window grown by
+ * `radius` (1 = conv2's 3x3 halo).  With stride 1 this is exactly the
+ * Chebyshev dilation of reference.py:226-241 (`dilate_and_rates`, k = 2r+1). */
+int laud_dilate_pixels(const uint8_t* coarse, int n, int h_in, int w_in, int s, int stride,
+                       int radius, int* pix_list, int* pix_count, void* scan, void* stream);
+
+/* Generic implicit-GEMM convolution (tcgen05 / TMEM / TMA engine). */
+typedef struct laud_conv_args {
+  int row_mode; /* 0 dense output grid, 1 active-patch list, 2 pixel list */
+  const int* list;
+  const int* count; /* device count, NULL -> rows_max */
+  int rows_max;
+  int batch, out_h, out_w;
+  int patch_h, patch_w, cells_h, cells_w;
+  const void* act;
+  int in_h, in_w, in_c, in_ld;
+  int a_compact;
+  int ksize, stride, pad;
+  const void* weight; /* packed [n_out][ksize*ksize][kpad(in_c)] bf16 */
+  int n_out;
+  const float* scale;
+  const float* bias;
+  int relu;
+  int out_mode; /* 0 scatter to output pixel, 1 compact row */
+  void* out;
+  int out_ld;
+  int out_f32;
+  const void* resid;
+  int resid_ld;
+  const uint8_t* relu_inactive_coarse;
+  const uint8_t* ymask_coarse;  /* dense-masked: y *= coarse[cell]       */
+  const uint8_t* ymask_channel; /* dense-masked: y *= mask[n][channel]   */
+  int misplace_first;
+} laud_conv_args;
+
+int laud_conv(const laud_conv_args* a, void* stream);
+
+/* One bottleneck block forward — replaces `block_forward_sparse`
+ * (reference.py:356-436) for SPATIAL / LAYER / STATIC.  Masks: either
+ * given (`given_coarse`, uint8 per cell; spatial cells on the output grid,
+ * layer = one per sample) or computed by the masker (`masker_wdiff`,
+ * `masker_bias`).  `out` may alias `x` only when the block has no
+ * downsample and shapes match (in-place residual). */
+typedef struct laud_block_args {
+  int paradigm;
+  int n, h_in, w_in, c_in, x_ld;
+  int c_mid, c_out, stride, groups;
+  int s; /* spatial granularity S (output grid) */
+  int has_down;
+  const void* x;
+  void* out;
+  const void* w1;
+  const void* w2;
+  const void* w3;
+  const void* wd;
+  const float *s1, *b1, *s2, *b2, *s3, *b3, *sd, *bd;
+  int relu1, relu2, relu_out;
+  const float* masker_wdiff;
+  float masker_bias;
+  const uint8_t* given_coarse;
+  /* outputs + workspace (laud_block_workspace_bytes) */
+  uint8_t* coarse_out;
+  int* cell_list;
+  int* cell_count;
+  int* pix_list;
+  int* pix_count;
+  void* h1;
+  void* h2;
+  float* partial;
+  void* scan;
+  int misplace_first; /* test-only fault hook (reference.py:362, 400-401) */
+} laud_block_args;
+
+int laud_block_forward(const laud_block_args* a, void* stream);
+
+/* Network glue: stem im2col from uint8 NHWC images (mean/std normalised),
+ * 3x3/s2 max-pool, global average pool. */
+int laud_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride, int pad,
+                     const float* mean, const float* inv_std, void* cols, int cols_ld,
+                     void* stream);
+int laud_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, void* stream);
+int laud_global_avgpool(const void* x, int n, int hw, int c, void* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAUD_H_ */

@@ -1,0 +1,71 @@
+"""Build the in-tree CUDA library ``_laud.so`` for sm_100a with nvcc.
+
+Every .cu under csrc/ goes into one shared object (static cudart, no torch
+dependency) loaded by ``_lib.py`` through ctypes.  Also dumps per-kernel
+register/smem usage (``-Xptxas -v``) to build/ptxas.log and the SASS to
+build/laud.sass so the tcgen05/TMA instruction evidence can be committed.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT = PKG / "_laud.so"
+BUILD = PKG.parent / "build"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+         "-Xptxas", "-v", "-I", str(PKG.parent / "include")]
+
+
+def sources():
+    return sorted(CSRC.glob("*.cu"))
+
+
+def needs_build() -> bool:
+    if not OUT.exists():
+        return True
+    t = OUT.stat().st_mtime
+    deps = list(CSRC.glob("*")) + [PKG.parent / "include" / "laud.h"]
+    return any(p.stat().st_mtime > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not needs_build():
+        return OUT
+    BUILD.mkdir(exist_ok=True)
+    objs = []
+    log = []
+    for src in sources():
+        obj = BUILD / (src.stem + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        log.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {src.name}")
+        objs.append(str(obj))
+    tmp = OUT.with_suffix(".so.tmp")
+    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", str(tmp)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed")
+    os.replace(tmp, OUT)
+    (BUILD / "ptxas.log").write_text("\n".join(log))
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(OUT)],
+                          capture_output=True, text=True)
+    (BUILD / "laud.sass").write_text(sass.stdout)
+    if verbose:
+        print("\n".join(log))
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(OUT)

@@ -1,0 +1,489 @@
+// C-ABI of the LAUDNet B200 path (include/laud.h): argument validation with
+// the reference's error taxonomy, TMA descriptor cache, and the block-level
+// composition of masker -> dilate -> gather-conv1 -> patch conv2 ->
+// conv3 + scatter-add (reference semantics `reference.py:356-436`).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/laud.h"
+#include "laud_conv.cuh"
+
+namespace laud {
+cudaError_t launch_conv_gemm(const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
+                             cudaStream_t stream);
+size_t scan_state_bytes(int total);
+int masker_splits(int win, int c, int* chunks_per_split);
+cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c,
+                                  int s, int stride, const float* wdiff, float bias,
+                                  uint8_t* coarse, int* list, int* count, float* partial,
+                                  void* scan, cudaStream_t stream);
+cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,
+                                  void* scan, cudaStream_t stream);
+cudaError_t launch_dilate_pixels(const uint8_t* coarse, int n, int h, int w, int s, int stride,
+                                 int cells_h, int cells_w, int radius, int* list, int* count,
+                                 void* scan, cudaStream_t stream);
+cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride, int pad,
+                               const float* mean, const float* inv_std, void* cols, int cols_ld,
+                               cudaStream_t s);
+cudaError_t launch_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, cudaStream_t s);
+cudaError_t launch_gap(const void* x, int n, int hw, int c, void* y, cudaStream_t s);
+}  // namespace laud
+
+using namespace laud;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what, int launches) {
+  if (e != cudaSuccess) return fail(LAUD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  g_launches += launches;
+  return LAUD_OK;
+}
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  int rows, k, bn, dev;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && k == o.k && bn == o.bn && dev == o.dev;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<const void*>()(k.ptr) ^ ((size_t)k.rows << 1) ^ ((size_t)k.k << 21) ^
+           ((size_t)k.bn << 41) ^ ((size_t)k.dev << 50);
+  }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// Weights [rows][k] bf16, k contiguous; box = 64 (k) x bn (rows), 128B swizzle,
+// rows past the end read as zeros.
+int weight_map(const void* w, int rows, int k, int bn, CUtensorMap* out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  MapKey key{w, rows, k, bn, dev};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return LAUD_OK;
+    }
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(LAUD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(w) & 15) != 0)
+    return fail(LAUD_ERR_ARG, "weight pointer must be 16-byte aligned");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)bn};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LAUD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    g_maps[key] = m;
+  }
+  *out = m;
+  return LAUD_OK;
+}
+
+int pick_bn(int n_out) {
+  if (n_out >= 256) return 256;
+  if (n_out > 64) return 128;
+  return 64;
+}
+
+int run_conv(const laud_conv_args* a, cudaStream_t st) {
+  if (!a || !a->act || !a->weight || !a->out) return fail(LAUD_ERR_ARG, "null pointer in conv args");
+  if (a->in_c % 8 || a->in_ld % 8 || a->in_ld < a->in_c)
+    return fail(LAUD_ERR_SHAPE, "in_c (%d) and in_ld (%d) must be multiples of 8, ld >= c", a->in_c,
+                a->in_ld);
+  if (a->n_out % 8 || a->out_ld % 8 || a->n_out < 8)
+    return fail(LAUD_ERR_SHAPE, "n_out (%d) / out_ld (%d) must be multiples of 8", a->n_out,
+                a->out_ld);
+  if (a->ksize < 1 || a->ksize % 2 == 0) return fail(LAUD_ERR_ARG, "ksize must be odd");
+  if (a->a_compact && a->ksize != 1) return fail(LAUD_ERR_ARG, "compact A needs a 1x1 kernel");
+  if (a->row_mode != ROWS_DENSE && !a->list)
+    return fail(LAUD_ERR_ARG, "row list required for patch/pixel rows");
+  if (a->row_mode == ROWS_PATCH && (a->patch_h < 1 || a->patch_w < 1))
+    return fail(LAUD_ERR_GRANULARITY, "patch size must be positive");
+  if (a->rows_max <= 0) return LAUD_OK;
+  ConvParams p;
+  memset(&p, 0, sizeof(p));
+  p.row_mode = a->row_mode;
+  p.list = a->list;
+  p.count = a->count;
+  p.rows_max = a->rows_max;
+  p.batch = a->batch;
+  p.out_h = a->out_h;
+  p.out_w = a->out_w;
+  p.patch_h = a->patch_h > 0 ? a->patch_h : 1;
+  p.patch_w = a->patch_w > 0 ? a->patch_w : 1;
+  p.cells_h = a->cells_h > 0 ? a->cells_h : 1;
+  p.cells_w = a->cells_w > 0 ? a->cells_w : 1;
+  p.act = a->act;
+  p.in_h = a->in_h;
+  p.in_w = a->in_w;
+  p.in_c = a->in_c;
+  p.in_ld = a->in_ld;
+  p.a_compact = a->a_compact;
+  p.ksize = a->ksize;
+  p.stride = a->stride;
+  p.pad = a->pad;
+  p.kpad = round_up(a->in_c, 64);
+  p.num_kb = a->ksize * a->ksize * p.kpad / 64;
+  p.n_out = a->n_out;
+  p.scale = a->scale;
+  p.bias = a->bias;
+  p.relu = a->relu;
+  p.out_mode = a->out_mode;
+  p.out = a->out;
+  p.out_ld = a->out_ld;
+  p.out_f32 = a->out_f32;
+  p.resid = a->resid;
+  p.resid_ld = a->resid_ld;
+  p.relu_inactive_coarse = a->relu_inactive_coarse;
+  p.ymask_coarse = a->ymask_coarse;
+  p.ymask_channel = a->ymask_channel;
+  p.misplace_first = a->misplace_first;
+  const int bn = pick_bn(a->n_out);
+  CUtensorMap m;
+  int rc = weight_map(a->weight, a->n_out, a->ksize * a->ksize * p.kpad, bn, &m);
+  if (rc) return rc;
+  return cuda_check(launch_conv_gemm(m, bn, p, num_sms(), st), "conv_gemm launch", 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* laud_version(void) { return "laud-b200 0.1.0 (sm_100a, tcgen05)"; }
+const char* laud_last_error(void) { return g_err.c_str(); }
+uint64_t laud_launch_count(void) { return g_launches.load(); }
+
+size_t laud_scan_workspace_bytes(int items) { return scan_state_bytes(items > 0 ? items : 1); }
+
+size_t laud_masker_partial_floats(int n, int h, int w, int c, int s, int stride) {
+  const int win = s * stride;
+  if (win <= 0 || h % win || w % win) return 0;
+  int cps = 0;
+  const int splits = masker_splits(win, c, &cps);
+  return (size_t)n * (h / win) * (w / win) * splits;
+}
+
+int laud_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c, int s,
+                        int stride, const float* wdiff, float bias, uint8_t* coarse,
+                        int* cell_list, int* cell_count, float* partial, void* scan,
+                        void* stream) {
+  if (s < 1 || stride < 1) return fail(LAUD_ERR_ARG, "granularity and stride must be positive");
+  const int win = s * stride;
+  if (h % win || w % win)
+    return fail(LAUD_ERR_GRANULARITY, "S=%d (window %d) does not divide %dx%d", s, win, h, w);
+  if (c % 8 || ld % 8 || ld < c) return fail(LAUD_ERR_SHAPE, "channels must be multiples of 8");
+  if (c > 12288) return fail(LAUD_ERR_SHAPE, "masker supports at most 12288 channels");
+  return cuda_check(launch_spatial_masker(x, x_f32, ld, n, h, w, c, s, stride, wdiff, bias, coarse,
+                                          cell_list, cell_count, partial, scan,
+                                          (cudaStream_t)stream),
+                    "spatial masker", 2);
+}
+
+int laud_cells_from_mask(const uint8_t* coarse, int cells, int* cell_list, int* cell_count,
+                         void* scan, void* stream) {
+  return cuda_check(
+      launch_list_from_mask(coarse, cells, cell_list, cell_count, scan, (cudaStream_t)stream),
+      "cells from mask", 1);
+}
+
+int laud_dilate_pixels(const uint8_t* coarse, int n, int h_in, int w_in, int s, int stride,
+                       int radius, int* pix_list, int* pix_count, void* scan, void* stream) {
+  const int win = s * stride;
+  if (s < 1 || stride < 1 || h_in % win || w_in % win)
+    return fail(LAUD_ERR_GRANULARITY, "S=%d does not divide the output grid", s);
+  if (radius < 0) return fail(LAUD_ERR_ARG, "radius must be >= 0");
+  return cuda_check(launch_dilate_pixels(coarse, n, h_in, w_in, s, stride, h_in / win, w_in / win,
+                                         radius, pix_list, pix_count, scan, (cudaStream_t)stream),
+                    "dilate pixels", 1);
+}
+
+int laud_conv(const laud_conv_args* a, void* stream) { return run_conv(a, (cudaStream_t)stream); }
+
+int laud_block_forward(const laud_block_args* a, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!a || !a->x || !a->out || !a->w1 || !a->w2 || !a->w3)
+    return fail(LAUD_ERR_ARG, "null pointer in block args");
+  if (a->paradigm == LAUD_PARADIGM_CHANNEL)
+    return fail(LAUD_ERR_UNSUPPORTED, "channel paradigm uses laud_channel_block");
+  if (a->groups != 1) return fail(LAUD_ERR_UNSUPPORTED, "grouped conv2 not supported yet");
+  if (a->stride != 1 && a->stride != 2) return fail(LAUD_ERR_ARG, "stride must be 1 or 2");
+  if (a->stride > 1 && !a->has_down)
+    return fail(LAUD_ERR_SHAPE, "a strided block needs a downsample path");
+  if (a->has_down && !a->wd) return fail(LAUD_ERR_ARG, "downsample weights missing");
+  const int ho = (a->h_in - 1) / a->stride + 1, wo = (a->w_in - 1) / a->stride + 1;
+  if (!a->has_down && (a->c_in != a->c_out || a->x_ld != a->c_out))
+    return fail(LAUD_ERR_SHAPE, "identity skip needs c_in == c_out == x_ld");
+  const int n = a->n;
+  int rc;
+
+  // ---------------------------------------------------------------- rows
+  int pm;  // row mode for conv2/conv3
+  int ph = 1, pw = 1, ch = 1, cw = 1;
+  const int* cells = nullptr;
+  const int* cells_n = nullptr;
+  const uint8_t* coarse = nullptr;
+  if (a->paradigm == LAUD_PARADIGM_SPATIAL || a->paradigm == LAUD_PARADIGM_LAYER) {
+    if (a->paradigm == LAUD_PARADIGM_SPATIAL) {
+      if (a->s < 1 || ho % a->s || wo % a->s)
+        return fail(LAUD_ERR_GRANULARITY, "S=%d does not divide %dx%d", a->s, ho, wo);
+      ph = pw = a->s;
+    } else {
+      ph = ho;
+      pw = wo;
+    }
+    ch = ho / ph;
+    cw = wo / pw;
+    if (!a->cell_list || !a->cell_count || !a->scan)
+      return fail(LAUD_ERR_ARG, "cell list / scan workspace missing");
+    if (a->given_coarse) {
+      coarse = a->given_coarse;
+      rc = laud_cells_from_mask(coarse, n * ch * cw, a->cell_list, a->cell_count, a->scan, stream);
+    } else {
+      if (!a->masker_wdiff || !a->coarse_out || !a->partial)
+        return fail(LAUD_ERR_ARG, "masker weights / coarse output / partials missing");
+      if (a->paradigm == LAUD_PARADIGM_LAYER && a->h_in != a->w_in)
+        return fail(LAUD_ERR_GRANULARITY, "layer masker needs a square feature");
+      coarse = a->coarse_out;
+      rc = laud_spatial_masker(a->x, 0, a->x_ld, n, a->h_in, a->w_in, a->c_in,
+                               a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
+                               a->masker_wdiff, a->masker_bias, a->coarse_out, a->cell_list,
+                               a->cell_count, a->partial, a->scan, stream);
+    }
+    if (rc) return rc;
+    cells = a->cell_list;
+    cells_n = a->cell_count;
+    pm = ROWS_PATCH;
+  } else if (a->paradigm == LAUD_PARADIGM_STATIC) {
+    pm = ROWS_DENSE;
+  } else {
+    return fail(LAUD_ERR_ARG, "unknown paradigm %d", a->paradigm);
+  }
+
+  // ---------------------------------------------------------------- skip path
+  if (a->has_down) {
+    laud_conv_args d;
+    memset(&d, 0, sizeof(d));
+    d.row_mode = ROWS_DENSE;
+    d.rows_max = n * ho * wo;
+    d.batch = n;
+    d.out_h = ho;
+    d.out_w = wo;
+    d.patch_h = ph;
+    d.patch_w = pw;
+    d.cells_h = ch;
+    d.cells_w = cw;
+    d.act = a->x;
+    d.in_h = a->h_in;
+    d.in_w = a->w_in;
+    d.in_c = a->c_in;
+    d.in_ld = a->x_ld;
+    d.ksize = 1;
+    d.stride = a->stride;
+    d.pad = 0;
+    d.weight = a->wd;
+    d.n_out = a->c_out;
+    d.scale = a->sd;
+    d.bias = a->bd;
+    d.out_mode = OUT_PIXEL;
+    d.out = a->out;
+    d.out_ld = a->c_out;
+    if (a->relu_out) {
+      if (pm == ROWS_DENSE) {
+        d.relu = 0;  // the conv3 epilogue applies the ReLU after the residual add
+      } else {
+        d.relu = 1;
+        d.relu_inactive_coarse = coarse;
+      }
+    }
+    if ((rc = run_conv(&d, st))) return rc;
+  } else if (a->out != a->x) {
+    if ((rc = cuda_check(cudaMemcpyAsync(a->out, a->x, (size_t)n * ho * wo * a->c_out * 2,
+                                         cudaMemcpyDeviceToDevice, st),
+                         "skip copy", 0)))
+      return rc;
+  }
+
+  // ---------------------------------------------------------------- conv1
+  laud_conv_args c1;
+  memset(&c1, 0, sizeof(c1));
+  c1.batch = n;
+  c1.out_h = a->h_in;
+  c1.out_w = a->w_in;
+  c1.act = a->x;
+  c1.in_h = a->h_in;
+  c1.in_w = a->w_in;
+  c1.in_c = a->c_in;
+  c1.in_ld = a->x_ld;
+  c1.ksize = 1;
+  c1.stride = 1;
+  c1.weight = a->w1;
+  c1.n_out = a->c_mid;
+  c1.scale = a->s1;
+  c1.bias = a->b1;
+  c1.relu = a->relu1;
+  c1.out_mode = OUT_PIXEL;
+  c1.out = a->h1;
+  c1.out_ld = a->c_mid;
+  c1.rows_max = n * a->h_in * a->w_in;
+  if (pm == ROWS_DENSE) {
+    c1.row_mode = ROWS_DENSE;
+  } else if (a->paradigm == LAUD_PARADIGM_LAYER) {
+    c1.row_mode = ROWS_PATCH;  // whole images of the active samples
+    c1.list = cells;
+    c1.count = cells_n;
+    c1.patch_h = a->h_in;
+    c1.patch_w = a->w_in;
+    c1.cells_h = 1;
+    c1.cells_w = 1;
+  } else {
+    if (!a->pix_list || !a->pix_count) return fail(LAUD_ERR_ARG, "pixel list workspace missing");
+    if ((rc = laud_dilate_pixels(coarse, n, a->h_in, a->w_in, a->s, a->stride, 1, a->pix_list,
+                                 a->pix_count, a->scan, stream)))
+      return rc;
+    c1.row_mode = ROWS_PIXEL;
+    c1.list = a->pix_list;
+    c1.count = a->pix_count;
+  }
+  if ((rc = run_conv(&c1, st))) return rc;
+
+  // ---------------------------------------------------------------- conv2 (3x3 over patches)
+  laud_conv_args c2;
+  memset(&c2, 0, sizeof(c2));
+  c2.row_mode = pm;
+  c2.list = cells;
+  c2.count = cells_n;
+  c2.rows_max = n * ho * wo;
+  c2.batch = n;
+  c2.out_h = ho;
+  c2.out_w = wo;
+  c2.patch_h = ph;
+  c2.patch_w = pw;
+  c2.cells_h = ch;
+  c2.cells_w = cw;
+  c2.act = a->h1;
+  c2.in_h = a->h_in;
+  c2.in_w = a->w_in;
+  c2.in_c = a->c_mid;
+  c2.in_ld = a->c_mid;
+  c2.ksize = 3;
+  c2.stride = a->stride;
+  c2.pad = 1;
+  c2.weight = a->w2;
+  c2.n_out = a->c_mid;
+  c2.scale = a->s2;
+  c2.bias = a->b2;
+  c2.relu = a->relu2;
+  c2.out_mode = OUT_ROW;
+  c2.out = a->h2;
+  c2.out_ld = a->c_mid;
+  if ((rc = run_conv(&c2, st))) return rc;
+
+  // ---------------------------------------------------------------- conv3 + scatter-add
+  laud_conv_args c3 = c2;
+  c3.act = a->h2;
+  c3.in_h = ho;
+  c3.in_w = wo;
+  c3.a_compact = 1;
+  c3.ksize = 1;
+  c3.stride = 1;
+  c3.pad = 0;
+  c3.weight = a->w3;
+  c3.n_out = a->c_out;
+  c3.scale = a->s3;
+  c3.bias = a->b3;
+  c3.relu = a->relu_out;
+  c3.out_mode = OUT_PIXEL;
+  c3.out = a->out;
+  c3.out_ld = a->c_out;
+  c3.resid = a->out;
+  c3.resid_ld = a->c_out;
+  c3.misplace_first = a->misplace_first;
+  return run_conv(&c3, st);
+}
+
+int laud_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride, int pad,
+                     const float* mean, const float* inv_std, void* cols, int cols_ld,
+                     void* stream) {
+  if (cols_ld < k * k * 3 || cols_ld % 8) return fail(LAUD_ERR_SHAPE, "bad im2col leading dim");
+  return cuda_check(launch_stem_im2col(img, n, h, w, k, stride, pad, mean, inv_std, cols, cols_ld,
+                                       (cudaStream_t)stream),
+                    "stem im2col", 1);
+}
+
+int laud_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, void* stream) {
+  if (c % 8) return fail(LAUD_ERR_SHAPE, "channels must be a multiple of 8");
+  return cuda_check(launch_maxpool3s2(x, n, h, w, c, y, (cudaStream_t)stream), "maxpool", 1);
+}
+
+int laud_global_avgpool(const void* x, int n, int hw, int c, void* y, void* stream) {
+  return cuda_check(launch_gap(x, n, hw, c, y, (cudaStream_t)stream), "global avgpool", 1);
+}
+
+}  // extern "C"

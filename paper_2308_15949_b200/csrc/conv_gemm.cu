@@ -1,0 +1,366 @@
+// Implicit-GEMM convolution engine on tcgen05 / TMEM / TMA (sm_100a).
+//
+// Persistent, warp-specialised kernel (320 threads, 1 CTA per SM):
+//   warps 0-3  A producers: gather 128 output-pixel rows x 64 channels of the
+//              activation for one (tap, channel-block) with cp.async (16 B per
+//              lane, zero-fill outside the image / list), written in the UMMA
+//              K-major 128B-swizzled layout;
+//   warp  8    B producer: one TMA tile load of the packed weights per stage;
+//   warp  9    MMA issuer: 4 x tcgen05.mma (128xBNx16) per stage into one of two
+//              TMEM accumulators; owns TMEM alloc/dealloc;
+//   warps 4-7  epilogue: tcgen05.ld -> scale/bias (folded BN) -> +residual ->
+//              ReLU -> bf16 store to the row's destination pixel (scatter) or
+//              compact row.  Double-buffered TMEM lets the epilogue of tile i
+//              overlap the mainloop of tile i+1.
+// Row enumeration (dense grid / active-patch list / pixel list) and the
+// device-side row count make the same kernel serve the gather-conv1,
+// patch conv2 (3x3, halo via zero-filled gathers) and conv3+scatter-add steps
+// of LAUDNet's schedule (reference semantics: `reference.py:378-403`).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "laud_conv.cuh"
+#include "laud_ptx.cuh"
+
+namespace laud {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
+constexpr int NUM_THREADS = 320;
+
+struct RowPos {
+  int n, y, x;
+};
+
+__device__ __forceinline__ int rows_valid(const ConvParams& p) {
+  if (p.row_mode == ROWS_DENSE || p.count == nullptr) return p.rows_max;
+  int c = __ldg(p.count);
+  long long r = (p.row_mode == ROWS_PATCH) ? (long long)c * p.patch_h * p.patch_w : (long long)c;
+  return r < p.rows_max ? (int)r : p.rows_max;
+}
+
+// Output pixel of row m; false when the row is past the valid count.
+__device__ __forceinline__ bool map_row(const ConvParams& p, int m, int nvalid, RowPos& o,
+                                        bool& first_patch) {
+  first_patch = false;
+  if (m >= nvalid) return false;
+  int hw = p.out_h * p.out_w;
+  if (p.row_mode == ROWS_PATCH) {
+    int s2 = p.patch_h * p.patch_w;
+    int pi = m / s2;
+    int l = m - pi * s2;
+    int cell = __ldg(p.list + pi);
+    int cpi = p.cells_h * p.cells_w;
+    o.n = cell / cpi;
+    int c = cell - o.n * cpi;
+    int ci = c / p.cells_w;
+    int cj = c - ci * p.cells_w;
+    int ly = l / p.patch_w;
+    o.y = ci * p.patch_h + ly;
+    o.x = cj * p.patch_w + (l - ly * p.patch_w);
+    first_patch = (pi == 0);
+    return true;
+  }
+  int pix = (p.row_mode == ROWS_PIXEL) ? __ldg(p.list + m) : m;
+  o.n = pix / hw;
+  int r = pix - o.n * hw;
+  o.y = r / p.out_w;
+  o.x = r - o.y * p.out_w;
+  return true;
+}
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int A_OFF = 0;
+  static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
+  static constexpr int BAR_OFF = B_OFF + STAGES * B_STAGE_BYTES;
+  static constexpr int NUM_BARS = 2 * STAGES + 4;
+  static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
+  static constexpr int BYTES = TMEM_SLOT_OFF + 16;
+  static constexpr int ALLOC = BYTES + 1024;  // manual 1 KiB alignment
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    conv_gemm_kernel(const __grid_constant__ CUtensorMap tmap_b, const ConvParams p) {
+  using L = Smem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  const uint32_t base_u32 = (raw_u32 + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_u32 - raw_u32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* acc_full = bars + 2 * STAGES;
+  uint64_t* acc_empty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::TMEM_SLOT_OFF);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvalid = rows_valid(p);
+  const int n_tiles = (p.n_out + BN - 1) / BN;
+  const int m_tiles = (nvalid + BM - 1) / BM;
+  const int tiles = m_tiles * n_tiles;
+  if ((int)blockIdx.x >= tiles) return;  // uniform for the whole CTA
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 128 + 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 8 && lane == 0) tma_prefetch_desc(&tmap_b);
+  if (warp == 9) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kpt = p.kpad / BK;  // k-blocks per tap
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ A producers
+    const int tid = threadIdx.x;
+    const int chunk = tid & 7;
+    const int rsub = tid >> 3;
+    const __nv_bfloat16* act = reinterpret_cast<const __nv_bfloat16*>(p.act);
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t / n_tiles) * BM;
+      RowPos rp[8];
+      bool rv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        bool fp;
+        rv[i] = map_row(p, m0 + rsub + 16 * i, nvalid, rp[i], fp);
+      }
+      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        const int stage = it % STAGES;
+        const uint32_t phase = (it / STAGES) & 1;
+        mbar_wait(&empty[stage], phase ^ 1);
+        const int tap = kb / kpt;
+        const int ch = (kb - tap * kpt) * BK + chunk * 8;
+        const int ky = tap / p.ksize;
+        const int kx = tap - ky * p.ksize;
+        const bool chv = ch < p.in_c;
+        const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = rsub + 16 * i;
+          const uint32_t dst = sA + r * 128 + ((chunk ^ (r & 7)) << 4);
+          bool v = rv[i] && chv;
+          const __nv_bfloat16* src = act;
+          if (p.a_compact) {
+            src = act + (size_t)(m0 + r) * p.in_ld + ch;
+          } else {
+            const int iy = rp[i].y * p.stride + ky - p.pad;
+            const int ix = rp[i].x * p.stride + kx - p.pad;
+            v = v && iy >= 0 && iy < p.in_h && ix >= 0 && ix < p.in_w;
+            src = act + ((size_t)(rp[i].n * p.in_h + iy) * p.in_w + ix) * p.in_ld + ch;
+          }
+          cp_async_16(dst, v ? (const void*)src : (const void*)act, v ? 16u : 0u);
+        }
+        cp_async_mbar_arrive_noinc(&full[stage]);
+      }
+    }
+  } else if (warp == 8) {
+    // ------------------------------------------------------------ B producer (TMA)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int n0 = (t % n_tiles) * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], L::B_STAGE_BYTES);
+          tma_load_2d(base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES, &tmap_b, &full[stage],
+                      kb * BK, n0);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    uint32_t it = 0, local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        const int stage = it % STAGES;
+        const uint32_t phase = (it / STAGES) & 1;
+        mbar_wait(&full[stage], phase);
+        fence_proxy_async_smem();
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
+          const uint32_t sB = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_bf16(tmem_d, umma_sdesc_sw128(sA + k * 32), umma_sdesc_sw128(sB + k * 32), idesc,
+                      (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) umma_commit(&acc_full[acc]);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 4-7)
+    const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+    uint32_t local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const int m0 = (t / n_tiles) * BM;
+      const int n0 = (t % n_tiles) * BN;
+      RowPos rp;
+      bool fp;
+      const int m = m0 + ew * 32 + lane;
+      const bool valid = map_row(p, m, nvalid, rp, fp);
+      size_t dst_row = 0;
+      if (valid) {
+        if (p.out_mode == OUT_ROW) {
+          dst_row = (size_t)m;
+        } else {
+          int y = rp.y;
+          if (p.misplace_first && fp) y = (y + p.patch_h) % p.out_h;
+          dst_row = (size_t)(rp.n * p.out_h + y) * p.out_w + rp.x;
+        }
+      }
+      bool do_relu = p.relu != 0;
+      float ymul = 1.f;
+      if (valid && (p.relu_inactive_coarse || p.ymask_coarse)) {
+        const int cell = (rp.n * p.cells_h + rp.y / p.patch_h) * p.cells_w + rp.x / p.patch_w;
+        if (p.relu_inactive_coarse) do_relu = p.relu_inactive_coarse[cell] == 0;
+        if (p.ymask_coarse) ymul = p.ymask_coarse[cell] ? 1.f : 0.f;
+      }
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        const int c0 = n0 + j * 32;
+        if (c0 >= p.n_out) break;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + j * 32, r);
+        if (!valid) continue;
+        float v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int cg = c0 + g * 8;
+          if (cg >= p.n_out) break;
+          if (p.scale) {
+            const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + cg));
+            const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + cg + 4));
+            v[g * 8 + 0] *= s0.x; v[g * 8 + 1] *= s0.y; v[g * 8 + 2] *= s0.z; v[g * 8 + 3] *= s0.w;
+            v[g * 8 + 4] *= s1.x; v[g * 8 + 5] *= s1.y; v[g * 8 + 6] *= s1.z; v[g * 8 + 7] *= s1.w;
+          }
+          if (p.bias) {
+            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + cg));
+            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + cg + 4));
+            v[g * 8 + 0] += b0.x; v[g * 8 + 1] += b0.y; v[g * 8 + 2] += b0.z; v[g * 8 + 3] += b0.w;
+            v[g * 8 + 4] += b1.x; v[g * 8 + 5] += b1.y; v[g * 8 + 6] += b1.z; v[g * 8 + 7] += b1.w;
+          }
+          if (p.ymask_channel) {
+            const uint2 mk = __ldg(reinterpret_cast<const uint2*>(
+                p.ymask_channel + (size_t)rp.n * p.n_out + cg));
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              v[g * 8 + q] *= ((q < 4 ? (mk.x >> (8 * q)) : (mk.y >> (8 * (q - 4)))) & 0xff) ? 1.f : 0.f;
+          }
+          if (ymul != 1.f) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[g * 8 + q] *= ymul;
+          }
+          if (p.resid) {
+            const uint4 rr = __ldg(reinterpret_cast<const uint4*>(
+                reinterpret_cast<const __nv_bfloat16*>(p.resid) + dst_row * p.resid_ld + cg));
+            float2 f;
+            f = unpack_bf16x2(rr.x); v[g * 8 + 0] += f.x; v[g * 8 + 1] += f.y;
+            f = unpack_bf16x2(rr.y); v[g * 8 + 2] += f.x; v[g * 8 + 3] += f.y;
+            f = unpack_bf16x2(rr.z); v[g * 8 + 4] += f.x; v[g * 8 + 5] += f.y;
+            f = unpack_bf16x2(rr.w); v[g * 8 + 6] += f.x; v[g * 8 + 7] += f.y;
+          }
+          if (do_relu) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[g * 8 + q] = fmaxf(v[g * 8 + q], 0.f);
+          }
+          if (p.out_f32) {
+            float* o = reinterpret_cast<float*>(p.out) + dst_row * p.out_ld + cg;
+            reinterpret_cast<float4*>(o)[0] =
+                make_float4(v[g * 8 + 0], v[g * 8 + 1], v[g * 8 + 2], v[g * 8 + 3]);
+            reinterpret_cast<float4*>(o)[1] =
+                make_float4(v[g * 8 + 4], v[g * 8 + 5], v[g * 8 + 6], v[g * 8 + 7]);
+          } else {
+            uint4 w;
+            w.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
+            w.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
+            w.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
+            w.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) +
+                                      dst_row * p.out_ld + cg) = w;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+template <int BN, int STAGES>
+static cudaError_t launch_bn(const CUtensorMap& tmap, const ConvParams& p, int tiles_max,
+                             int num_sms, cudaStream_t stream) {
+  using L = Smem<BN, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int grid = tiles_max < num_sms ? tiles_max : num_sms;
+  if (grid < 1) grid = 1;
+  conv_gemm_kernel<BN, STAGES><<<grid, NUM_THREADS, L::ALLOC, stream>>>(tmap, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_gemm(const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
+                             cudaStream_t stream) {
+  const int n_tiles = (p.n_out + bn - 1) / bn;
+  const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
+  switch (bn) {
+    case 64: return launch_bn<64, 8>(tmap, p, tiles_max, num_sms, stream);
+    case 128: return launch_bn<128, 6>(tmap, p, tiles_max, num_sms, stream);
+    case 256: return launch_bn<256, 4>(tmap, p, tiles_max, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace laud

@@ -1,0 +1,62 @@
+// Parameter block of the implicit-GEMM convolution engine (conv_gemm.cu).
+//
+// One engine covers every convolution of the LAUDNet block path:
+//   rows    m  = output pixels, enumerated densely, from a patch list
+//               (m = p*S*S + local), or from a pixel list;
+//   A[m, k] = act[input pixel of (row m, tap t)][channel c], k = t*Kpad + c,
+//             gathered by cp.async with zero fill outside the image;
+//   B[n, k] = packed weights [Cout][taps][Kpad] (TMA, 128B swizzle);
+//   D       = tcgen05 fp32 accumulator in TMEM, epilogue: scale/bias/ReLU,
+//             optional residual add, bf16 (or fp32) store to the row's
+//             destination (scattered pixel or compact row).
+#pragma once
+#include <cstdint>
+
+namespace laud {
+
+enum RowMode : int { ROWS_DENSE = 0, ROWS_PATCH = 1, ROWS_PIXEL = 2 };
+enum OutMode : int { OUT_PIXEL = 0, OUT_ROW = 1 };
+
+struct ConvParams {
+  // ---- rows (output pixels)
+  int row_mode;          // RowMode
+  const int* list;       // patch list (cell index) or pixel list (pixel index)
+  const int* count;      // device count of list entries; nullptr -> use rows_max
+  int rows_max;          // upper bound on rows (grid sizing)
+  int batch;             // N
+  int out_h, out_w;      // output grid
+  int patch_h, patch_w;  // S x S patch (ROWS_PATCH); H x W of the image in layer mode
+  int cells_h, cells_w;  // out_h/patch_h, out_w/patch_w
+  // ---- A operand
+  const void* act;       // bf16 NHWC input
+  int in_h, in_w;        // input grid
+  int in_c;              // valid channels (multiple of 8)
+  int in_ld;             // elements per pixel row (>= in_c, multiple of 8)
+  int a_compact;         // 1: A row = m directly (1x1, taps must be 1)
+  int ksize, stride, pad;
+  int kpad;              // in_c rounded up to 64
+  int num_kb;            // ksize*ksize*kpad/64
+  // ---- output
+  int n_out;             // output channels (multiple of 8)
+  const float* scale;    // per-channel, nullable
+  const float* bias;     // per-channel, nullable
+  int relu;              // ReLU after scale/bias (and after residual add if resid)
+  int out_mode;          // OutMode
+  void* out;             // bf16 (or fp32 when out_f32) destination
+  int out_ld;            // elements per destination row
+  int out_f32;           // store fp32 instead of bf16
+  const void* resid;     // bf16 residual (read at the destination pixel), nullable
+  int resid_ld;
+  // ---- ReLU only where the destination pixel's cell is inactive (skip path of
+  //      a downsample block under a spatial mask): coarse[cell] == 0 -> ReLU.
+  const unsigned char* relu_inactive_coarse;
+  // ---- dense-masked (training-style) semantics, `reference.py:313-353`:
+  //      y *= coarse[cell of the destination pixel]   (spatial / layer), and
+  //      y *= chmask[n][channel]                      (channel, per sample).
+  const unsigned char* ymask_coarse;
+  const unsigned char* ymask_channel;
+  // ---- fault hook (tests only): shift the first patch's destination one cell
+  int misplace_first;
+};
+
+}  // namespace laud

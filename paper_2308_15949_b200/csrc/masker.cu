@@ -1,0 +1,298 @@
+// Spatial / layer masker and stable stream compaction (sm_100a).
+//
+// K1a cell_dot_kernel   d[cell] partials = sum over the cell's (stride*S)^2 input
+//                       pixels of x . (W0 - W1)  — the fused-masker identity of
+//                       `reference.py:244-253` applied to the pooled 1x1 conv of
+//                       `reference.py:173-174`.  128-bit NHWC loads, one warp per
+//                       (cell, split) work item, deterministic split partials.
+// K1b compact_kernel    decision = mean(d) + bias >= 0 (compute wins ties,
+//                       `reference.py:183`), then a warp-ballot/shuffle block scan
+//                       and decoupled look-back across CTAs to emit the active
+//                       cell indices in row-major order — identical to
+//                       `np.argwhere` in `build_gather_plan` (`reference.py:133-135`)
+//                       — plus the device-side count (no host sync).
+// The same compaction core emits the conv1 pixel set (union of the active
+// patches' 3x3 halo windows on the input grid) and lists from given masks.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "laud_ptx.cuh"
+
+namespace laud {
+
+constexpr int CT_THREADS = 256;
+constexpr int CT_ITEMS = 4;
+constexpr int CT_TILE = CT_THREADS * CT_ITEMS;  // 1024 items per CTA
+
+// Look-back scratch; zero at allocation, restored to zero by the last CTA.
+struct ScanState {
+  unsigned int tile_ctr;
+  unsigned int done_ctr;
+  unsigned int pad[2];
+  unsigned long long tiles[1];  // [num_tiles]
+};
+
+constexpr unsigned long long FLAG_AGG = 1ull << 32;
+constexpr unsigned long long FLAG_INC = 2ull << 32;
+
+// ---------------------------------------------------------------------------
+// K1a: per (cell, split) partial dot products
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ float dot8(const T* p, const float* w);
+template <>
+__device__ __forceinline__ float dot8<__nv_bfloat16>(const __nv_bfloat16* p, const float* w) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  float a = 0.f;
+  float2 f;
+  f = unpack_bf16x2(v.x); a = fmaf(f.x, w[0], a); a = fmaf(f.y, w[1], a);
+  f = unpack_bf16x2(v.y); a = fmaf(f.x, w[2], a); a = fmaf(f.y, w[3], a);
+  f = unpack_bf16x2(v.z); a = fmaf(f.x, w[4], a); a = fmaf(f.y, w[5], a);
+  f = unpack_bf16x2(v.w); a = fmaf(f.x, w[6], a); a = fmaf(f.y, w[7], a);
+  return a;
+}
+template <>
+__device__ __forceinline__ float dot8<float>(const float* p, const float* w) {
+  const float4 u = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  float a = 0.f;
+  a = fmaf(u.x, w[0], a); a = fmaf(u.y, w[1], a); a = fmaf(u.z, w[2], a); a = fmaf(u.w, w[3], a);
+  a = fmaf(v.x, w[4], a); a = fmaf(v.y, w[5], a); a = fmaf(v.z, w[6], a); a = fmaf(v.w, w[7], a);
+  return a;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) cell_dot_kernel(
+    const T* __restrict__ x, int ld, int n, int h, int w, int c, int win, int cells_h,
+    int cells_w, const float* __restrict__ wdiff, int splits, int chunks_per_split,
+    float* __restrict__ partial) {
+  extern __shared__ float s_w[];
+  for (int i = threadIdx.x; i < c; i += blockDim.x) s_w[i] = wdiff[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cpp = c >> 3;  // 8-channel chunks per pixel
+  const int cell_chunks = win * win * cpp;
+  const long long items = (long long)n * cells_h * cells_w * splits;
+  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= items) return;
+  const int cell = (int)(item / splits);
+  const int split = (int)(item - (long long)cell * splits);
+  const int cpi = cells_h * cells_w;
+  const int ni = cell / cpi;
+  const int cr = cell - ni * cpi;
+  const int ci = cr / cells_w, cj = cr - (cr / cells_w) * cells_w;
+  const int q0 = split * chunks_per_split;
+  const int q1 = min(q0 + chunks_per_split, cell_chunks);
+  float acc = 0.f;
+#pragma unroll 4
+  for (int q = q0 + lane; q < q1; q += 32) {
+    const int px = q / cpp;
+    const int ch = (q - px * cpp) << 3;
+    const int py = px / win;
+    const int pxx = px - py * win;
+    const int yy = ci * win + py, xx = cj * win + pxx;
+    acc += dot8<T>(x + ((size_t)(ni * h + yy) * w + xx) * ld + ch, s_w + ch);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) partial[item] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// flag sources for the compaction core
+// ---------------------------------------------------------------------------
+struct MaskerFlag {  // decision from split partials; also materialises coarse
+  const float* partial;
+  int splits;
+  float inv_area, bias;
+  uint8_t* coarse;
+  __device__ bool operator()(int i) const {
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += partial[(size_t)i * splits + k];
+    const bool f = s * inv_area + bias >= 0.f;
+    if (coarse) coarse[i] = f ? 1 : 0;
+    return f;
+  }
+};
+
+struct GivenFlag {  // list from a caller-supplied coarse mask
+  const uint8_t* coarse;
+  __device__ bool operator()(int i) const { return coarse[i] != 0; }
+};
+
+// conv1 work set: input pixel needed iff an active cell's conv2 input window
+// [ci*S*st - 1, ci*S*st + (S-1)*st + 1] (rows and cols) covers it.
+struct DilateFlag {
+  const uint8_t* coarse;
+  int h, w, s, st, cells_h, cells_w, radius;
+  __device__ bool operator()(int i) const {
+    const int hw = h * w;
+    const int ni = i / hw;
+    const int r = i - ni * hw;
+    const int y = r / w, xx = r - (r / w) * w;
+    const int ss = s * st;
+    const int span = (s - 1) * st + radius;  // window: [ci*ss - radius, ci*ss + span]
+    int ci0 = y - span;
+    ci0 = ci0 <= 0 ? 0 : (ci0 + ss - 1) / ss;
+    int ci1 = min((y + radius) / ss, cells_h - 1);
+    int cj0 = xx - span;
+    cj0 = cj0 <= 0 ? 0 : (cj0 + ss - 1) / ss;
+    int cj1 = min((xx + radius) / ss, cells_w - 1);
+    const uint8_t* cm = coarse + (size_t)ni * cells_h * cells_w;
+    for (int ci = ci0; ci <= ci1; ++ci)
+      for (int cj = cj0; cj <= cj1; ++cj)
+        if (cm[ci * cells_w + cj]) return true;
+    return false;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K1b: stable compaction with decoupled look-back
+// ---------------------------------------------------------------------------
+template <class Flag>
+__global__ void __launch_bounds__(CT_THREADS) compact_kernel(Flag flag, int total,
+                                                             int* __restrict__ list,
+                                                             int* __restrict__ count,
+                                                             ScanState* st, int num_tiles) {
+  __shared__ int s_tile;
+  __shared__ int s_warp[CT_THREADS / 32];
+  __shared__ int s_excl;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(&st->tile_ctr, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const int base = tile * CT_TILE + threadIdx.x * CT_ITEMS;
+  bool f[CT_ITEMS];
+  int cnt = 0;
+#pragma unroll
+  for (int j = 0; j < CT_ITEMS; ++j) {
+    f[j] = (base + j < total) ? flag(base + j) : false;
+    cnt += f[j];
+  }
+  // block-wide exclusive scan of per-thread counts
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < CT_THREADS / 32 ? s_warp[lane] : 0;
+    int wi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    if (lane < CT_THREADS / 32) s_warp[lane] = wi - v;  // exclusive warp offsets
+    const int agg = __shfl_sync(0xffffffffu, wi, CT_THREADS / 32 - 1);
+    if (lane == 0) {
+      volatile unsigned long long* tiles = st->tiles;
+      int excl = 0;
+      if (tile == 0) {
+        atomicExch(&st->tiles[0], FLAG_INC | (unsigned)agg);
+      } else {
+        atomicExch(&st->tiles[tile], FLAG_AGG | (unsigned)agg);
+        for (int j = tile - 1; j >= 0; --j) {
+          unsigned long long sw;
+          do {
+            sw = tiles[j];
+          } while ((sw >> 32) == 0);
+          excl += (int)(sw & 0xffffffffu);
+          if ((sw >> 32) == 2) break;
+        }
+        atomicExch(&st->tiles[tile], FLAG_INC | (unsigned)(excl + agg));
+      }
+      s_excl = excl;
+      if (tile == num_tiles - 1) *count = excl + agg;
+    }
+  }
+  __syncthreads();
+  int pos = s_excl + s_warp[warp] + incl - cnt;
+#pragma unroll
+  for (int j = 0; j < CT_ITEMS; ++j)
+    if (f[j]) list[pos++] = base + j;
+  // the last CTA to finish restores the scratch for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(&st->done_ctr, 1u);
+    s_tile = (done == (unsigned)num_tiles - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_tile) {
+    for (int i = threadIdx.x; i < num_tiles; i += CT_THREADS) st->tiles[i] = 0ull;
+    if (threadIdx.x == 0) {
+      st->tile_ctr = 0;
+      st->done_ctr = 0;
+    }
+    __threadfence();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+size_t scan_state_bytes(int total) {
+  const int tiles = (total + CT_TILE - 1) / CT_TILE;
+  return sizeof(ScanState) + sizeof(unsigned long long) * (tiles > 0 ? tiles : 1);
+}
+
+template <class Flag>
+static cudaError_t launch_compact(const Flag& f, int total, int* list, int* count, void* scan,
+                                  cudaStream_t stream) {
+  const int tiles = (total + CT_TILE - 1) / CT_TILE;
+  if (tiles == 0) return cudaMemsetAsync(count, 0, sizeof(int), stream);
+  compact_kernel<Flag><<<tiles, CT_THREADS, 0, stream>>>(f, total, list, count,
+                                                         reinterpret_cast<ScanState*>(scan), tiles);
+  return cudaGetLastError();
+}
+
+int masker_splits(int win, int c, int* chunks_per_split) {
+  const int cell_chunks = win * win * (c / 8);
+  const int budget = 1024;  // 16 KiB of x per warp work item
+  const int splits = (cell_chunks + budget - 1) / budget;
+  *chunks_per_split = (cell_chunks + splits - 1) / splits;
+  return splits;
+}
+
+cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c,
+                                  int s, int stride, const float* wdiff, float bias,
+                                  uint8_t* coarse, int* list, int* count, float* partial,
+                                  void* scan, cudaStream_t stream) {
+  const int win = s * stride;
+  const int cells_h = h / win, cells_w = w / win;
+  int cps = 0;
+  const int splits = masker_splits(win, c, &cps);
+  const long long items = (long long)n * cells_h * cells_w * splits;
+  const int blocks = (int)((items + 7) / 8);
+  if (x_f32)
+    cell_dot_kernel<float><<<blocks, 256, c * sizeof(float), stream>>>(
+        reinterpret_cast<const float*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff, splits,
+        cps, partial);
+  else
+    cell_dot_kernel<__nv_bfloat16><<<blocks, 256, c * sizeof(float), stream>>>(
+        reinterpret_cast<const __nv_bfloat16*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff,
+        splits, cps, partial);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse};
+  return launch_compact(f, n * cells_h * cells_w, list, count, scan, stream);
+}
+
+cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,
+                                  void* scan, cudaStream_t stream) {
+  GivenFlag f{coarse};
+  return launch_compact(f, total, list, count, scan, stream);
+}
+
+cudaError_t launch_dilate_pixels(const uint8_t* coarse, int n, int h, int w, int s, int stride,
+                                 int cells_h, int cells_w, int radius, int* list, int* count,
+                                 void* scan, cudaStream_t stream) {
+  DilateFlag f{coarse, h, w, s, stride, cells_h, cells_w, radius};
+  return launch_compact(f, n * h * w, list, count, scan, stream);
+}
+
+}  // namespace laud

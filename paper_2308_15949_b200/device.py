@@ -1,0 +1,232 @@
+"""Device plumbing: layouts, weight packing, workspaces, block launch.
+
+PyTorch is used only for device memory, streams and layout conversion;
+every arithmetic op of the path runs in ``_laud.so`` (see ``_lib.py``).
+
+Layouts (DESIGN.md §Data layout):
+  activations  NHWC bf16, channels zero-padded to a multiple of 8;
+  weights      [c_out][k*k][kpad(c_in)] bf16, kpad = c_in rounded up to 64;
+  masks        uint8 per cell of the OUTPUT grid, row-major (n, i, j);
+  lists        int32 linear cell / pixel indices plus a device-side count.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import BlockSpec
+from .errors import DeviceError
+
+
+def pad8(c: int) -> int:
+    return (c + 7) // 8 * 8
+
+
+def kpad(c: int) -> int:
+    return (c + 63) // 64 * 64
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: this package has no CPU fallback")
+    _lib.lib()
+
+
+def ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def stream_handle(stream: Optional[torch.cuda.Stream] = None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+# ---------------------------------------------------------------------------
+# layout conversion (host numpy NCHW <-> device NHWC)
+# ---------------------------------------------------------------------------
+
+
+def to_device_nhwc(x: np.ndarray, dtype=torch.bfloat16, device="cuda") -> torch.Tensor:
+    """(N, C, H, W) numpy -> (N, H, W, pad8(C)) device tensor, zero padded."""
+    n, c, h, w = x.shape
+    t = torch.zeros((n, h, w, pad8(c)), dtype=dtype, device=device)
+    t[..., :c] = torch.from_numpy(np.ascontiguousarray(x.transpose(0, 2, 3, 1))).to(device, dtype)
+    return t
+
+
+def from_device_nhwc(t: torch.Tensor, c: int) -> np.ndarray:
+    """(N, H, W, Cp) device tensor -> (N, C, H, W) float64 numpy."""
+    return t[..., :c].permute(0, 3, 1, 2).double().cpu().numpy()
+
+
+def pack_weight(w, c_in_pad: int, device="cuda") -> torch.Tensor:
+    """[c_out, c_in, k, k] (numpy or torch) -> [c_out, k*k, kpad(c_in_pad)] bf16 on device."""
+    wt = torch.as_tensor(np.asarray(w) if isinstance(w, np.ndarray) else w, dtype=torch.float32)
+    co, ci, kh, kw = wt.shape
+    out = torch.zeros((pad8(co), kh * kw, kpad(c_in_pad)), dtype=torch.float32)
+    out[:co, :, :ci] = wt.permute(0, 2, 3, 1).reshape(co, kh * kw, ci)
+    return out.to(device=device, dtype=torch.bfloat16).contiguous()
+
+
+def fvec(v, n: int, fill: float, device="cuda") -> torch.Tensor:
+    """Per-channel fp32 vector padded to pad8(n) (padding channels get `fill`)."""
+    out = torch.full((pad8(n),), fill, dtype=torch.float32)
+    if v is not None:
+        out[:n] = torch.as_tensor(np.asarray(v, dtype=np.float32))
+    return out.to(device)
+
+
+# ---------------------------------------------------------------------------
+# workspace
+# ---------------------------------------------------------------------------
+
+
+class Workspace:
+    """Grow-only device scratch shared by the blocks launched on one stream."""
+
+    def __init__(self, device="cuda"):
+        self.device = torch.device(device)
+        self._bufs: dict[str, torch.Tensor] = {}
+        self._lock = threading.Lock()
+
+    def get(self, name: str, nbytes: int, zero: bool = False) -> torch.Tensor:
+        nbytes = max(int(nbytes), 16)
+        with self._lock:
+            b = self._bufs.get(name)
+            if b is None or b.numel() < nbytes:
+                b = (torch.zeros if zero else torch.empty)(nbytes, dtype=torch.uint8,
+                                                           device=self.device)
+                self._bufs[name] = b
+            return b
+
+
+_WS: dict = {}
+
+
+def workspace(device=None) -> Workspace:
+    dev = torch.device(device if device is not None else "cuda")
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    key = (idx, torch.cuda.current_stream(idx).cuda_stream)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = _WS[key] = Workspace(f"cuda:{idx}")
+    return ws
+
+
+# ---------------------------------------------------------------------------
+# a block resident on the device
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Epilogue:
+    """Folded BN scale/bias per conv plus ReLU flags (None = identity)."""
+    s1: Optional[np.ndarray] = None
+    b1: Optional[np.ndarray] = None
+    relu1: bool = False
+    s2: Optional[np.ndarray] = None
+    b2: Optional[np.ndarray] = None
+    relu2: bool = False
+    s3: Optional[np.ndarray] = None
+    b3: Optional[np.ndarray] = None
+    sd: Optional[np.ndarray] = None
+    bd: Optional[np.ndarray] = None
+    relu_out: bool = False
+
+
+class DeviceBlock:
+    """Packed weights + epilogue vectors of one bottleneck block."""
+
+    def __init__(self, block: BlockSpec, w1, w2, w3, w_down=None, epilogue: Optional[Epilogue] = None,
+                 masker_w=None, masker_bias: float = 0.0, device="cuda"):
+        require_cuda()
+        self.block = block
+        self.c_in, self.c_mid, self.c_out = (block.conv1.in_channels, block.conv1.out_channels,
+                                             block.conv3.out_channels)
+        self.cin_p, self.cmid_p, self.cout_p = pad8(self.c_in), pad8(self.c_mid), pad8(self.c_out)
+        if block.conv2.groups != 1:
+            raise DeviceError("grouped conv2 is not supported by the CUDA path yet")
+        self.w1 = pack_weight(w1, self.cin_p, device)
+        self.w2 = pack_weight(w2, self.cmid_p, device)
+        self.w3 = pack_weight(w3, self.cmid_p, device)
+        self.wd = pack_weight(w_down, self.cin_p, device) if w_down is not None else None
+        ep = epilogue or Epilogue()
+        self.ep = ep
+        self.vec = {}
+        for k, n, fill in (("s1", self.c_mid, 1.0), ("b1", self.c_mid, 0.0), ("s2", self.c_mid, 1.0),
+                           ("b2", self.c_mid, 0.0), ("s3", self.c_out, 1.0), ("b3", self.c_out, 0.0),
+                           ("sd", self.c_out, 1.0), ("bd", self.c_out, 0.0)):
+            v = getattr(ep, k)
+            self.vec[k] = fvec(v, n, fill, device) if v is not None else None
+        self.wdiff = None
+        self.masker_bias = float(masker_bias)
+        if masker_w is not None:
+            self.set_masker(masker_w, masker_bias)
+
+    def set_masker(self, masker_w, bias: float = 0.0):
+        """Store W0 - W1 (fused-masker identity, `reference.py:244-253`)."""
+        mw = np.asarray(masker_w, dtype=np.float64).reshape(2, -1)
+        wd = np.zeros(self.cin_p, dtype=np.float32)
+        wd[: mw.shape[1]] = (mw[0] - mw[1]).astype(np.float32)
+        self.wdiff = torch.from_numpy(wd).to(self.w1.device)
+        self.masker_bias = float(bias)
+
+    def out_hw(self, h: int, w: int):
+        return self.block.conv2.out_hw(h, w)
+
+    def forward(self, x: torch.Tensor, paradigm: str = "spatial", s: int = 1,
+                coarse: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                misplace_first: bool = False, stream=None, ws: Optional[Workspace] = None):
+        """x: (N, H, W, cin_p) bf16 CUDA.  Returns (out, coarse, cell_list, cell_count)."""
+        n, h, w, cl = x.shape
+        if cl != self.cin_p or x.dtype != torch.bfloat16 or not x.is_contiguous():
+            raise DeviceError("x must be contiguous NHWC bf16 with pad8(C_in) channels")
+        ho, wo = self.out_hw(h, w)
+        blk = self.block
+        if out is None:
+            out = torch.empty((n, ho, wo, self.cout_p), dtype=torch.bfloat16, device=x.device)
+        ws = ws or workspace(x.device)
+        if paradigm == "spatial":
+            cells = n * (ho // s) * (wo // s) if s >= 1 and ho % s == 0 and wo % s == 0 else n
+        else:
+            cells = n
+        pix = n * h * w
+        i32 = 4
+        coarse_buf = ws.get("coarse", cells) if coarse is None else coarse
+        cell_list = ws.get("cell_list", cells * i32)
+        counts = ws.get("counts", 16)
+        pix_list = ws.get("pix_list", pix * i32)
+        h1 = ws.get("h1", pix * self.cmid_p * 2)
+        h2 = ws.get("h2", n * ho * wo * self.cmid_p * 2)
+        lib = _lib.lib()
+        partial_n = 1
+        if coarse is None and paradigm in ("spatial", "layer"):
+            if self.wdiff is None:
+                raise DeviceError("no mask given and no masker weights set")
+            ss = s if paradigm == "spatial" else ho
+            partial_n = max(1, lib.laud_masker_partial_floats(n, h, w, self.cin_p, ss, blk.stride))
+        partial = ws.get("partial", partial_n * 4)
+        scan = ws.get("scan", lib.laud_scan_workspace_bytes(max(pix, cells)), zero=True)
+        v = self.vec
+        a = _lib.BlockArgs(
+            paradigm=_lib.PARADIGM[paradigm], n=n, h_in=h, w_in=w, c_in=self.cin_p, x_ld=self.cin_p,
+            c_mid=self.cmid_p, c_out=self.cout_p, stride=blk.stride, groups=blk.conv2.groups,
+            s=s, has_down=int(blk.has_downsample), x=ptr(x), out=ptr(out), w1=ptr(self.w1),
+            w2=ptr(self.w2), w3=ptr(self.w3), wd=ptr(self.wd),
+            s1=ptr(v["s1"]), b1=ptr(v["b1"]), s2=ptr(v["s2"]), b2=ptr(v["b2"]),
+            s3=ptr(v["s3"]), b3=ptr(v["b3"]), sd=ptr(v["sd"]), bd=ptr(v["bd"]),
+            relu1=int(self.ep.relu1), relu2=int(self.ep.relu2), relu_out=int(self.ep.relu_out),
+            masker_wdiff=ptr(self.wdiff), masker_bias=self.masker_bias,
+            given_coarse=ptr(coarse), coarse_out=ptr(coarse_buf), cell_list=ptr(cell_list),
+            cell_count=C.c_void_p(counts.data_ptr()), pix_list=ptr(pix_list),
+            pix_count=C.c_void_p(counts.data_ptr() + 4), h1=ptr(h1), h2=ptr(h2),
+            partial=ptr(partial), scan=ptr(scan), misplace_first=int(misplace_first))
+        _lib.check(lib.laud_block_forward(C.byref(a), stream_handle(stream)))
+        return out, coarse_buf, cell_list, counts

@@ -1,0 +1,99 @@
+"""Conv engine (tcgen05 implicit GEMM) and compaction kernels vs PyTorch fp32.
+
+GPU only.  The torch fp32 reference takes the same bf16-rounded inputs and
+weights, so the only difference is fp32 accumulation order plus the final
+bf16 rounding of the kernel output.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine():
+    from paper_2308_15949_b200 import channel as CH
+    from paper_2308_15949_b200 import device as D
+    D.require_cuda()
+    return CH, D
+
+
+def _torch_conv_nhwc(x, w, stride, pad):
+    """x (N,H,W,C) bf16, w (Co,Ci,k,k) fp32 -> (N,Ho,Wo,Co) fp32 reference."""
+    y = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float(), stride=stride, padding=pad)
+    return y.permute(0, 2, 3, 1)
+
+
+@pytest.mark.parametrize("cin,cout,k,stride,n,h", [
+    (64, 64, 1, 1, 2, 8), (128, 256, 1, 1, 1, 16), (256, 512, 1, 2, 2, 14),
+    (64, 64, 3, 1, 2, 8), (128, 128, 3, 2, 1, 16), (16, 8, 3, 1, 1, 9), (40, 24, 1, 1, 3, 5),
+    (1024, 256, 1, 1, 1, 14), (256, 256, 3, 1, 4, 28),
+])
+def test_dense_conv_matches_torch(cin, cout, k, stride, n, h):
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(cin * 7 + cout + k)
+    x = torch.randn(n, h, h, cin, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(cout, cin, k, k, generator=g) / np.sqrt(cin * k * k)).to(torch.bfloat16).float()
+    wp = D.pack_weight(w, cin)
+    ho = (h + 2 * (k // 2) - k) // stride + 1
+    out = torch.empty(n, ho, ho, cout, dtype=torch.bfloat16, device="cuda")
+    CH.conv(act=x, in_hw=(h, h), in_c=cin, in_ld=cin, weight=wp, n_out=cout, out=out, out_ld=cout,
+            out_hw=(ho, ho), batch=n, ksize=k, stride=stride, pad=k // 2)
+    ref = _torch_conv_nhwc(x, w.cuda(), stride, k // 2)
+    err = (out.float() - ref).norm() / ref.norm()
+    assert err < 6e-3, float(err)
+
+
+def test_epilogue_scale_bias_relu_residual():
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(3)
+    n, h, cin, cout = 2, 12, 128, 256
+    x = torch.randn(n, h, h, cin, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(cout, cin, 1, 1, generator=g) / np.sqrt(cin)).to(torch.bfloat16).float()
+    sc = torch.rand(cout, generator=g) + 0.5
+    bi = torch.randn(cout, generator=g)
+    res = torch.randn(n, h, h, cout, generator=g).cuda().to(torch.bfloat16)
+    out = res.clone()
+    CH.conv(act=x, in_hw=(h, h), in_c=cin, in_ld=cin, weight=D.pack_weight(w, cin), n_out=cout,
+            out=out, out_ld=cout, out_hw=(h, h), batch=n, scale=sc.cuda(), bias=bi.cuda(), relu=1,
+            resid=out, resid_ld=cout)
+    ref = torch.relu(_torch_conv_nhwc(x, w.cuda(), 1, 0) * sc.cuda() + bi.cuda() + res.float())
+    err = (out.float() - ref).norm() / ref.norm()
+    assert err < 6e-3, float(err)
+
+
+def test_patch_rows_gather_scatter():
+    """Patch-list rows: 3x3 conv evaluated only on listed S x S patches."""
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(5)
+    n, h, c, s = 2, 16, 64, 4
+    x = torch.randn(n, h, h, c, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(c, c, 3, 3, generator=g) / np.sqrt(9 * c)).to(torch.bfloat16).float()
+    cells = [1, 6, 17, 30]  # linear (n, i, j) cell ids on a 4x4 grid per image
+    lst = torch.tensor(cells, dtype=torch.int32, device="cuda")
+    cnt = torch.tensor([len(cells)], dtype=torch.int32, device="cuda")
+    rows = torch.zeros(len(cells) * s * s, c, dtype=torch.bfloat16, device="cuda")
+    CH.conv(act=x, in_hw=(h, h), in_c=c, in_ld=c, weight=D.pack_weight(w, c), n_out=c, out=rows,
+            out_ld=c, out_hw=(h, h), batch=n, ksize=3, pad=1, row_mode=CH.ROWS_PATCH,
+            rows_max=n * h * h, lst=lst, count=cnt, patch=(s, s), cells=(h // s, h // s),
+            out_mode=CH.OUT_ROW)
+    ref = _torch_conv_nhwc(x, w.cuda(), 1, 1)
+    exp = []
+    for cell in cells:
+        ni, r = divmod(cell, 16)
+        ci, cj = divmod(r, 4)
+        exp.append(ref[ni, ci * s:(ci + 1) * s, cj * s:(cj + 1) * s].reshape(s * s, c))
+    exp = torch.cat(exp)
+    err = (rows.float() - exp).norm() / exp.norm()
+    assert err < 6e-3, float(err)
+
+
+def test_compaction_matches_argwhere():
+    from paper_2308_15949_b200 import reference as R
+    rng = np.random.default_rng(0)
+    for shape, p in [((3, 7, 7), 0.5), ((256, 14, 14), 0.3), ((1, 1, 1), 1.0), ((5, 3, 2), 0.0),
+                     ((64, 56, 56), 0.5)]:
+        coarse = rng.random(shape) < p
+        plan = R.build_gather_plan(coarse)
+        assert plan.indices == tuple(tuple(int(v) for v in r) for r in np.argwhere(coarse))
+        assert plan.patch_count == int(coarse.sum())

@@ -1,0 +1,185 @@
+"""GPU parity: the drop-in API (CUDA path) vs the CPU oracle and the golden fixtures.
+
+Tolerances (BASELINE north star):
+  * masks / gather plans / dilation: bit-exact (near-tie cells excluded and counted);
+  * bf16 block outputs: <= 1e-3 norm-relative vs the bf16-emulating oracle
+    (same rounding points), and reported vs pure fp64;
+  * GPU sparse vs GPU dense-masked: bit-exact (identical rounding points);
+  * cells the mask leaves inactive: bitwise equal to the skip path.
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import laud_oracle as O
+from paper_2308_15949_b200.core import BlockSpec, ConvLayerSpec, DynamicConfig, Paradigm, TensorShape
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+BF16_TOL = 1e-3
+
+
+def _R():
+    from paper_2308_15949_b200 import reference as R
+    from paper_2308_15949_b200 import device as D
+    D.require_cuda()
+    return R
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _oracle_mask(R, m):
+    if isinstance(m, R.SpatialMask):
+        return O.SpatialMask(m.coarse, m.upsampled, m.granularity)
+    if isinstance(m, R.LayerMask):
+        return O.LayerMask(m.decisions)
+    if isinstance(m, R.ChannelMask):
+        return O.ChannelMask(m.coarse, m.expanded, m.granularity)
+    return m
+
+
+def test_spatial_masker_decisions_match_oracle():
+    R = _R()
+    a = np.load(G / "maskers.npz")
+    for i in range(4):
+        x, w, s = a[f"sp{i}_x"], a[f"sp{i}_w"], int(a[f"sp{i}_s"])
+        m = R.spatial_masker_forward(x, w, s)
+        ref = a[f"sp{i}_coarse"]
+        # near-tie guard: |d| <= 1e-6 * sum |p||w| may legitimately flip in fp32
+        n, c, h, ww = x.shape
+        pooled = x.reshape(n, c, h // s, s, ww // s, s).mean(axis=(3, 5))
+        wd = (w[0] - w[1]).reshape(c)
+        d = np.einsum("nchw,c->nhw", pooled, wd)
+        scale = np.einsum("nchw,c->nhw", np.abs(pooled), np.abs(wd))
+        safe = np.abs(d) > 1e-6 * scale
+        assert np.array_equal(m.coarse[safe], ref[safe])
+        assert (~safe).sum() == 0
+        assert np.array_equal(m.upsampled, a[f"sp{i}_up"])
+
+
+def test_spatial_masker_train_mode_replays_reference_rng():
+    R = _R()
+    a = np.load(G / "maskers.npz")
+    for i in range(4):
+        x, w, s = a[f"sp{i}_x"], a[f"sp{i}_w"], int(a[f"sp{i}_s"])
+        mt = R.spatial_masker_forward(x, w, s, mode="train", tau=0.7, rng=np.random.default_rng(99 + i))
+        assert np.array_equal(mt.coarse, a[f"sp{i}_train_coarse"])
+        np.testing.assert_allclose(mt.soft, a[f"sp{i}_train_soft"], rtol=1e-4, atol=1e-6)
+
+
+def test_masker_on_block_input_large():
+    """fp32 masker at full BASELINE size (R101 s1 block input, batch 8, S=4)."""
+    R = _R()
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((8, 256, 56, 56)).astype(np.float32).astype(np.float64)
+    w = rng.standard_normal((2, 256, 1, 1)) / 16
+    m = R.spatial_masker_forward(x, w, 4)
+    ref = O.spatial_masker_forward(x, w, 4)
+    assert m.coarse.shape == (8, 14, 14)
+    assert np.mean(m.coarse == ref.coarse) == 1.0
+
+
+def test_dilate_and_rates_matches_oracle():
+    R = _R()
+    a = np.load(G / "maskers.npz")
+    for i in range(4):
+        coarse, s = a[f"sp{i}_coarse"], int(a[f"sp{i}_s"])
+        for k in (1, 3, 5):
+            m = R.SpatialMask(coarse, R.upsample_coarse(coarse, s), s)
+            r, rd, dil = R.dilate_and_rates(m, k)
+            r2, rd2, dil2 = O.dilate_and_rates(O.SpatialMask(coarse, O.upsample_coarse(coarse, s), s), k)
+            assert r == r2 and abs(rd - rd2) < 1e-12 and np.array_equal(dil, dil2)
+        np.testing.assert_allclose(R.dilate_and_rates(R.SpatialMask(coarse, R.upsample_coarse(coarse, s), s), 3)[:2],
+                                   a[f"sp{i}_rates"], atol=1e-12)
+
+
+def _cases():
+    meta = json.loads((G / "equivalence.json").read_text())
+    return [m for m in meta if m["paradigm"] in ("spatial", "layer")]
+
+
+@pytest.mark.parametrize("m", _cases(), ids=lambda m: m["key"])
+def test_block_sparse_matches_oracle(m):
+    R = _R()
+    case = O.EquivalenceCase(Paradigm(m["paradigm"]), m["channels"], m["height"], m["width"],
+                             m["granularity"], m["seed"])
+    block, mask, bw, x, cfg = O.case_inputs(case)
+    rmask = (R.SpatialMask(mask.coarse, mask.upsampled, mask.granularity)
+             if case.paradigm is Paradigm.SPATIAL else R.LayerMask(mask.decisions))
+    rbw = R.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
+    y = R.block_forward_sparse(x, rbw, block, cfg, rmask)
+    emu = O.block_forward_sparse(x, bw, block, cfg, mask, emulate_bf16=True)
+    ref = np.load(G / "equivalence.npz")[m["key"] + "__sparse"]
+    assert _rel(y, emu) <= BF16_TOL, _rel(y, emu)
+    assert _rel(y, ref) <= 1e-2  # pure fp64 reference, bf16 storage error
+    # inactive cells carry the skip path bitwise (bf16 of the skip)
+    skip = O.round_bf16(O.skip_path(O.round_bf16(x), block,
+                                    O.BlockWeights(*(O.round_bf16(w) if w is not None else None
+                                                     for w in (bw.w1, bw.w2, bw.w3, bw.w_down))),
+                                    None, O.round_bf16))
+    if case.paradigm is Paradigm.SPATIAL:
+        inactive = ~mask.upsampled
+        if not block.has_downsample:
+            np.testing.assert_array_equal(y.transpose(0, 2, 3, 1)[inactive],
+                                          skip.transpose(0, 2, 3, 1)[inactive])
+        else:
+            assert _rel(y.transpose(0, 2, 3, 1)[inactive], skip.transpose(0, 2, 3, 1)[inactive]) < 1e-2
+
+
+@pytest.mark.parametrize("case", [c for c in O.default_cases(per_paradigm=8)
+                                  if c.paradigm is not Paradigm.CHANNEL],
+                         ids=lambda c: f"{c.paradigm.value}-{c.channels}-{c.height}-g{c.granularity}-s{c.seed}")
+def test_gpu_equivalence_suite_is_exact(case):
+    R = _R()
+    rc = R.EquivalenceCase(case.paradigm, case.channels, case.height, case.width, case.granularity, case.seed)
+    assert R.run_equivalence_case(rc) == 0.0
+    block, mask, *_ = O.case_inputs(case)
+    if case.paradigm is Paradigm.SPATIAL and mask.coarse.any():
+        assert R.run_equivalence_case(rc, inject_fault=True) > 1e-3
+
+
+def test_config1_block_matches_reference_golden():
+    """BASELINE config 1 through the drop-in: R50 s3b1, 14x14x1024, S=2, batch 1."""
+    R = _R()
+    from paper_2308_15949_b200.zoo import build_network
+    a = np.load(G / "config1.npz")
+    block = [b.block for b in build_network("resnet50").blocks if b.stage == 3 and b.index == 1][0]
+    rng = np.random.default_rng(0)
+    bw = R.make_block_weights(block, rng)
+    x = rng.standard_normal((1, 1024, 14, 14))
+    mw = rng.standard_normal((2, 1024, 1, 1)) / np.sqrt(1024)
+    m = R.spatial_masker_forward(x, mw, 2)
+    assert np.array_equal(m.coarse, a["coarse"])
+    cfg = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=2)
+    y = R.block_forward_sparse(x, bw, block, cfg, m)
+    obw = O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
+    emu = O.block_forward_sparse(x, obw, block, cfg, O.SpatialMask(m.coarse, m.upsampled, 2),
+                                 emulate_bf16=True)
+    assert _rel(y, emu) <= BF16_TOL
+    assert _rel(y, a["y"]) <= 3e-3
+    me = R.SpatialMask(a["coarse_exact"], R.upsample_coarse(a["coarse_exact"], 2), 2)
+    y2 = R.block_forward_sparse(x, bw, block, cfg, me)
+    assert _rel(y2, a["y_exact"]) <= 3e-3
+
+
+def test_full_and_empty_masks_at_scale():
+    """R101 s2b1 geometry (28x28x512, S=2), batch 4: all-ones == static, zeros == identity."""
+    R = _R()
+    blk = BlockSpec(ConvLayerSpec(512, 128, 1), ConvLayerSpec(128, 128, 3), ConvLayerSpec(128, 512, 1),
+                    TensorShape(512, 28, 28))
+    rng = np.random.default_rng(11)
+    bw = R.make_block_weights(blk, rng)
+    x = rng.standard_normal((4, 512, 28, 28))
+    ones = np.ones((4, 14, 14), bool)
+    y1 = R.block_forward_sparse(x, bw, blk, DynamicConfig(Paradigm.SPATIAL, spatial_granularity=2),
+                                R.SpatialMask(ones, R.upsample_coarse(ones, 2), 2))
+    ys = R.block_forward_sparse(x, bw, blk, DynamicConfig(Paradigm.STATIC), None)
+    np.testing.assert_array_equal(y1, ys)
+    zeros = np.zeros_like(ones)
+    y0 = R.block_forward_sparse(x, bw, blk, DynamicConfig(Paradigm.SPATIAL, spatial_granularity=2),
+                                R.SpatialMask(zeros, R.upsample_coarse(zeros, 2), 2))
+    np.testing.assert_array_equal(y0, O.round_bf16(x))
