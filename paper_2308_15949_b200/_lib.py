@@ -62,7 +62,7 @@ _SIGS = {
     "laud_spatial_masker": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.c_int, _vp, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp]),
     "laud_cells_from_mask": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp]),
-    "laud_dilate_pixels": (C.c_int, [_vp] + [C.c_int] * 7 + [_vp, _vp, _vp, _vp]),
+    "laud_dilate_pixels": (C.c_int, [_vp] + [C.c_int] * 6 + [_vp, _vp, _vp, _vp]),
     "laud_conv": (C.c_int, [C.POINTER(ConvArgs), _vp]),
     "laud_block_forward": (C.c_int, [C.POINTER(BlockArgs), _vp]),
     "laud_stem_im2col": (C.c_int, [_vp] + [C.c_int] * 6 + [_vp, _vp, _vp, C.c_int, _vp]),
