@@ -44,6 +44,18 @@ const char* laud_last_error(void);
 /* Number of kernels this library launched since load (diagnostics / bench). */
 uint64_t laud_launch_count(void);
 
+/* Per-launch CUDA-event profiling (off by default; outside timed regions).
+ * laud_profile_end synchronises, fills up to max_records records in launch
+ * order and returns how many were written.  rows = actual GEMM rows (device
+ * count resolved), k = kernel taps * input channels; flops = 2*rows*n_out*k. */
+typedef struct laud_profile_record {
+  int tag; /* 0 conv engine, 1 masker, 2 compaction/dilation, 3 glue */
+  float ms;
+  long long rows, n_out, k, bytes;
+} laud_profile_record;
+void laud_profile_begin(void);
+int laud_profile_end(laud_profile_record* out, int max_records);
+
 /* Bytes of look-back scratch for a compaction over `items` elements.  Must be
  * zeroed once after allocation; the kernels restore it to zero. */
 size_t laud_scan_workspace_bytes(int items);

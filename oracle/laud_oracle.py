@@ -711,3 +711,76 @@ def spatial_block_flops(block: BlockSpec, coarse: np.ndarray, s: int) -> dict:
     total = 2 * (r_dil_in * f1 + r * f2 + r * f3 + fd + fm)
     static = 2 * (f1 + f2 + f3 + fd)
     return dict(r=r, r_dil_in=r_dil_in, flops=total, static_flops=static)
+
+
+# ---------------------------------------------------------------------------
+# EXT: network composer — stem, max-pool, blocks, GAP, FC
+# ---------------------------------------------------------------------------
+
+IMAGENET_MEAN = np.array([123.675, 116.28, 103.53])
+IMAGENET_STD = np.array([58.395, 57.12, 57.375])
+
+
+def maxpool3s2(x):
+    """3x3 / stride 2 / pad 1 max-pool, NCHW (padding never wins)."""
+    n, c, h, w = x.shape
+    ho, wo = (h - 1) // 2 + 1, (w - 1) // 2 + 1
+    p = np.pad(x, ((0, 0), (0, 0), (1, 1), (1, 1)), constant_values=-np.inf)
+    out = np.full((n, c, ho, wo), -np.inf)
+    for dy in range(3):
+        for dx in range(3):
+            out = np.maximum(out, p[:, :, dy:dy + 2 * (ho - 1) + 1:2, dx:dx + 2 * (wo - 1) + 1:2])
+    return out
+
+
+def network_forward(params: dict, images_u8: np.ndarray, paradigm: str = "spatial",
+                    plan=(4, 2, 2, 1), biases=None, masks=None, emulate_bf16: bool = False,
+                    record=None) -> np.ndarray:
+    """EXT: whole-network forward on the CPU in fp64 (N, H, W, 3) uint8 -> logits.
+
+    The reference has block specs only (`zoo.py:160-241`); this
+    composes stem -> max-pool -> blocks (`block_forward_sparse` per block with
+    folded-BN/ReLU epilogues) -> GAP -> FC with the parameters produced by
+    ``paper_2308_15949_b200.network.make_params``.  ``masks`` (optional list of
+    coarse arrays, one per block) overrides the masker decisions, so GPU runs
+    can be replayed exactly; ``biases`` are the per-block masker biases.
+    """
+    rnd = round_bf16 if emulate_bf16 else (lambda a: a)
+    net = params["net"]
+    x = (images_u8.astype(np.float64) - IMAGENET_MEAN) / IMAGENET_STD
+    x = rnd(x.transpose(0, 3, 1, 2))
+    st = net.stem
+    y = conv_raw(x, rnd(params["stem_w"]), st.stride, st.kernel // 2)
+    x = rnd(np.maximum(y + params["stem_b"].reshape(1, -1, 1, 1), 0.0))
+    if net.stem_pool:
+        x = maxpool3s2(x)
+    for i, bp in enumerate(params["blocks"]):
+        blk = bp["block"]
+        out = blk.output_shape
+        ep = Epilogues(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"], relu2=True,
+                       s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"], relu_out=True)
+        bw = BlockWeights(bp["w1"], bp["w2"], bp["w3"], bp["wd"])
+        bias = 0.0 if biases is None else biases[i]
+        if paradigm == "static":
+            cfg = DynamicConfig(Paradigm.STATIC)
+            mask = None
+        elif paradigm == "layer":
+            cfg = DynamicConfig(Paradigm.LAYER)
+            if masks is not None:
+                d = np.asarray(masks[i]).reshape(-1).astype(bool)
+            else:
+                d = block_spatial_mask(x, bp["masker_w"], blk, out.height, bias).coarse.reshape(-1)
+            mask = LayerMask(d)
+        else:
+            s = plan[bp["stage"] - 1]
+            cfg = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=s)
+            if masks is not None:
+                c = np.asarray(masks[i]).reshape(x.shape[0], out.height // s, out.width // s).astype(bool)
+                mask = SpatialMask(c, upsample_coarse(c, s), s)
+            else:
+                mask = block_spatial_mask(x, bp["masker_w"], blk, s, bias)
+        if record is not None:
+            record.append(mask)
+        x = block_forward_sparse(x, bw, blk, cfg, mask, epilogues=ep, emulate_bf16=emulate_bf16)
+    feat = rnd(x.mean(axis=(2, 3)))
+    return feat @ rnd(params["fc_w"]).T + params["fc_b"]

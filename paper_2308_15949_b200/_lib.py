@@ -53,7 +53,15 @@ class BlockArgs(C.Structure):
     ]
 
 
+class ProfileRecord(C.Structure):
+    """Mirror of ``laud_profile_record`` (include/laud.h)."""
+    _fields_ = [("tag", C.c_int), ("ms", C.c_float), ("rows", C.c_longlong),
+                ("n_out", C.c_longlong), ("k", C.c_longlong), ("bytes", C.c_longlong)]
+
+
 _SIGS = {
+    "laud_profile_begin": (None, []),
+    "laud_profile_end": (C.c_int, [C.POINTER(ProfileRecord), C.c_int]),
     "laud_version": (C.c_char_p, []),
     "laud_last_error": (C.c_char_p, []),
     "laud_launch_count": (C.c_uint64, []),

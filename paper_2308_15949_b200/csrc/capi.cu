@@ -12,6 +12,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/laud.h"
 #include "laud_conv.cuh"
@@ -43,6 +44,39 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+
+// Optional per-launch CUDA-event profiling (laud_profile_*), off by default.
+struct ProfRec {
+  int tag;               // 0 conv, 1 masker, 2 compaction/dilate, 3 glue
+  cudaEvent_t e0, e1;
+  const int* count;      // device row count (nullable)
+  long long rows_per_count, rows_max, n_out, k_alg, bytes;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+
+struct ProfScope {
+  ProfRec rec;
+  bool on;
+  cudaStream_t st;
+  ProfScope(int tag, cudaStream_t s) : on(false), st(s) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_on) return;
+    on = true;
+    memset(&rec, 0, sizeof(rec));
+    rec.tag = tag;
+    cudaEventCreate(&rec.e0);
+    cudaEventCreate(&rec.e1);
+    cudaEventRecord(rec.e0, st);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(rec.e1, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(rec);
+  }
+};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -209,12 +243,59 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   CUtensorMap m;
   int rc = weight_map(a->weight, a->n_out, a->ksize * a->ksize * p.kpad, bn, &m);
   if (rc) return rc;
+  ProfScope ps(0, st);
+  if (ps.on) {
+    ps.rec.count = a->row_mode == ROWS_DENSE ? nullptr : a->count;
+    ps.rec.rows_per_count = a->row_mode == ROWS_PATCH ? (long long)p.patch_h * p.patch_w : 1;
+    ps.rec.rows_max = a->rows_max;
+    ps.rec.n_out = a->n_out;
+    ps.rec.k_alg = (long long)a->ksize * a->ksize * a->in_c;
+  }
   return cuda_check(launch_conv_gemm(m, bn, p, num_sms(), st), "conv_gemm launch", 1);
 }
 
 }  // namespace
 
 extern "C" {
+
+void laud_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = true;
+}
+
+int laud_profile_end(laud_profile_record* out, int max_records) {
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = false;
+    recs.swap(g_prof);
+  }
+  int n = 0;
+  for (auto& r : recs) {
+    cudaEventSynchronize(r.e1);
+    if (out && n < max_records) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.e0, r.e1);
+      long long rows = r.rows_max;
+      if (r.count) {
+        int c = 0;
+        cudaMemcpy(&c, r.count, sizeof(int), cudaMemcpyDeviceToHost);
+        rows = (long long)c * r.rows_per_count;
+        if (rows > r.rows_max) rows = r.rows_max;
+      }
+      out[n].tag = r.tag;
+      out[n].ms = ms;
+      out[n].rows = rows;
+      out[n].n_out = r.n_out;
+      out[n].k = r.k_alg;
+      out[n].bytes = r.bytes;
+      ++n;
+    }
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  return n;
+}
 
 const char* laud_version(void) { return "laud-b200 0.1.0 (sm_100a, tcgen05)"; }
 const char* laud_last_error(void) { return g_err.c_str(); }
@@ -240,6 +321,8 @@ int laud_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, i
     return fail(LAUD_ERR_GRANULARITY, "S=%d (window %d) does not divide %dx%d", s, win, h, w);
   if (c % 8 || ld % 8 || ld < c) return fail(LAUD_ERR_SHAPE, "channels must be multiples of 8");
   if (c > 12288) return fail(LAUD_ERR_SHAPE, "masker supports at most 12288 channels");
+  ProfScope ps(1, (cudaStream_t)stream);
+  if (ps.on) ps.rec.bytes = (long long)n * h * w * c * (x_f32 ? 4 : 2);
   return cuda_check(launch_spatial_masker(x, x_f32, ld, n, h, w, c, s, stride, wdiff, bias, coarse,
                                           cell_list, cell_count, partial, scan,
                                           (cudaStream_t)stream),
@@ -248,6 +331,8 @@ int laud_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, i
 
 int laud_cells_from_mask(const uint8_t* coarse, int cells, int* cell_list, int* cell_count,
                          void* scan, void* stream) {
+  ProfScope ps(2, (cudaStream_t)stream);
+  if (ps.on) ps.rec.bytes = (long long)cells * 5;
   return cuda_check(
       launch_list_from_mask(coarse, cells, cell_list, cell_count, scan, (cudaStream_t)stream),
       "cells from mask", 1);
@@ -259,6 +344,8 @@ int laud_dilate_pixels(const uint8_t* coarse, int n, int h_in, int w_in, int s, 
   if (s < 1 || stride < 1 || h_in % win || w_in % win)
     return fail(LAUD_ERR_GRANULARITY, "S=%d does not divide the output grid", s);
   if (radius < 0) return fail(LAUD_ERR_ARG, "radius must be >= 0");
+  ProfScope ps(2, (cudaStream_t)stream);
+  if (ps.on) ps.rec.bytes = (long long)n * h_in * w_in * 4;
   return cuda_check(launch_dilate_pixels(coarse, n, h_in, w_in, s, stride, h_in / win, w_in / win,
                                          radius, pix_list, pix_count, scan, (cudaStream_t)stream),
                     "dilate pixels", 1);

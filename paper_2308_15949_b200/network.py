@@ -1,0 +1,269 @@
+"""LAUDNet network executor on the CUDA path.
+
+Runs a whole LAUD-ResNet / RegNet-style backbone from the zoo specs:
+stem (im2col + tcgen05 GEMM, folded BN, ReLU) -> 3x3/s2 max-pool -> the
+bottleneck blocks (spatial / layer / static paradigms, masker-driven masks)
+-> global average pool -> FC (fp32 logits).  Everything after the input
+upload is stream-ordered on the device with no host synchronisation, so a
+forward can be captured in a CUDA graph.
+
+Weights are random-init (no checkpoints exist); folded-BN
+scale/bias are synthetic.  Masker weights are random N(0, 1/C); a per-block
+masker bias (EXT, a conv bias on the masker's logit 0) is calibrated on a
+calibration batch so the block's activation ratio hits ``target_ratio`` —
+the role a trained masker's FLOPs loss plays in the paper.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import channel as CH
+from . import device as D
+from .core import Paradigm
+from .zoo import build_network, parse_plan
+
+IMAGENET_MEAN = (123.675, 116.28, 103.53)
+IMAGENET_STD = (58.395, 57.12, 57.375)
+
+
+def make_params(arch: str = "resnet101", seed: int = 0) -> dict:
+    """Random-init parameters of a whole network, pure numpy (host-side init).
+
+    Shared by the CUDA executor and the CPU oracle's network composer so both
+    run the same weights.  Conv weights N(0,1)/sqrt(fan_in) as in
+    `reference.py:271-286`; folded BN: scale sqrt(2) after the ReLU'd convs,
+    0.5 on conv3, small random biases; masker W ~ N(0, 1/C) of shape (2, C, 1, 1).
+    """
+    net = build_network(arch)
+    rng = np.random.default_rng(seed)
+    st = net.stem
+    p = {"arch": arch, "net": net}
+    p["stem_w"] = rng.standard_normal((st.out_channels, 3, st.kernel, st.kernel)) * \
+        np.sqrt(2.0 / (3 * st.kernel ** 2))
+    p["stem_b"] = rng.standard_normal(st.out_channels) * 0.01
+    blocks = []
+    for bi in net.blocks:
+        blk = bi.block
+        cm, co, ci = blk.conv1.out_channels, blk.conv3.out_channels, blk.input_shape.channels
+
+        def draw(layer):
+            cig = layer.in_channels // layer.groups
+            return rng.standard_normal((layer.out_channels, cig, layer.kernel, layer.kernel)) / \
+                np.sqrt(cig * layer.kernel ** 2)
+
+        wd = rng.standard_normal((co, ci, 1, 1)) / np.sqrt(ci) if blk.has_downsample else None
+        w1, w2, w3 = draw(blk.conv1), draw(blk.conv2), draw(blk.conv3)
+        blocks.append(dict(
+            stage=bi.stage, index=bi.index, block=blk, w1=w1, w2=w2, w3=w3, wd=wd,
+            s1=np.full(cm, np.sqrt(2.0)), b1=rng.standard_normal(cm) * 0.05,
+            s2=np.full(cm, np.sqrt(2.0)), b2=rng.standard_normal(cm) * 0.05,
+            s3=np.full(co, 0.5), b3=rng.standard_normal(co) * 0.05,
+            sd=np.ones(co), bd=np.zeros(co),
+            masker_w=rng.standard_normal((2, ci, 1, 1)) / np.sqrt(ci)))
+    p["blocks"] = blocks
+    fc_in = net.classifier_features
+    p["fc_w"] = rng.standard_normal((net.num_classes, fc_in)) / np.sqrt(fc_in)
+    p["fc_b"] = rng.standard_normal(net.num_classes) * 0.01
+    return p
+
+
+@dataclass
+class BlockSlot:
+    stage: int
+    index: int
+    db: D.DeviceBlock
+    s: int           # spatial granularity (output grid); 0 for static
+
+
+class LaudNetwork:
+    """A LAUD backbone + classifier resident on one GPU."""
+
+    def __init__(self, arch: str = "resnet101", paradigm: str = "spatial", plan: str = "4-2-2-1",
+                 target_ratio: float = 0.5, seed: int = 0, device="cuda"):
+        D.require_cuda()
+        params = make_params(arch, seed)
+        self.params = params
+        self.net = params["net"]
+        self.paradigm = paradigm
+        self.target_ratio = target_ratio
+        self.device = torch.device(device)
+        net = self.net
+        para = Paradigm(paradigm)
+        if para is Paradigm.SPATIAL:
+            self.plan = parse_plan(plan, net, para).values
+        else:
+            self.plan = tuple(net.stage_feature(i + 1).height for i in range(len(net.stages)))
+        # stem: k x k / s2 conv over 3 channels via im2col (K = k*k*3 padded to 8)
+        st = net.stem
+        self.stem_k, self.stem_stride = st.kernel, st.stride
+        self.stem_cols = D.pad8(st.kernel * st.kernel * 3)
+        ws = params["stem_w"]
+        wcol = np.zeros((st.out_channels, 1, 1, self.stem_cols))
+        wcol[:, 0, 0, : st.kernel * st.kernel * 3] = ws.transpose(0, 2, 3, 1).reshape(st.out_channels, -1)
+        self.stem_w = D.pack_weight(wcol.transpose(0, 3, 1, 2), self.stem_cols, device)
+        self.stem_c = D.pad8(st.out_channels)
+        self.stem_scale = D.fvec(np.ones(st.out_channels), st.out_channels, 1.0, device)
+        self.stem_bias = D.fvec(params["stem_b"], st.out_channels, 0.0, device)
+        self.mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32, device=device)
+        self.inv_std = torch.tensor([1.0 / s for s in IMAGENET_STD], dtype=torch.float32, device=device)
+        # blocks
+        self.slots: list[BlockSlot] = []
+        for bp in params["blocks"]:
+            blk = bp["block"]
+            ep = D.Epilogue(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"],
+                            relu2=True, s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"],
+                            relu_out=True)
+            db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep,
+                               masker_w=bp["masker_w"], device=device)
+            s = self.plan[bp["stage"] - 1] if para is Paradigm.SPATIAL else 0
+            self.slots.append(BlockSlot(bp["stage"], bp["index"], db, s))
+        fc_in = net.classifier_features
+        self.fc_w = D.pack_weight(params["fc_w"][:, :, None, None], D.pad8(fc_in), device)
+        self.fc_b = D.fvec(params["fc_b"], net.num_classes, 0.0, device)
+        self.n_cls = D.pad8(net.num_classes)
+        self._bufs = {}
+        self.ws = D.Workspace(device)
+
+    # ------------------------------------------------------------------ buffers
+    def _buf(self, name, shape, dtype=torch.bfloat16):
+        """View of a grow-only flat buffer (stable addresses across forwards)."""
+        numel = int(np.prod(shape))
+        b = self._bufs.get(name)
+        if b is None or b.numel() < numel or b.dtype != dtype:
+            b = torch.empty(numel, dtype=dtype, device=self.device)
+            self._bufs[name] = b
+        return b[:numel].view(shape)
+
+    def _block_paradigm(self, slot: BlockSlot) -> str:
+        return self.paradigm if self.paradigm in ("spatial", "layer") else "static"
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, images: torch.Tensor, stream=None, record=None) -> torch.Tensor:
+        """images: (N, H, W, 3) uint8 on the device -> (N, classes) fp32 logits.
+
+        ``record`` (optional list) receives (slot, coarse, counts) references
+        per dynamic block for post-hoc rate statistics.
+        """
+        net = self.net
+        n, h, w, _ = images.shape
+        k, st = self.stem_k, self.stem_stride
+        pad = k // 2
+        ho, wo = (h + 2 * pad - k) // st + 1, (w + 2 * pad - k) // st + 1
+        sh = D.stream_handle(stream)
+        cols = self._buf("cols", (n * ho * wo, self.stem_cols))
+        _lib.call("laud_stem_im2col", D.ptr(images), n, h, w, k, st, pad, D.ptr(self.mean),
+                  D.ptr(self.inv_std), D.ptr(cols), self.stem_cols, sh)
+        stem_out = self._buf("stem", (n, ho, wo, self.stem_c))
+        CH.conv(act=cols, in_hw=(n * ho * wo, 1), in_c=self.stem_cols, in_ld=self.stem_cols,
+                weight=self.stem_w, n_out=self.stem_c, out=stem_out, out_ld=self.stem_c,
+                out_hw=(ho, wo), batch=n, a_compact=1, scale=self.stem_scale, bias=self.stem_bias,
+                relu=1, stream=stream)
+        x = stem_out
+        if net.stem_pool:
+            ph, pw = (ho - 1) // 2 + 1, (wo - 1) // 2 + 1
+            pool = self._buf("pool", (n, ph, pw, self.stem_c))
+            _lib.call("laud_maxpool3s2", D.ptr(stem_out), n, ho, wo, self.stem_c, D.ptr(pool), sh)
+            x = pool
+        ping = 0
+        for slot in self.slots:
+            db = slot.db
+            hh, ww = x.shape[1], x.shape[2]
+            oh, ow = db.out_hw(hh, ww)
+            para = self._block_paradigm(slot)
+            if db.block.has_downsample:
+                ping ^= 1
+                out = self._buf(f"act{ping}", (n, oh, ow, db.cout_p))
+            else:
+                out = x  # in-place residual: conv1 reads x before conv3 writes it
+            y, coarse, cells, counts = db.forward(x, para, slot.s if para == "spatial" else 0,
+                                                  out=out, stream=stream, ws=self.ws)
+            if record is not None and para != "static":
+                ncell = n * (oh // slot.s) * (ow // slot.s) if para == "spatial" else n
+                record.append((slot, coarse[:ncell].clone(), counts[:8].clone()))
+            x = y
+        c = x.shape[-1]
+        feat = self._buf("feat", (n, c))
+        _lib.call("laud_global_avgpool", D.ptr(x), n, x.shape[1] * x.shape[2], c, D.ptr(feat), sh)
+        logits = self._buf("logits", (n, self.n_cls), torch.float32)
+        CH.conv(act=feat, in_hw=(n, 1), in_c=c, in_ld=c, weight=self.fc_w, n_out=self.n_cls,
+                out=logits, out_ld=self.n_cls, out_hw=(n, 1), batch=n, a_compact=1,
+                bias=self.fc_b, out_f32=1, stream=stream)
+        return logits
+
+    # ------------------------------------------------------------------ calibration
+    def calibrate(self, images: torch.Tensor, ratio: Optional[float] = None):
+        """Set each dynamic block's masker bias so its active ratio ~= ``ratio``.
+
+        Block by block on the calibration batch: run the block's masker alone,
+        read the per-cell decision values d, and place the threshold at the
+        (1 - ratio) quantile (bias = -quantile).  Done once, outside timing.
+        """
+        ratio = self.target_ratio if ratio is None else ratio
+        if self.paradigm not in ("spatial", "layer"):
+            return
+        for slot in self.slots:
+            slot.db.masker_bias = -1e30  # placeholder; set below
+        saved = []
+        lib = _lib.lib()
+        orig_forward = D.DeviceBlock.forward
+
+        def hooked(db, x, paradigm="spatial", s=1, **kw):
+            if paradigm in ("spatial", "layer"):
+                n, h, w, cp = x.shape
+                ho, wo = db.out_hw(h, w)
+                ss = s if paradigm == "spatial" else ho
+                cells = n * (ho // ss) * (wo // ss)
+                npart = lib.laud_masker_partial_floats(n, h, w, cp, ss, db.block.stride)
+                part = torch.empty(max(1, npart), dtype=torch.float32, device=x.device)
+                coarse = torch.empty(cells, dtype=torch.uint8, device=x.device)
+                lst = torch.empty(cells, dtype=torch.int32, device=x.device)
+                cnt = torch.zeros(1, dtype=torch.int32, device=x.device)
+                scan = self.ws.get("scan", lib.laud_scan_workspace_bytes(max(cells, n * h * w)), zero=True)
+                _lib.call("laud_spatial_masker", D.ptr(x), 0, cp, n, h, w, cp, ss, db.block.stride,
+                          D.ptr(db.wdiff), 0.0, D.ptr(coarse), D.ptr(lst), D.ptr(cnt), D.ptr(part),
+                          D.ptr(scan), D.stream_handle())
+                win = ss * db.block.stride
+                dbar = part.view(cells, -1).sum(1) / float(win * win)
+                q = torch.quantile(dbar.double(), 1.0 - ratio).item()
+                db.masker_bias = float(-q)
+                saved.append(db.masker_bias)
+            return orig_forward(db, x, paradigm, s, **kw)
+
+        D.DeviceBlock.forward = hooked
+        try:
+            self.forward(images)
+        finally:
+            D.DeviceBlock.forward = orig_forward
+        torch.cuda.synchronize()
+        return saved
+
+    def masker_biases(self):
+        return [slot.db.masker_bias for slot in self.slots]
+
+    def set_masker_biases(self, biases):
+        for slot, b in zip(self.slots, biases):
+            slot.db.masker_bias = float(b)
+
+    def rate_stats(self, images: torch.Tensor):
+        """Per-block measured activation ratio (host sync; not for timing)."""
+        rec = []
+        self.forward(images, record=rec)
+        torch.cuda.synchronize()
+        out = []
+        for slot, coarse, counts in rec:
+            out.append(dict(stage=slot.stage, index=slot.index, s=slot.s,
+                            r=float(coarse.float().mean().item()),
+                            patches=int(counts.view(torch.int32)[0].item())))
+        return out
+
+
+def random_images(n: int, h: int = 224, w: int = 224, seed: int = 0, device="cuda") -> torch.Tensor:
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.randint(0, 256, (n, h, w, 3), dtype=torch.uint8, generator=g).to(device)

@@ -82,3 +82,19 @@ def test_no_cpu_fallback_without_gpu():
     import numpy as np
     with pytest.raises(DeviceError):
         R.build_gather_plan(np.ones((1, 2, 2), bool))
+
+
+def _prototype_arity():
+    body = re.sub(r"/\*.*?\*/", "", HDR, flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(laud_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", body):
+        params = m.group(2).strip()
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_ctypes_signatures_match_header_arity():
+    from paper_2308_15949_b200 import _lib
+    ar = _prototype_arity()
+    for name, (_, args) in _lib._SIGS.items():
+        assert len(args) == ar[name], (name, len(args), ar[name])
