@@ -193,7 +193,7 @@ class LaudNetwork:
         _lib.call("laud_global_avgpool", D.ptr(x), n, x.shape[1] * x.shape[2], c, D.ptr(feat), sh)
         logits = self._buf("logits", (n, self.n_cls), torch.float32)
         CH.conv(act=feat, in_hw=(n, 1), in_c=c, in_ld=c, weight=self.fc_w, n_out=self.n_cls,
-                out=logits, out_ld=self.n_cls, out_hw=(n, 1), batch=n, a_compact=1,
+                out=logits, out_ld=self.n_cls, out_hw=(n, 1), batch=1, a_compact=1,
                 bias=self.fc_b, out_f32=1, stream=stream)
         return logits
 
