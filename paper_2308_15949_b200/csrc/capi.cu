@@ -49,23 +49,31 @@ std::atomic<uint64_t> g_launches{0};
 struct ProfRec {
   int tag;               // 0 conv, 1 masker, 2 compaction/dilate, 3 glue
   cudaEvent_t e0, e1;
-  const int* count;      // device row count (nullable)
+  int snap;              // index of the count snapshot (-1: none)
   long long rows_per_count, rows_max, n_out, k_alg, bytes;
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
+int* g_prof_counts = nullptr;  // device snapshots of row counts at launch time
+int g_prof_nsnap = 0;
+constexpr int kProfSnaps = 8192;
 
 struct ProfScope {
   ProfRec rec;
   bool on;
   cudaStream_t st;
-  ProfScope(int tag, cudaStream_t s) : on(false), st(s) {
+  ProfScope(int tag, cudaStream_t s, const int* count = nullptr) : on(false), st(s) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     if (!g_prof_on) return;
     on = true;
     memset(&rec, 0, sizeof(rec));
     rec.tag = tag;
+    rec.snap = -1;
+    if (count && g_prof_counts && g_prof_nsnap < kProfSnaps) {  // snapshot before e0
+      rec.snap = g_prof_nsnap++;
+      cudaMemcpyAsync(g_prof_counts + rec.snap, count, sizeof(int), cudaMemcpyDeviceToDevice, st);
+    }
     cudaEventCreate(&rec.e0);
     cudaEventCreate(&rec.e1);
     cudaEventRecord(rec.e0, st);
@@ -243,9 +251,8 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   CUtensorMap m;
   int rc = weight_map(a->weight, a->n_out, a->ksize * a->ksize * p.kpad, bn, &m);
   if (rc) return rc;
-  ProfScope ps(0, st);
+  ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
   if (ps.on) {
-    ps.rec.count = a->row_mode == ROWS_DENSE ? nullptr : a->count;
     ps.rec.rows_per_count = a->row_mode == ROWS_PATCH ? (long long)p.patch_h * p.patch_w : 1;
     ps.rec.rows_max = a->rows_max;
     ps.rec.n_out = a->n_out;
@@ -260,6 +267,8 @@ extern "C" {
 
 void laud_profile_begin(void) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_prof_counts) cudaMalloc(&g_prof_counts, kProfSnaps * sizeof(int));
+  g_prof_nsnap = 0;
   g_prof_on = true;
 }
 
@@ -271,16 +280,18 @@ int laud_profile_end(laud_profile_record* out, int max_records) {
     recs.swap(g_prof);
   }
   int n = 0;
+  std::vector<int> snaps(kProfSnaps, 0);
+  cudaDeviceSynchronize();
+  if (g_prof_counts && g_prof_nsnap)
+    cudaMemcpy(snaps.data(), g_prof_counts, g_prof_nsnap * sizeof(int), cudaMemcpyDeviceToHost);
   for (auto& r : recs) {
     cudaEventSynchronize(r.e1);
     if (out && n < max_records) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, r.e0, r.e1);
       long long rows = r.rows_max;
-      if (r.count) {
-        int c = 0;
-        cudaMemcpy(&c, r.count, sizeof(int), cudaMemcpyDeviceToHost);
-        rows = (long long)c * r.rows_per_count;
+      if (r.snap >= 0) {
+        rows = (long long)snaps[r.snap] * r.rows_per_count;
         if (rows > r.rows_max) rows = r.rows_max;
       }
       out[n].tag = r.tag;

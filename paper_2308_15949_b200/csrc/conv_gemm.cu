@@ -1,17 +1,18 @@
 // Implicit-GEMM convolution engine on tcgen05 / TMEM / TMA (sm_100a).
 //
-// Persistent, warp-specialised kernel (320 threads, 1 CTA per SM):
+// Persistent, warp-specialised kernel (448 threads, 1 CTA per SM):
 //   warps 0-3  A producers: gather 128 output-pixel rows x 64 channels of the
 //              activation for one (tap, channel-block) with cp.async (16 B per
 //              lane, zero-fill outside the image / list), written in the UMMA
 //              K-major 128B-swizzled layout;
-//   warp  8    B producer: one TMA tile load of the packed weights per stage;
-//   warp  9    MMA issuer: 4 x tcgen05.mma (128xBNx16) per stage into one of two
+//   warp 12    B producer: one TMA tile load of the packed weights per stage;
+//   warp 13    MMA issuer: 4 x tcgen05.mma (128xBNx16) per stage into one of two
 //              TMEM accumulators; owns TMEM alloc/dealloc;
-//   warps 4-7  epilogue: tcgen05.ld -> scale/bias (folded BN) -> +residual ->
-//              ReLU -> bf16 store to the row's destination pixel (scatter) or
-//              compact row.  Double-buffered TMEM lets the epilogue of tile i
-//              overlap the mainloop of tile i+1.
+//   warps 4-11 epilogue (4 TMEM lane quadrants x 2 column halves):
+//              tcgen05.ld -> scale/bias (folded BN) -> +residual -> ReLU ->
+//              bf16 row staged in smem -> coalesced store to the row's
+//              destination pixel (scatter) or compact row.  Double-buffered
+//              TMEM lets the epilogue of tile i overlap the mainloop of i+1.
 // Row enumeration (dense grid / active-patch list / pixel list) and the
 // device-side row count make the same kernel serve the gather-conv1,
 // patch conv2 (3x3, halo via zero-filled gathers) and conv3+scatter-add steps
@@ -27,7 +28,10 @@ namespace laud {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
-constexpr int NUM_THREADS = 320;
+constexpr int NUM_EPI_WARPS = 8;   // warps 4..11
+constexpr int WARP_TMA = 12;
+constexpr int WARP_MMA = 13;
+constexpr int NUM_THREADS = 14 * 32;
 
 struct RowPos {
   int n, y, x;
@@ -75,7 +79,11 @@ struct Smem {
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
-  static constexpr int BAR_OFF = B_OFF + STAGES * B_STAGE_BYTES;
+  static constexpr int STG_ROW = BN * 2 + 16;  // padded: conflict-free row-per-lane access
+  static constexpr int STG_OFF = B_OFF + STAGES * B_STAGE_BYTES;
+  static constexpr int VEC_OFF = STG_OFF + BM * STG_ROW;  // per-warp scale/bias slices
+  static constexpr int VEC_BYTES = NUM_EPI_WARPS * 2 * (BN / 2) * 4;
+  static constexpr int BAR_OFF = VEC_OFF + VEC_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
   static constexpr int BYTES = TMEM_SLOT_OFF + 16;
@@ -113,12 +121,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 128);
+      mbar_init(&acc_empty[a], NUM_EPI_WARPS * 32);
     }
     fence_barrier_init();
   }
-  if (warp == 8 && lane == 0) tma_prefetch_desc(&tmap_b);
-  if (warp == 9) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  if (warp == WARP_TMA && lane == 0) tma_prefetch_desc(&tmap_b);
+  if (warp == WARP_MMA) tmem_alloc<L::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -170,7 +178,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         cp_async_mbar_arrive_noinc(&full[stage]);
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == WARP_TMA) {
     // ------------------------------------------------------------ B producer (TMA)
     if (lane == 0) {
       uint32_t it = 0;
@@ -186,7 +194,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == WARP_MMA) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
     uint32_t it = 0, local = 0;
@@ -218,26 +226,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 4-7)
-    const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+    // ------------------------------------------------------------ epilogue (warps 4-11)
+    // Warp e handles TMEM lane quadrant q = warp % 4 (rows 32q..32q+31) and
+    // column half hf of the tile.  Rows are staged through shared memory so
+    // the residual read and the destination write are coalesced 16-byte-per-
+    // lane row segments (a scattered destination row is contiguous in NHWC);
+    // the residual is prefetched with cp.async before the accumulator lands.
+    constexpr int HALF = BN / 2;        // columns per warp
+    constexpr int CPR = HALF / 8;       // 16-byte chunks per staged half-row
+    const int q = warp & 3;
+    const int hf = (warp - 4) >> 2;
+    const int col0 = hf * HALF;
+    uint8_t* stg = base + L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
+    const uint32_t stg_u32 = base_u32 + L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
+    float* vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + (warp - 4) * 2 * HALF;
+    float* vbi = vsc + HALF;
+    const __nv_bfloat16* resid = reinterpret_cast<const __nv_bfloat16*>(p.resid);
+    __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
+    const bool staged = !p.out_f32;
     uint32_t local = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = (t / n_tiles) * BM;
-      const int n0 = (t % n_tiles) * BN;
+      const int c_base = (t % n_tiles) * BN + col0;      // first output channel of this warp
+      const int nch = max(0, min(HALF, p.n_out - c_base));  // valid channels (multiple of 8)
+      const int vchunks = nch >> 3;
       RowPos rp;
       bool fp;
-      const int m = m0 + ew * 32 + lane;
+      const int m = m0 + q * 32 + lane;
       const bool valid = map_row(p, m, nvalid, rp, fp);
-      size_t dst_row = 0;
+      long long dst_row = 0;
       if (valid) {
         if (p.out_mode == OUT_ROW) {
-          dst_row = (size_t)m;
+          dst_row = m;
         } else {
           int y = rp.y;
           if (p.misplace_first && fp) y = (y + p.patch_h) % p.out_h;
-          dst_row = (size_t)(rp.n * p.out_h + y) * p.out_w + rp.x;
+          dst_row = (long long)(rp.n * p.out_h + y) * p.out_w + rp.x;
         }
       }
       bool do_relu = p.relu != 0;
@@ -247,84 +273,112 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.relu_inactive_coarse) do_relu = p.relu_inactive_coarse[cell] == 0;
         if (p.ymask_coarse) ymul = p.ymask_coarse[cell] ? 1.f : 0.f;
       }
+      // per-tile channel vectors -> smem (coalesced), residual rows -> smem (cp.async)
+      for (int i = lane; i < HALF; i += 32) {
+        const int c = c_base + i;
+        vsc[i] = (p.scale && c < p.n_out) ? __ldg(p.scale + c) : 1.f;
+        vbi[i] = (p.bias && c < p.n_out) ? __ldg(p.bias + c) : 0.f;
+      }
+      if (staged && resid && vchunks > 0) {
+#pragma unroll 4
+        for (int idx = lane; idx < 32 * CPR; idx += 32) {
+          const int r = idx / CPR, c = idx % CPR;
+          const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+          const long long dr = __shfl_sync(0xffffffffu, dst_row, r);
+          const bool ok = rv && c < vchunks;
+          const __nv_bfloat16* src = resid + dr * p.resid_ld + c_base + c * 8;
+          cp_async_16(stg_u32 + r * L::STG_ROW + c * 16, ok ? (const void*)src : (const void*)resid,
+                      ok ? 16u : 0u);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if (staged && resid) asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col0;
+      uint8_t* my_row = stg + lane * L::STG_ROW;
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
-        const int c0 = n0 + j * 32;
-        if (c0 >= p.n_out) break;
+      for (int j = 0; j < HALF / 32; ++j) {
+        if (j * 32 >= nch) break;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tbase + j * 32, r);
         if (!valid) continue;
-        float v[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const int cg = c0 + g * 8;
-          if (cg >= p.n_out) break;
-          if (p.scale) {
-            const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + cg));
-            const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + cg + 4));
-            v[g * 8 + 0] *= s0.x; v[g * 8 + 1] *= s0.y; v[g * 8 + 2] *= s0.z; v[g * 8 + 3] *= s0.w;
-            v[g * 8 + 4] *= s1.x; v[g * 8 + 5] *= s1.y; v[g * 8 + 6] *= s1.z; v[g * 8 + 7] *= s1.w;
-          }
-          if (p.bias) {
-            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + cg));
-            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + cg + 4));
-            v[g * 8 + 0] += b0.x; v[g * 8 + 1] += b0.y; v[g * 8 + 2] += b0.z; v[g * 8 + 3] += b0.w;
-            v[g * 8 + 4] += b1.x; v[g * 8 + 5] += b1.y; v[g * 8 + 6] += b1.z; v[g * 8 + 7] += b1.w;
-          }
+          const int cl = j * 32 + g * 8;  // local column within this warp's half
+          if (cl >= nch) break;
+          float v[8];
+          const float4 s0 = *reinterpret_cast<const float4*>(vsc + cl);
+          const float4 s1 = *reinterpret_cast<const float4*>(vsc + cl + 4);
+          const float4 b0 = *reinterpret_cast<const float4*>(vbi + cl);
+          const float4 b1 = *reinterpret_cast<const float4*>(vbi + cl + 4);
+          v[0] = fmaf(__uint_as_float(r[g * 8 + 0]), s0.x, b0.x);
+          v[1] = fmaf(__uint_as_float(r[g * 8 + 1]), s0.y, b0.y);
+          v[2] = fmaf(__uint_as_float(r[g * 8 + 2]), s0.z, b0.z);
+          v[3] = fmaf(__uint_as_float(r[g * 8 + 3]), s0.w, b0.w);
+          v[4] = fmaf(__uint_as_float(r[g * 8 + 4]), s1.x, b1.x);
+          v[5] = fmaf(__uint_as_float(r[g * 8 + 5]), s1.y, b1.y);
+          v[6] = fmaf(__uint_as_float(r[g * 8 + 6]), s1.z, b1.z);
+          v[7] = fmaf(__uint_as_float(r[g * 8 + 7]), s1.w, b1.w);
           if (p.ymask_channel) {
             const uint2 mk = __ldg(reinterpret_cast<const uint2*>(
-                p.ymask_channel + (size_t)rp.n * p.n_out + cg));
+                p.ymask_channel + (size_t)rp.n * p.n_out + c_base + cl));
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              v[g * 8 + q] *= ((q < 4 ? (mk.x >> (8 * q)) : (mk.y >> (8 * (q - 4)))) & 0xff) ? 1.f : 0.f;
+            for (int e = 0; e < 8; ++e)
+              v[e] *= ((e < 4 ? (mk.x >> (8 * e)) : (mk.y >> (8 * (e - 4)))) & 0xff) ? 1.f : 0.f;
           }
-          if (ymul != 1.f) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[g * 8 + q] *= ymul;
-          }
-          if (p.resid) {
-            const uint4 rr = __ldg(reinterpret_cast<const uint4*>(
-                reinterpret_cast<const __nv_bfloat16*>(p.resid) + dst_row * p.resid_ld + cg));
+          for (int e = 0; e < 8; ++e) v[e] *= ymul;
+          uint4* slot = reinterpret_cast<uint4*>(my_row + cl * 2);
+          if (staged && resid) {
+            const uint4 rr = *slot;
             float2 f;
-            f = unpack_bf16x2(rr.x); v[g * 8 + 0] += f.x; v[g * 8 + 1] += f.y;
-            f = unpack_bf16x2(rr.y); v[g * 8 + 2] += f.x; v[g * 8 + 3] += f.y;
-            f = unpack_bf16x2(rr.z); v[g * 8 + 4] += f.x; v[g * 8 + 5] += f.y;
-            f = unpack_bf16x2(rr.w); v[g * 8 + 6] += f.x; v[g * 8 + 7] += f.y;
+            f = unpack_bf16x2(rr.x); v[0] += f.x; v[1] += f.y;
+            f = unpack_bf16x2(rr.y); v[2] += f.x; v[3] += f.y;
+            f = unpack_bf16x2(rr.z); v[4] += f.x; v[5] += f.y;
+            f = unpack_bf16x2(rr.w); v[6] += f.x; v[7] += f.y;
           }
           if (do_relu) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[g * 8 + q] = fmaxf(v[g * 8 + q], 0.f);
+            for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
           }
-          if (p.out_f32) {
-            float* o = reinterpret_cast<float*>(p.out) + dst_row * p.out_ld + cg;
-            reinterpret_cast<float4*>(o)[0] =
-                make_float4(v[g * 8 + 0], v[g * 8 + 1], v[g * 8 + 2], v[g * 8 + 3]);
-            reinterpret_cast<float4*>(o)[1] =
-                make_float4(v[g * 8 + 4], v[g * 8 + 5], v[g * 8 + 6], v[g * 8 + 7]);
+          if (!staged) {
+            float* o = reinterpret_cast<float*>(p.out) + dst_row * p.out_ld + c_base + cl;
+            reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<float4*>(o)[1] = make_float4(v[4], v[5], v[6], v[7]);
           } else {
             uint4 w;
-            w.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
-            w.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
-            w.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
-            w.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) +
-                                      dst_row * p.out_ld + cg) = w;
+            w.x = pack_bf16x2(v[0], v[1]);
+            w.y = pack_bf16x2(v[2], v[3]);
+            w.z = pack_bf16x2(v[4], v[5]);
+            w.w = pack_bf16x2(v[6], v[7]);
+            *slot = w;
           }
         }
       }
+      // accumulator consumed: hand the TMEM buffer back to the MMA warp early
       tc_fence_before();
       mbar_arrive(&acc_empty[acc]);
+      __syncwarp();
+      if (staged && vchunks > 0) {
+#pragma unroll 4
+        for (int idx = lane; idx < 32 * CPR; idx += 32) {
+          const int r = idx / CPR, c = idx % CPR;
+          const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+          const long long dr = __shfl_sync(0xffffffffu, dst_row, r);
+          if (rv && c < vchunks)
+            *reinterpret_cast<uint4*>(outp + dr * p.out_ld + c_base + c * 8) =
+                *reinterpret_cast<const uint4*>(stg + r * L::STG_ROW + c * 16);
+        }
+      }
+      __syncwarp();
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == WARP_MMA) {
     tc_fence_after();
     tmem_dealloc<L::TMEM_COLS>(tmem_base);
   }
@@ -356,9 +410,9 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap, int bn, const ConvParams& 
   const int n_tiles = (p.n_out + bn - 1) / bn;
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
   switch (bn) {
-    case 64: return launch_bn<64, 8>(tmap, p, tiles_max, num_sms, stream);
-    case 128: return launch_bn<128, 6>(tmap, p, tiles_max, num_sms, stream);
-    case 256: return launch_bn<256, 4>(tmap, p, tiles_max, num_sms, stream);
+    case 64: return launch_bn<64, 6>(tmap, p, tiles_max, num_sms, stream);
+    case 128: return launch_bn<128, 4>(tmap, p, tiles_max, num_sms, stream);
+    case 256: return launch_bn<256, 3>(tmap, p, tiles_max, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }
