@@ -294,7 +294,7 @@ def block_sweep(torch, args, flush):
         s = plan[bp["stage"] - 1]
         ep = D.Epilogue(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"], relu2=True,
                         s3=bp["s3"], b3=bp["b3"], relu_out=True)
-        db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], None, ep)
+        db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], None, ep, fold_scale=True)
         wsp = D.Workspace()
         n = args.batch
         h = blk.input_shape.height

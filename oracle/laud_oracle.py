@@ -757,9 +757,12 @@ def network_forward(params: dict, images_u8: np.ndarray, paradigm: str = "spatia
     for i, bp in enumerate(params["blocks"]):
         blk = bp["block"]
         out = blk.output_shape
-        ep = Epilogues(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"], relu2=True,
-                       s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"], relu_out=True)
-        bw = BlockWeights(bp["w1"], bp["w2"], bp["w3"], bp["wd"])
+        # folded BN as the device executor packs it: W' = W * s (rounded once), + b
+        fold = lambda w, sc: None if w is None else w * sc.reshape(-1, 1, 1, 1)  # noqa: E731
+        ep = Epilogues(b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"],
+                       relu_out=True)
+        bw = BlockWeights(fold(bp["w1"], bp["s1"]), fold(bp["w2"], bp["s2"]),
+                          fold(bp["w3"], bp["s3"]), fold(bp["wd"], bp["sd"]))
         bias = 0.0 if biases is None else biases[i]
         if paradigm == "static":
             cfg = DynamicConfig(Paradigm.STATIC)

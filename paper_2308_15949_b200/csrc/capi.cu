@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,8 +19,8 @@
 #include "laud_conv.cuh"
 
 namespace laud {
-cudaError_t launch_conv_gemm(const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
-                             cudaStream_t stream);
+cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn,
+                             const ConvParams& p, int num_sms, cudaStream_t stream);
 size_t scan_state_bytes(int total);
 int masker_splits(int win, int c, int* chunks_per_split);
 cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c,
@@ -155,10 +156,10 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
 // Weights [rows][k] bf16, k contiguous; box = 64 (k) x bn (rows), 128B swizzle,
 // rows past the end read as zeros.
-int weight_map(const void* w, int rows, int k, int bn, CUtensorMap* out) {
+int tensor_map_2d(const void* w, int rows, int k, int ld, int bn, CUtensorMap* out) {
   int dev = 0;
   cudaGetDevice(&dev);
-  MapKey key{w, rows, k, bn, dev};
+  MapKey key{w, rows, k * 65536 + ld, bn, dev};
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = g_maps.find(key);
@@ -173,7 +174,7 @@ int weight_map(const void* w, int rows, int k, int bn, CUtensorMap* out) {
     return fail(LAUD_ERR_ARG, "weight pointer must be 16-byte aligned");
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)bn};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box,
@@ -188,10 +189,15 @@ int weight_map(const void* w, int rows, int k, int bn, CUtensorMap* out) {
   return LAUD_OK;
 }
 
-int pick_bn(int n_out) {
-  if (n_out >= 256) return 256;
-  if (n_out > 64) return 128;
-  return 64;
+// Tile width: BN=128 (double-buffered epilogue staging) for epilogue-heavy
+// small-K convs and for grids too small to fill the SMs at BN=256.
+int pick_bn(int n_out, int k, long long rows) {
+  if (n_out <= 64) return 64;
+  if (n_out <= 128) return 128;
+  if (k <= 512) return 128;
+  const long long tiles256 = ((rows + 127) / 128) * ((n_out + 255) / 256);
+  if (tiles256 < 2 * num_sms()) return 128;
+  return 256;
 }
 
 int run_conv(const laud_conv_args* a, cudaStream_t st) {
@@ -247,10 +253,29 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   p.ymask_coarse = a->ymask_coarse;
   p.ymask_channel = a->ymask_channel;
   p.misplace_first = a->misplace_first;
-  const int bn = pick_bn(a->n_out);
+  const int bn = pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   CUtensorMap m;
-  int rc = weight_map(a->weight, a->n_out, a->ksize * a->ksize * p.kpad, bn, &m);
+  const int kw = a->ksize * a->ksize * p.kpad;
+  int rc = tensor_map_2d(a->weight, a->n_out, kw, kw, bn, &m);
   if (rc) return rc;
+  // A operand: [a_rows][in_c] with row stride in_ld, gathered 4 rows at a time
+  CUtensorMap ma;
+  memset(&ma, 0, sizeof(ma));
+  static const int a_tma_env = [] {
+    const char* e = getenv("LAUD_A_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  p.a_tma = a_tma_env && (reinterpret_cast<uintptr_t>(a->act) % 16 == 0);
+  if (p.a_tma) {
+    const long long arows = a->a_compact ? (long long)a->rows_max
+                                         : (long long)a->batch * a->in_h * a->in_w;
+    if (arows >= (1ll << 31) - 1) {
+      p.a_tma = 0;
+    } else {
+      p.a_rows = (int)arows;
+      if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, 1, &ma))) return rc;
+    }
+  }
   ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
   if (ps.on) {
     ps.rec.rows_per_count = a->row_mode == ROWS_PATCH ? (long long)p.patch_h * p.patch_w : 1;
@@ -258,7 +283,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
     ps.rec.n_out = a->n_out;
     ps.rec.k_alg = (long long)a->ksize * a->ksize * a->in_c;
   }
-  return cuda_check(launch_conv_gemm(m, bn, p, num_sms(), st), "conv_gemm launch", 1);
+  return cuda_check(launch_conv_gemm(ma, m, bn, p, num_sms(), st), "conv_gemm launch", 1);
 }
 
 }  // namespace

@@ -74,14 +74,15 @@ __device__ __forceinline__ bool map_row(const ConvParams& p, int m, int nvalid, 
   return true;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NSTG>
 struct Smem {
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
   static constexpr int STG_ROW = BN * 2 + 16;  // padded: conflict-free row-per-lane access
   static constexpr int STG_OFF = B_OFF + STAGES * B_STAGE_BYTES;
-  static constexpr int VEC_OFF = STG_OFF + BM * STG_ROW;  // per-warp scale/bias slices
+  static constexpr int STG_BUF = BM * STG_ROW;  // one staging buffer
+  static constexpr int VEC_OFF = STG_OFF + NSTG * STG_BUF;  // per-warp scale/bias slices
   static constexpr int VEC_BYTES = NUM_EPI_WARPS * 2 * (BN / 2) * 4;
   static constexpr int BAR_OFF = VEC_OFF + VEC_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
@@ -91,10 +92,11 @@ struct Smem {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NSTG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    conv_gemm_kernel(const __grid_constant__ CUtensorMap tmap_b, const ConvParams p) {
-  using L = Smem<BN, STAGES>;
+    conv_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                     const ConvParams p) {
+  using L = Smem<BN, STAGES, NSTG>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base_u32 = (raw_u32 + 1023u) & ~1023u;
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 128 + 1);
+      mbar_init(&full[s], p.a_tma ? 2 : 128 + 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -125,7 +127,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == WARP_TMA && lane == 0) tma_prefetch_desc(&tmap_b);
+  if (warp == WARP_TMA && lane == 0) {
+    tma_prefetch_desc(&tmap_b);
+    if (p.a_tma) tma_prefetch_desc(&tmap_a);
+  }
   if (warp == WARP_MMA) tmem_alloc<L::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -136,10 +141,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp < 4) {
     // ------------------------------------------------------------ A producers
     const int tid = threadIdx.x;
+    uint32_t it = 0;
+    if (p.a_tma) {
+      // One output row per thread; per (tap, channel block) every 4th lane issues
+      // a TMA tile::gather4 of its 4 rows' source pixels (OOB index -> zeros).
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / n_tiles) * BM;
+        RowPos rp;
+        bool fp;
+        const bool rv = map_row(p, m0 + tid, nvalid, rp, fp);
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          const int tap = kb / kpt;
+          const int c0 = (kb - tap * kpt) * BK;
+          const int ky = tap / p.ksize;
+          const int kx = tap - ky * p.ksize;
+          int row = p.a_rows;  // out of bounds -> zero fill
+          if (rv) {
+            if (p.a_compact) {
+              row = m0 + tid;
+            } else {
+              const int iy = rp.y * p.stride + ky - p.pad;
+              const int ix = rp.x * p.stride + kx - p.pad;
+              if (iy >= 0 && iy < p.in_h && ix >= 0 && ix < p.in_w)
+                row = (rp.n * p.in_h + iy) * p.in_w + ix;
+            }
+          }
+          const int r1 = __shfl_down_sync(0xffffffffu, row, 1);
+          const int r2 = __shfl_down_sync(0xffffffffu, row, 2);
+          const int r3 = __shfl_down_sync(0xffffffffu, row, 3);
+          const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
+          if (tid == 0) mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES);
+          if ((lane & 3) == 0) tma_gather4(sA + tid * 128, &tmap_a, &full[stage], c0, row, r1, r2, r3);
+        }
+      }
+    } else {
     const int chunk = tid & 7;
     const int rsub = tid >> 3;
     const __nv_bfloat16* act = reinterpret_cast<const __nv_bfloat16*>(p.act);
-    uint32_t it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int m0 = (t / n_tiles) * BM;
       RowPos rp[8];
@@ -177,6 +218,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         cp_async_mbar_arrive_noinc(&full[stage]);
       }
+    }
     }
   } else if (warp == WARP_TMA) {
     // ------------------------------------------------------------ B producer (TMA)
@@ -230,71 +272,90 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Warp e handles TMEM lane quadrant q = warp % 4 (rows 32q..32q+31) and
     // column half hf of the tile.  Rows are staged through shared memory so
     // the residual read and the destination write are coalesced 16-byte-per-
-    // lane row segments (a scattered destination row is contiguous in NHWC);
-    // the residual is prefetched with cp.async before the accumulator lands.
+    // lane row segments (a scattered destination row is contiguous in NHWC).
+    // With NSTG = 2 the residual of the next tile is prefetched (cp.async)
+    // into the other staging buffer while this tile is finished and stored.
     constexpr int HALF = BN / 2;        // columns per warp
     constexpr int CPR = HALF / 8;       // 16-byte chunks per staged half-row
     const int q = warp & 3;
     const int hf = (warp - 4) >> 2;
     const int col0 = hf * HALF;
-    uint8_t* stg = base + L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
-    const uint32_t stg_u32 = base_u32 + L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
+    const int stg_off0 = L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
     float* vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + (warp - 4) * 2 * HALF;
     float* vbi = vsc + HALF;
     const __nv_bfloat16* resid = reinterpret_cast<const __nv_bfloat16*>(p.resid);
     __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
     const bool staged = !p.out_f32;
+    const bool pre = staged && resid != nullptr;
+
+    // per-row destination of tile t for this lane's row
+    struct RowInfo {
+      bool valid;
+      long long dst;
+      RowPos rp;
+      bool fp;
+    };
+    auto row_info = [&](int t) {
+      RowInfo ri;
+      const int m = (t / n_tiles) * BM + q * 32 + lane;
+      ri.valid = map_row(p, m, nvalid, ri.rp, ri.fp);
+      ri.dst = 0;
+      if (ri.valid) {
+        if (p.out_mode == OUT_ROW) {
+          ri.dst = m;
+        } else {
+          int y = ri.rp.y;
+          if (p.misplace_first && ri.fp) y = (y + p.patch_h) % p.out_h;
+          ri.dst = (long long)(ri.rp.n * p.out_h + y) * p.out_w + ri.rp.x;
+        }
+      }
+      return ri;
+    };
+    auto prefetch = [&](int t, const RowInfo& ri, int buf) {
+      const int c_base = (t % n_tiles) * BN + col0;
+      const int vchunks = max(0, min(HALF, p.n_out - c_base)) >> 3;
+      const uint32_t sbase = base_u32 + stg_off0 + buf * L::STG_BUF;
+#pragma unroll 4
+      for (int idx = lane; idx < 32 * CPR; idx += 32) {
+        const int r = idx / CPR, c = idx % CPR;
+        const int rv = __shfl_sync(0xffffffffu, (int)ri.valid, r);
+        const long long dr = __shfl_sync(0xffffffffu, ri.dst, r);
+        const bool ok = rv && c < vchunks;
+        const __nv_bfloat16* src = resid + dr * p.resid_ld + c_base + c * 8;
+        cp_async_16(sbase + r * L::STG_ROW + c * 16, ok ? (const void*)src : (const void*)resid,
+                    ok ? 16u : 0u);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
     uint32_t local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    int t = blockIdx.x;
+    RowInfo cur = row_info(t);
+    if (pre) prefetch(t, cur, 0);
+    for (; t < tiles; t += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int m0 = (t / n_tiles) * BM;
+      const int buf = NSTG == 2 ? (local & 1) : 0;
+      uint8_t* stg = base + stg_off0 + buf * L::STG_BUF;
       const int c_base = (t % n_tiles) * BN + col0;      // first output channel of this warp
       const int nch = max(0, min(HALF, p.n_out - c_base));  // valid channels (multiple of 8)
       const int vchunks = nch >> 3;
-      RowPos rp;
-      bool fp;
-      const int m = m0 + q * 32 + lane;
-      const bool valid = map_row(p, m, nvalid, rp, fp);
-      long long dst_row = 0;
-      if (valid) {
-        if (p.out_mode == OUT_ROW) {
-          dst_row = m;
-        } else {
-          int y = rp.y;
-          if (p.misplace_first && fp) y = (y + p.patch_h) % p.out_h;
-          dst_row = (long long)(rp.n * p.out_h + y) * p.out_w + rp.x;
-        }
-      }
       bool do_relu = p.relu != 0;
       float ymul = 1.f;
-      if (valid && (p.relu_inactive_coarse || p.ymask_coarse)) {
+      if (cur.valid && (p.relu_inactive_coarse || p.ymask_coarse)) {
+        const RowPos& rp = cur.rp;
         const int cell = (rp.n * p.cells_h + rp.y / p.patch_h) * p.cells_w + rp.x / p.patch_w;
         if (p.relu_inactive_coarse) do_relu = p.relu_inactive_coarse[cell] == 0;
         if (p.ymask_coarse) ymul = p.ymask_coarse[cell] ? 1.f : 0.f;
       }
-      // per-tile channel vectors -> smem (coalesced), residual rows -> smem (cp.async)
       for (int i = lane; i < HALF; i += 32) {
         const int c = c_base + i;
         vsc[i] = (p.scale && c < p.n_out) ? __ldg(p.scale + c) : 1.f;
         vbi[i] = (p.bias && c < p.n_out) ? __ldg(p.bias + c) : 0.f;
       }
-      if (staged && resid && vchunks > 0) {
-#pragma unroll 4
-        for (int idx = lane; idx < 32 * CPR; idx += 32) {
-          const int r = idx / CPR, c = idx % CPR;
-          const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
-          const long long dr = __shfl_sync(0xffffffffu, dst_row, r);
-          const bool ok = rv && c < vchunks;
-          const __nv_bfloat16* src = resid + dr * p.resid_ld + c_base + c * 8;
-          cp_async_16(stg_u32 + r * L::STG_ROW + c * 16, ok ? (const void*)src : (const void*)resid,
-                      ok ? 16u : 0u);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      if (staged && resid) asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if (pre) asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col0;
       uint8_t* my_row = stg + lane * L::STG_ROW;
@@ -303,7 +364,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (j * 32 >= nch) break;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tbase + j * 32, r);
-        if (!valid) continue;
+        if (!cur.valid) continue;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int cl = j * 32 + g * 8;  // local column within this warp's half
@@ -323,15 +384,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           v[7] = fmaf(__uint_as_float(r[g * 8 + 7]), s1.w, b1.w);
           if (p.ymask_channel) {
             const uint2 mk = __ldg(reinterpret_cast<const uint2*>(
-                p.ymask_channel + (size_t)rp.n * p.n_out + c_base + cl));
+                p.ymask_channel + (size_t)cur.rp.n * p.n_out + c_base + cl));
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               v[e] *= ((e < 4 ? (mk.x >> (8 * e)) : (mk.y >> (8 * (e - 4)))) & 0xff) ? 1.f : 0.f;
           }
+          if (p.ymask_coarse) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] *= ymul;
+            for (int e = 0; e < 8; ++e) v[e] *= ymul;
+          }
           uint4* slot = reinterpret_cast<uint4*>(my_row + cl * 2);
-          if (staged && resid) {
+          if (pre) {
             const uint4 rr = *slot;
             float2 f;
             f = unpack_bf16x2(rr.x); v[0] += f.x; v[1] += f.y;
@@ -344,7 +407,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
           }
           if (!staged) {
-            float* o = reinterpret_cast<float*>(p.out) + dst_row * p.out_ld + c_base + cl;
+            float* o = reinterpret_cast<float*>(p.out) + cur.dst * p.out_ld + c_base + cl;
             reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], v[3]);
             reinterpret_cast<float4*>(o)[1] = make_float4(v[4], v[5], v[6], v[7]);
           } else {
@@ -361,18 +424,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&acc_empty[acc]);
       __syncwarp();
+      // next tile's rows; with two staging buffers its residual streams in now
+      const int tn = t + gridDim.x;
+      RowInfo nxt = cur;
+      if (tn < tiles) {
+        nxt = row_info(tn);
+        if (pre && NSTG == 2) prefetch(tn, nxt, (local + 1) & 1);
+      }
       if (staged && vchunks > 0) {
 #pragma unroll 4
         for (int idx = lane; idx < 32 * CPR; idx += 32) {
           const int r = idx / CPR, c = idx % CPR;
-          const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
-          const long long dr = __shfl_sync(0xffffffffu, dst_row, r);
+          const int rv = __shfl_sync(0xffffffffu, (int)cur.valid, r);
+          const long long dr = __shfl_sync(0xffffffffu, cur.dst, r);
           if (rv && c < vchunks)
             *reinterpret_cast<uint4*>(outp + dr * p.out_ld + c_base + c * 8) =
                 *reinterpret_cast<const uint4*>(stg + r * L::STG_ROW + c * 16);
         }
       }
       __syncwarp();
+      if (tn < tiles && pre && NSTG == 1) prefetch(tn, nxt, 0);
+      cur = nxt;
     }
   }
 
@@ -388,31 +460,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // host side
 // ---------------------------------------------------------------------------
 
-template <int BN, int STAGES>
-static cudaError_t launch_bn(const CUtensorMap& tmap, const ConvParams& p, int tiles_max,
+template <int BN, int STAGES, int NSTG>
+static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const ConvParams& p, int tiles_max,
                              int num_sms, cudaStream_t stream) {
-  using L = Smem<BN, STAGES>;
+  using L = Smem<BN, STAGES, NSTG>;
+  static_assert(L::ALLOC <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, NSTG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   int grid = tiles_max < num_sms ? tiles_max : num_sms;
   if (grid < 1) grid = 1;
-  conv_gemm_kernel<BN, STAGES><<<grid, NUM_THREADS, L::ALLOC, stream>>>(tmap, p);
+  conv_gemm_kernel<BN, STAGES, NSTG><<<grid, NUM_THREADS, L::ALLOC, stream>>>(tmap_a, tmap, p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_conv_gemm(const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
+cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
                              cudaStream_t stream) {
   const int n_tiles = (p.n_out + bn - 1) / bn;
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
   switch (bn) {
-    case 64: return launch_bn<64, 6>(tmap, p, tiles_max, num_sms, stream);
-    case 128: return launch_bn<128, 4>(tmap, p, tiles_max, num_sms, stream);
-    case 256: return launch_bn<256, 3>(tmap, p, tiles_max, num_sms, stream);
+    case 64: return launch_bn<64, 6, 2>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+    case 128: return launch_bn<128, 4, 2>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+    case 256: return launch_bn<256, 3, 1>(tmap_a, tmap, p, tiles_max, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -33,6 +33,8 @@ struct ConvParams {
   int in_c;              // valid channels (multiple of 8)
   int in_ld;             // elements per pixel row (>= in_c, multiple of 8)
   int a_compact;         // 1: A row = m directly (1x1, taps must be 1)
+  int a_tma;             // 1: A rows gathered with TMA tile::gather4 (else cp.async)
+  int a_rows;            // rows of the A tensor map (also the out-of-bounds marker)
   int ksize, stride, pad;
   int kpad;              // in_c rounded up to 64
   int num_kb;            // ksize*ksize*kpad/64

@@ -141,11 +141,18 @@ class Epilogue:
     relu_out: bool = False
 
 
+def _fold(w, scale):
+    """W * scale[:, None, None, None] (numpy), identity when scale is None."""
+    if scale is None:
+        return w
+    return np.asarray(w, dtype=np.float64) * np.asarray(scale, dtype=np.float64).reshape(-1, 1, 1, 1)
+
+
 class DeviceBlock:
     """Packed weights + epilogue vectors of one bottleneck block."""
 
     def __init__(self, block: BlockSpec, w1, w2, w3, w_down=None, epilogue: Optional[Epilogue] = None,
-                 masker_w=None, masker_bias: float = 0.0, device="cuda"):
+                 masker_w=None, masker_bias: float = 0.0, device="cuda", fold_scale: bool = False):
         require_cuda()
         self.block = block
         self.c_in, self.c_mid, self.c_out = (block.conv1.in_channels, block.conv1.out_channels,
@@ -153,11 +160,17 @@ class DeviceBlock:
         self.cin_p, self.cmid_p, self.cout_p = pad8(self.c_in), pad8(self.c_mid), pad8(self.c_out)
         if block.conv2.groups != 1:
             raise DeviceError("grouped conv2 is not supported by the CUDA path yet")
+        ep = epilogue or Epilogue()
+        if fold_scale:
+            # inference BN folding: per-output-channel scale goes into the weights
+            w1, w2, w3 = _fold(w1, ep.s1), _fold(w2, ep.s2), _fold(w3, ep.s3)
+            w_down = _fold(w_down, ep.sd) if w_down is not None else None
+            ep = Epilogue(None, ep.b1, ep.relu1, None, ep.b2, ep.relu2, None, ep.b3, None, ep.bd,
+                          ep.relu_out)
         self.w1 = pack_weight(w1, self.cin_p, device)
         self.w2 = pack_weight(w2, self.cmid_p, device)
         self.w3 = pack_weight(w3, self.cmid_p, device)
         self.wd = pack_weight(w_down, self.cin_p, device) if w_down is not None else None
-        ep = epilogue or Epilogue()
         self.ep = ep
         self.vec = {}
         for k, n, fill in (("s1", self.c_mid, 1.0), ("b1", self.c_mid, 0.0), ("s2", self.c_mid, 1.0),

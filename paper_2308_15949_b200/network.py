@@ -121,7 +121,7 @@ class LaudNetwork:
                             relu2=True, s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"],
                             relu_out=True)
             db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep,
-                               masker_w=bp["masker_w"], device=device)
+                               masker_w=bp["masker_w"], device=device, fold_scale=True)
             s = self.plan[bp["stage"] - 1] if para is Paradigm.SPATIAL else 0
             self.slots.append(BlockSlot(bp["stage"], bp["index"], db, s))
         fc_in = net.classifier_features

@@ -1,0 +1,40 @@
+"""Whole-network parity: CUDA LaudNetwork vs the oracle network composer.
+
+The GPU's own masker decisions are replayed in the oracle (decisions are
+checked separately, tie-guarded, in test_gpu_parity), so the comparison
+isolates the arithmetic: bf16 storage at the same points, fp32 vs fp64
+accumulation.  Tolerance 2e-2 norm-relative on logits after 33 blocks of
+bf16 storage (per-block gate is 1e-3; errors compound through depth).
+"""
+import numpy as np
+import pytest
+
+from oracle import laud_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _net(arch, paradigm, plan="4-2-2-1", ratio=0.5):
+    import torch
+    from paper_2308_15949_b200.network import LaudNetwork, random_images
+    net = LaudNetwork(arch, paradigm, plan, ratio, seed=0)
+    img = random_images(2, seed=3)
+    net.calibrate(img)
+    rec = []
+    logits = net.forward(img, record=rec)
+    torch.cuda.synchronize()
+    masks = [c.cpu().numpy() for _, c, _ in rec]
+    return net, img.cpu().numpy(), logits[:, :1000].double().cpu().numpy(), masks
+
+
+@pytest.mark.parametrize("arch,paradigm", [("resnet50", "spatial"), ("resnet101", "spatial"),
+                                           ("resnet50", "layer"), ("resnet50", "static")])
+def test_network_matches_oracle(arch, paradigm):
+    net, img, logits, masks = _net(arch, paradigm)
+    plan = tuple(net.plan)
+    ref = O.network_forward(net.params, img, paradigm, plan, masks=masks or None, emulate_bf16=True)
+    rel = np.linalg.norm(logits - ref) / np.linalg.norm(ref)
+    assert rel < 2e-2, rel
+    if paradigm == "spatial":
+        r = np.mean([m.mean() for m in masks])
+        assert 0.3 < r < 0.7
