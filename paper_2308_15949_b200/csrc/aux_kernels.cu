@@ -8,31 +8,54 @@
 
 namespace laud {
 
-// cols[(n*ho + oy)*wo + ox][(ky*k + kx)*3 + c] = (img - mean[c]) * inv_std[c], zero padded,
-// columns k*k*3 .. cols_ld-1 zero.
-__global__ void stem_im2col_kernel(const uint8_t* __restrict__ img, int n, int h, int w, int k,
-                                   int stride, int pad, int ho, int wo, const float* __restrict__ mean,
-                                   const float* __restrict__ inv_std, __nv_bfloat16* __restrict__ cols,
-                                   int cols_ld) {
-  const long long total = (long long)n * ho * wo * cols_ld;
+// Stem im2col, K laid out per kernel row: cols[pix][ky*SEG + kx*3 + c] with
+// SEG = pad8(k*3) (zero tail), value (img - mean[c]) * inv_std[c], zero padded
+// outside the image.  One thread per (output pixel, ky) writes one SEG-wide
+// 16-byte-aligned segment; cols_ld = k*SEG.
+template <int K>
+__global__ void stem_im2col_kernel(const uint8_t* __restrict__ img, int n, int h, int w, int stride,
+                                   int pad, int ho, int wo, const float* __restrict__ mean,
+                                   const float* __restrict__ inv_std,
+                                   __nv_bfloat16* __restrict__ cols, int cols_ld) {
+  constexpr int SEG = (K * 3 + 7) / 8 * 8;
+  const float m0 = mean[0], m1 = mean[1], m2 = mean[2];
+  const float s0 = inv_std[0], s1 = inv_std[1], s2 = inv_std[2];
+  const long long total = (long long)n * ho * wo * K;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const int col = (int)(i % cols_ld);
-    const long long row = i / cols_ld;
-    float v = 0.f;
-    if (col < k * k * 3) {
-      const int c = col % 3;
-      const int tap = col / 3;
-      const int ky = tap / k, kx = tap - (tap / k) * k;
-      const int ox = (int)(row % wo);
-      const long long t = row / wo;
-      const int oy = (int)(t % ho);
-      const int ni = (int)(t / ho);
-      const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
-      if (iy >= 0 && iy < h && ix >= 0 && ix < w)
-        v = ((float)img[((size_t)(ni * h + iy) * w + ix) * 3 + c] - mean[c]) * inv_std[c];
+    const int ky = (int)(i % K);
+    const long long pix = i / K;
+    const int ox = (int)(pix % wo);
+    const long long t = pix / wo;
+    const int oy = (int)(t % ho);
+    const int ni = (int)(t / ho);
+    const int iy = oy * stride + ky - pad;
+    float v[SEG];
+#pragma unroll
+    for (int j = 0; j < SEG; ++j) v[j] = 0.f;
+    if (iy >= 0 && iy < h) {
+      const uint8_t* row = img + (size_t)(ni * h + iy) * w * 3;
+      const int x0 = ox * stride - pad;
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) {
+        const int ix = x0 + kx;
+        if (ix >= 0 && ix < w) {
+          v[kx * 3 + 0] = ((float)row[ix * 3 + 0] - m0) * s0;
+          v[kx * 3 + 1] = ((float)row[ix * 3 + 1] - m1) * s1;
+          v[kx * 3 + 2] = ((float)row[ix * 3 + 2] - m2) * s2;
+        }
+      }
     }
-    cols[i] = __float2bfloat16_rn(v);
+    uint4* dst = reinterpret_cast<uint4*>(cols + (size_t)pix * cols_ld + ky * SEG);
+#pragma unroll
+    for (int j = 0; j < SEG / 8; ++j) {
+      uint4 o;
+      o.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
+      o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
+      o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
+      o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
+      dst[j] = o;
+    }
   }
 }
 
@@ -93,10 +116,19 @@ cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, i
                                const float* mean, const float* inv_std, void* cols, int cols_ld,
                                cudaStream_t s) {
   const int ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
-  const long long total = (long long)n * ho * wo * cols_ld;
-  const int blocks = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
-  stem_im2col_kernel<<<blocks, 256, 0, s>>>(img, n, h, w, k, stride, pad, ho, wo, mean, inv_std,
-                                            reinterpret_cast<__nv_bfloat16*>(cols), cols_ld);
+  const long long total = (long long)n * ho * wo * k;
+  const int blocks = (int)((total + 255) / 256 < 148 * 64 ? (total + 255) / 256 : 148 * 64);
+  auto* c = reinterpret_cast<__nv_bfloat16*>(cols);
+  switch (k) {
+    case 7:
+      stem_im2col_kernel<7><<<blocks, 256, 0, s>>>(img, n, h, w, stride, pad, ho, wo, mean, inv_std, c, cols_ld);
+      break;
+    case 3:
+      stem_im2col_kernel<3><<<blocks, 256, 0, s>>>(img, n, h, w, stride, pad, ho, wo, mean, inv_std, c, cols_ld);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -594,7 +594,9 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
 int laud_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride, int pad,
                      const float* mean, const float* inv_std, void* cols, int cols_ld,
                      void* stream) {
-  if (cols_ld < k * k * 3 || cols_ld % 8) return fail(LAUD_ERR_SHAPE, "bad im2col leading dim");
+  if ((k != 3 && k != 7) || cols_ld != k * ((k * 3 + 7) / 8 * 8))
+    return fail(LAUD_ERR_SHAPE, "stem im2col: k must be 3 or 7 and cols_ld = k * pad8(3k)");
+  ProfScope ps(3, (cudaStream_t)stream);
   return cuda_check(launch_stem_im2col(img, n, h, w, k, stride, pad, mean, inv_std, cols, cols_ld,
                                        (cudaStream_t)stream),
                     "stem im2col", 1);
@@ -602,10 +604,12 @@ int laud_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride,
 
 int laud_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, void* stream) {
   if (c % 8) return fail(LAUD_ERR_SHAPE, "channels must be a multiple of 8");
+  ProfScope ps(3, (cudaStream_t)stream);
   return cuda_check(launch_maxpool3s2(x, n, h, w, c, y, (cudaStream_t)stream), "maxpool", 1);
 }
 
 int laud_global_avgpool(const void* x, int n, int hw, int c, void* y, void* stream) {
+  ProfScope ps(3, (cudaStream_t)stream);
   return cuda_check(launch_gap(x, n, hw, c, y, (cudaStream_t)stream), "global avgpool", 1);
 }
 

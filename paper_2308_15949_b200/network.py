@@ -103,10 +103,13 @@ class LaudNetwork:
         # stem: k x k / s2 conv over 3 channels via im2col (K = k*k*3 padded to 8)
         st = net.stem
         self.stem_k, self.stem_stride = st.kernel, st.stride
-        self.stem_cols = D.pad8(st.kernel * st.kernel * 3)
-        ws = params["stem_w"]
-        wcol = np.zeros((st.out_channels, 1, 1, self.stem_cols))
-        wcol[:, 0, 0, : st.kernel * st.kernel * 3] = ws.transpose(0, 2, 3, 1).reshape(st.out_channels, -1)
+        # im2col K layout per kernel row: ky * seg + kx * 3 + c, seg = pad8(3k)
+        seg = D.pad8(st.kernel * 3)
+        self.stem_cols = st.kernel * seg
+        ws = params["stem_w"]  # (co, 3, k, k)
+        wcol = np.zeros((st.out_channels, st.kernel, seg))
+        wcol[:, :, : st.kernel * 3] = ws.transpose(0, 2, 3, 1).reshape(st.out_channels, st.kernel, -1)
+        wcol = wcol.reshape(st.out_channels, 1, 1, self.stem_cols)
         self.stem_w = D.pack_weight(wcol.transpose(0, 3, 1, 2), self.stem_cols, device)
         self.stem_c = D.pad8(st.out_channels)
         self.stem_scale = D.fvec(np.ones(st.out_channels), st.out_channels, 1.0, device)
