@@ -149,6 +149,55 @@ struct DilateFlag {
 // ---------------------------------------------------------------------------
 // K1b: stable compaction with decoupled look-back
 // ---------------------------------------------------------------------------
+// Decoupled look-back, one warp: publish this tile's aggregate, then scan the
+// predecessors 32 at a time (one lane each) until the nearest inclusive
+// prefix; returns the exclusive prefix (same value in every lane).
+__device__ __forceinline__ int warp_lookback(ScanState* st, int tile, int agg, int lane) {
+  if (lane == 0)
+    atomicExch(&st->tiles[tile], (tile == 0 ? FLAG_INC : FLAG_AGG) | (unsigned)agg);
+  int excl = 0;
+  if (tile > 0) {
+    volatile unsigned long long* tiles = st->tiles;
+    for (int j = tile - 1;; j -= 32) {
+      const int idx = j - lane;  // lane 0 = nearest predecessor
+      unsigned long long sw = FLAG_INC;
+      if (idx >= 0) {
+        do {
+          sw = tiles[idx];
+        } while ((sw >> 32) == 0);
+      }
+      const unsigned inc = __ballot_sync(0xffffffffu, (sw >> 32) == 2);
+      const int stop = inc ? __ffs(inc) - 1 : 31;
+      int v = (lane <= stop && idx >= 0) ? (int)(sw & 0xffffffffu) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      excl += v;
+      if (inc) break;
+    }
+    if (lane == 0) atomicExch(&st->tiles[tile], FLAG_INC | (unsigned)(excl + agg));
+  }
+  return excl;
+}
+
+// The last CTA to finish restores the look-back scratch for the next launch.
+__device__ __forceinline__ void scan_state_release(ScanState* st, int num_tiles, int* s_flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(&st->done_ctr, 1u);
+    *s_flag = (done == (unsigned)num_tiles - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (*s_flag) {
+    for (int i = threadIdx.x; i < num_tiles; i += blockDim.x) st->tiles[i] = 0ull;
+    if (threadIdx.x == 0) {
+      st->tile_ctr = 0;
+      st->done_ctr = 0;
+    }
+    __threadfence();
+  }
+}
+
 template <class Flag>
 __global__ void __launch_bounds__(CT_THREADS) compact_kernel(Flag flag, int total,
                                                              int* __restrict__ list,
@@ -188,23 +237,8 @@ __global__ void __launch_bounds__(CT_THREADS) compact_kernel(Flag flag, int tota
     }
     if (lane < CT_THREADS / 32) s_warp[lane] = wi - v;  // exclusive warp offsets
     const int agg = __shfl_sync(0xffffffffu, wi, CT_THREADS / 32 - 1);
+    const int excl = warp_lookback(st, tile, agg, lane);
     if (lane == 0) {
-      volatile unsigned long long* tiles = st->tiles;
-      int excl = 0;
-      if (tile == 0) {
-        atomicExch(&st->tiles[0], FLAG_INC | (unsigned)agg);
-      } else {
-        atomicExch(&st->tiles[tile], FLAG_AGG | (unsigned)agg);
-        for (int j = tile - 1; j >= 0; --j) {
-          unsigned long long sw;
-          do {
-            sw = tiles[j];
-          } while ((sw >> 32) == 0);
-          excl += (int)(sw & 0xffffffffu);
-          if ((sw >> 32) == 2) break;
-        }
-        atomicExch(&st->tiles[tile], FLAG_INC | (unsigned)(excl + agg));
-      }
       s_excl = excl;
       if (tile == num_tiles - 1) *count = excl + agg;
     }
@@ -214,29 +248,100 @@ __global__ void __launch_bounds__(CT_THREADS) compact_kernel(Flag flag, int tota
 #pragma unroll
   for (int j = 0; j < CT_ITEMS; ++j)
     if (f[j]) list[pos++] = base + j;
-  // the last CTA to finish restores the scratch for the next launch
+  scan_state_release(st, num_tiles, &s_tile);
+}
+
+// ---------------------------------------------------------------------------
+// K1 fused: masker dot products + decision + compaction in one pass over x
+// (cells that fit one warp work item).  TC cells per CTA, one warp per cell.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) masker_fused_kernel(
+    const T* __restrict__ x, int ld, int n, int h, int w, int c, int win, int cells_h, int cells_w,
+    const float* __restrict__ wdiff, float bias, float inv_area, int tc, uint8_t* __restrict__ coarse,
+    float* __restrict__ dots, int* __restrict__ list, int* __restrict__ count, ScanState* st,
+    int num_tiles) {
+  extern __shared__ float s_w[];           // c floats
+  __shared__ unsigned char s_flag[256];
+  __shared__ int s_tile, s_excl, s_rel;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(&st->tile_ctr, 1u);
+  for (int i = threadIdx.x; i < c; i += blockDim.x) s_w[i] = wdiff[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned done = atomicAdd(&st->done_ctr, 1u);
-    s_tile = (done == (unsigned)num_tiles - 1) ? 1 : 0;
-  }
-  __syncthreads();
-  if (s_tile) {
-    for (int i = threadIdx.x; i < num_tiles; i += CT_THREADS) st->tiles[i] = 0ull;
-    if (threadIdx.x == 0) {
-      st->tile_ctr = 0;
-      st->done_ctr = 0;
+  const int tile = s_tile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = n * cells_h * cells_w;
+  const int cell0 = tile * tc;
+  const int cpp = c >> 3;
+  const int cell_chunks = win * win * cpp;
+  const int cpi = cells_h * cells_w;
+  for (int lc = warp; lc < tc; lc += 8) {
+    const int cell = cell0 + lc;
+    bool f = false;
+    if (cell < total) {
+      const int ni = cell / cpi;
+      const int cr = cell - ni * cpi;
+      const int ci = cr / cells_w, cj = cr - (cr / cells_w) * cells_w;
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll 4
+      for (int q = lane; q < cell_chunks; q += 64) {
+        const int px = q / cpp;
+        const int ch = (q - px * cpp) << 3;
+        const int py = px / win;
+        a0 += dot8<T>(x + ((size_t)(ni * h + ci * win + py) * w + cj * win + (px - py * win)) * ld + ch,
+                      s_w + ch);
+        const int q2 = q + 32;
+        if (q2 < cell_chunks) {
+          const int px2 = q2 / cpp;
+          const int ch2 = (q2 - px2 * cpp) << 3;
+          const int py2 = px2 / win;
+          a1 += dot8<T>(x + ((size_t)(ni * h + ci * win + py2) * w + cj * win + (px2 - py2 * win)) * ld + ch2,
+                        s_w + ch2);
+        }
+      }
+      float acc = a0 + a1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      f = acc * inv_area + bias >= 0.f;
+      if (lane == 0) {
+        coarse[cell] = f ? 1 : 0;
+        if (dots) dots[cell] = acc;
+      }
     }
-    __threadfence();
+    if (lane == 0) s_flag[lc] = f ? 1 : 0;
   }
+  __syncthreads();
+  // tile-local exclusive scan of tc (<= 256) flags: thread t owns flag t
+  const bool mine = threadIdx.x < tc && s_flag[threadIdx.x];
+  const unsigned bal = __ballot_sync(0xffffffffu, mine);
+  __shared__ int s_wc[8];
+  if (lane == 0) s_wc[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < 8 ? s_wc[lane] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane < 8) s_wc[lane] = incl - v;
+    const int agg = __shfl_sync(0xffffffffu, incl, 7);
+    const int excl = warp_lookback(st, tile, agg, lane);
+    if (lane == 0) {
+      s_excl = excl;
+      if (tile == num_tiles - 1) *count = excl + agg;
+    }
+  }
+  __syncthreads();
+  if (mine) list[s_excl + s_wc[warp] + __popc(bal & ((1u << lane) - 1u))] = cell0 + threadIdx.x;
+  scan_state_release(st, num_tiles, &s_rel);
 }
 
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 size_t scan_state_bytes(int total) {
-  const int tiles = (total + CT_TILE - 1) / CT_TILE;
+  const int tiles = total / 8 + 2;  // fused masker tiles hold >= 8 items
   return sizeof(ScanState) + sizeof(unsigned long long) * (tiles > 0 ? tiles : 1);
 }
 
@@ -266,7 +371,24 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
   const int cells_h = h / win, cells_w = w / win;
   int cps = 0;
   const int splits = masker_splits(win, c, &cps);
-  const long long items = (long long)n * cells_h * cells_w * splits;
+  const int total = n * cells_h * cells_w;
+  if (splits == 1 && total > 0 && total <= 4096) {  // small grids: one launch wins
+    // one pass: dots + decisions + compaction; ~2 waves of CTAs over the SMs
+    // one cell per warp: as many resident warps (bytes in flight) as the SMs hold
+    const int tc = 8;
+    const int tiles = (total + tc - 1) / tc;
+    const float inv_area = 1.0f / (float)(win * win);
+    if (x_f32)
+      masker_fused_kernel<float><<<tiles, 256, c * sizeof(float), stream>>>(
+          reinterpret_cast<const float*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff, bias,
+          inv_area, tc, coarse, partial, list, count, reinterpret_cast<ScanState*>(scan), tiles);
+    else
+      masker_fused_kernel<__nv_bfloat16><<<tiles, 256, c * sizeof(float), stream>>>(
+          reinterpret_cast<const __nv_bfloat16*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff,
+          bias, inv_area, tc, coarse, partial, list, count, reinterpret_cast<ScanState*>(scan), tiles);
+    return cudaGetLastError();
+  }
+  const long long items = (long long)total * splits;
   const int blocks = (int)((items + 7) / 8);
   if (x_f32)
     cell_dot_kernel<float><<<blocks, 256, c * sizeof(float), stream>>>(
@@ -279,7 +401,7 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse};
-  return launch_compact(f, n * cells_h * cells_w, list, count, scan, stream);
+  return launch_compact(f, total, list, count, scan, stream);
 }
 
 cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,
