@@ -109,6 +109,16 @@ typedef struct laud_conv_args {
   const uint8_t* relu_inactive_coarse;
   const uint8_t* ymask_coarse;  /* dense-masked: y *= coarse[cell]       */
   const uint8_t* ymask_channel; /* dense-masked: y *= mask[n][channel]   */
+  /* per-sample dynamic width (channel skipping): rows padded per sample to
+   * sample_rows (multiple of 128); k_n = chan_count[n]; n_dyn skips output
+   * columns >= k_n, k_dyn runs K = taps * roundup(k_n, 64); b_batched: weight
+   * is [batch][n_out][K]; col_index[n][col_index_ld] maps output column ->
+   * scale/bias channel. */
+  int sample_rows;
+  const int* chan_count;
+  int n_dyn, k_dyn, b_batched;
+  const int* col_index;
+  int col_index_ld;
   int misplace_first;
 } laud_conv_args;
 
@@ -148,7 +158,34 @@ typedef struct laud_block_args {
   float* partial;
   void* scan;
   int misplace_first; /* test-only fault hook (reference.py:362, 400-401) */
+  /* channel paradigm (reference.py:189-218, 404-423): masker MLP weights
+   * fp32 w1 [hidden][c_in], w2 [2D][hidden]; G channels per decision; either
+   * a given expanded mask [n][c_mid] (uint8) or the masker runs.  Outputs:
+   * coarse [n][D], expanded [n][c_mid], kept lists sel [n][c_mid] + count [n],
+   * optional logit gaps dvals [n][D]; wpack = laud_channel_pack_bytes(). */
+  const float* ch_w1;
+  const float* ch_w2;
+  int ch_hidden, ch_d, ch_groups;
+  const uint8_t* given_chmask;
+  uint8_t* ch_coarse;
+  uint8_t* ch_expanded;
+  int* ch_sel;
+  int* ch_count;
+  float* ch_dvals;
+  void* wpack;
 } laud_block_args;
+
+/* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):
+ * GAP over hw pixels, relu(w1 gap), w2 hidden -> d interleaved pairs, keep iff
+ * l0 >= l1, G-fold expansion to cm (= d*g) channels padded to cm_p, ordered
+ * kept-channel lists sel [n][cm_p] and counts [n]; dvals = l0 - l1 (nullable). */
+int laud_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c, const float* w1,
+                        int hidden, const float* w2, int d, int g, int cm, int cm_p,
+                        uint8_t* coarse, float* dvals, uint8_t* expanded, int* sel, int* count,
+                        void* stream);
+
+/* Bytes of per-sample packed weights the channel paradigm needs. */
+size_t laud_channel_pack_bytes(int n, int c_in, int c_mid, int c_out);
 
 int laud_block_forward(const laud_block_args* a, void* stream);
 

@@ -33,7 +33,9 @@ class ConvArgs(C.Structure):
         ("weight", _vp), ("n_out", C.c_int), ("scale", _vp), ("bias", _vp), ("relu", C.c_int),
         ("out_mode", C.c_int), ("out", _vp), ("out_ld", C.c_int), ("out_f32", C.c_int),
         ("resid", _vp), ("resid_ld", C.c_int), ("relu_inactive_coarse", _vp),
-        ("ymask_coarse", _vp), ("ymask_channel", _vp), ("misplace_first", C.c_int),
+        ("ymask_coarse", _vp), ("ymask_channel", _vp), ("sample_rows", C.c_int),
+        ("chan_count", _vp), ("n_dyn", C.c_int), ("k_dyn", C.c_int), ("b_batched", C.c_int),
+        ("col_index", _vp), ("col_index_ld", C.c_int), ("misplace_first", C.c_int),
     ]
 
 
@@ -49,7 +51,10 @@ class BlockArgs(C.Structure):
         ("masker_wdiff", _vp), ("masker_bias", C.c_float), ("given_coarse", _vp),
         ("coarse_out", _vp), ("cell_list", _vp), ("cell_count", _vp), ("pix_list", _vp),
         ("pix_count", _vp), ("h1", _vp), ("h2", _vp), ("partial", _vp), ("scan", _vp),
-        ("misplace_first", C.c_int),
+        ("misplace_first", C.c_int), ("ch_w1", _vp), ("ch_w2", _vp), ("ch_hidden", C.c_int),
+        ("ch_d", C.c_int), ("ch_groups", C.c_int), ("given_chmask", _vp), ("ch_coarse", _vp),
+        ("ch_expanded", _vp), ("ch_sel", _vp), ("ch_count", _vp), ("ch_dvals", _vp),
+        ("wpack", _vp),
     ]
 
 
@@ -67,6 +72,9 @@ _SIGS = {
     "laud_launch_count": (C.c_uint64, []),
     "laud_scan_workspace_bytes": (C.c_size_t, [C.c_int]),
     "laud_masker_partial_floats": (C.c_size_t, [C.c_int] * 6),
+    "laud_channel_pack_bytes": (C.c_size_t, [C.c_int] * 4),
+    "laud_channel_masker": (C.c_int, [_vp] + [C.c_int] * 5 + [_vp, C.c_int, _vp] + [C.c_int] * 4
+                            + [_vp] * 6),
     "laud_spatial_masker": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.c_int, _vp, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp]),
     "laud_cells_from_mask": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp]),

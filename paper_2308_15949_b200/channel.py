@@ -72,9 +72,72 @@ def dense_block(db: D.DeviceBlock, x: torch.Tensor, ymask: Optional[torch.Tensor
     return out
 
 
+def _rm():
+    from . import reference as R
+    return R
+
+
 def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None):
-    raise DeviceError("channel masker kernel not built yet")
+    """GAP -> relu(W1 .) -> W2 -> D pairs -> keep iff l0 >= l1 -> repeat G.
+
+    Device version of `reference.py:189-218` (K5 kernel, fp32 math).  Train
+    mode replays the reference's Gumbel draw (`rng.gumbel(size=(N, D, 2))`)
+    on the device logit gaps.
+    """
+    import numpy as np
+    from .errors import ShapeMismatch
+    R = _rm()
+    if mode not in ("inference", "train"):
+        raise ValueError(f"unknown mode {mode!r}")
+    D.require_cuda()
+    w1, w2 = (np.asarray(w, dtype=np.float64) for w in weights)
+    hd, c = w1.shape
+    xn = np.asarray(x)
+    if xn.shape[1] != c:
+        raise ShapeMismatch(f"input has {xn.shape[1]} channels, masker expects {c}")
+    if w2.shape[1] != hd or w2.shape[0] % 2:
+        raise ShapeMismatch("second MLP layer must map hidden -> 2*D")
+    d = w2.shape[0] // 2
+    n, _, h, w = xn.shape
+    xd = D.to_device_nhwc(xn, dtype=torch.float32)
+    cp = xd.shape[-1]
+    cm = d * g
+    cmp = D.pad8(cm)
+    w1p = np.zeros((hd, cp), np.float32)
+    w1p[:, :c] = w1
+    t_w1 = torch.from_numpy(w1p).cuda()
+    t_w2 = torch.from_numpy(w2.astype(np.float32)).cuda()
+    coarse = torch.empty(n * d, dtype=torch.uint8, device="cuda")
+    dvals = torch.empty(n * d, dtype=torch.float32, device="cuda")
+    exp = torch.empty(n * cmp, dtype=torch.uint8, device="cuda")
+    sel = torch.empty(n * cmp, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(n, dtype=torch.int32, device="cuda")
+    _lib.call("laud_channel_masker", D.ptr(xd), 1, cp, n, h * w, cp, D.ptr(t_w1), hd, D.ptr(t_w2),
+              d, g, cm, cmp, D.ptr(coarse), D.ptr(dvals), D.ptr(exp), D.ptr(sel), D.ptr(cnt),
+              D.stream_handle())
+    soft = None
+    if mode == "inference":
+        cz = coarse.view(n, d).bool().cpu().numpy()
+    else:
+        dv = dvals.view(n, d).double().cpu().numpy()
+        cz, soft = R._decide_train(dv, tau, rng)
+    return R.ChannelMask(cz, np.repeat(cz, g, axis=1), g, soft)
 
 
 def channel_block_sparse(x, bw, block, mask):
-    raise DeviceError("channel-skipping block kernel not built yet")
+    """Channel-skipping block forward on the device (`reference.py:404-423`)."""
+    import numpy as np
+    from .errors import MaskShapeMismatch, ShapeMismatch
+    R = _rm()
+    if block.conv2.groups != 1:
+        raise ShapeMismatch("sparse channel execution requires groups == 1")
+    n = x.shape[0]
+    m = np.asarray(mask.expanded)
+    if m.shape != (n, block.conv2.out_channels):
+        raise MaskShapeMismatch(f"channel mask {m.shape} != {(n, block.conv2.out_channels)}")
+    db = R.device_block(bw, block)
+    mm = np.zeros((n, db.cmid_p), np.uint8)
+    mm[:, : m.shape[1]] = m
+    xd = D.to_device_nhwc(x)
+    y, *_ = db.forward(xd, "channel", chmask=torch.from_numpy(mm.reshape(-1)).cuda())
+    return D.from_device_nhwc(y, block.output_shape.channels)

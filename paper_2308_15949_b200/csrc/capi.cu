@@ -37,6 +37,15 @@ cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, i
                                cudaStream_t s);
 cudaError_t launch_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, cudaStream_t s);
 cudaError_t launch_gap(const void* x, int n, int hw, int c, void* y, cudaStream_t s);
+cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c,
+                                  const float* w1, int hd, const float* w2, int d, int g, int cm,
+                                  int cm_p, uint8_t* coarse, float* dvals, uint8_t* expanded,
+                                  int* sel, int* count, cudaStream_t s);
+cudaError_t launch_channel_lists(const uint8_t* expanded, int n, int cm_p, int* sel, int* count,
+                                 cudaStream_t s);
+cudaError_t launch_pack_weights(const void* src, int src_rows, int taps, int src_k, void* dst,
+                                int dst_rows, int dst_k, const int* sel, const int* count,
+                                int sel_ld, int row_sel, int col_sel, int n, cudaStream_t s);
 }  // namespace laud
 
 using namespace laud;
@@ -156,10 +165,11 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
 // Weights [rows][k] bf16, k contiguous; box = 64 (k) x bn (rows), 128B swizzle,
 // rows past the end read as zeros.
-int tensor_map_2d(const void* w, int rows, int k, int ld, int bn, CUtensorMap* out) {
+int tensor_map_2d(const void* w, int rows, int k, int ld, int bn, CUtensorMap* out,
+                  int batch = 0) {
   int dev = 0;
   cudaGetDevice(&dev);
-  MapKey key{w, rows, k * 65536 + ld, bn, dev};
+  MapKey key{w, rows + batch * 1000003, k * 65536 + ld, bn, dev};
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = g_maps.find(key);
@@ -173,13 +183,14 @@ int tensor_map_2d(const void* w, int rows, int k, int ld, int bn, CUtensorMap* o
   if ((reinterpret_cast<uintptr_t>(w) & 15) != 0)
     return fail(LAUD_ERR_ARG, "weight pointer must be 16-byte aligned");
   CUtensorMap m;
-  cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)bn};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)(batch > 0 ? batch : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * rows};
+  cuuint32_t box[3] = {64, (cuuint32_t)bn, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, batch > 0 ? 3 : 2, const_cast<void*>(w),
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(LAUD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
@@ -252,11 +263,20 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   p.relu_inactive_coarse = a->relu_inactive_coarse;
   p.ymask_coarse = a->ymask_coarse;
   p.ymask_channel = a->ymask_channel;
+  p.sample_rows = a->sample_rows;
+  p.chan_count = a->chan_count;
+  p.n_dyn = a->n_dyn;
+  p.k_dyn = a->k_dyn;
+  p.b_batched = a->b_batched;
+  p.col_index = a->col_index;
+  p.col_index_ld = a->col_index_ld;
+  if (a->sample_rows % 128) return fail(LAUD_ERR_ARG, "sample_rows must be a multiple of 128");
+  if ((a->n_dyn || a->k_dyn) && !a->chan_count) return fail(LAUD_ERR_ARG, "chan_count missing");
   p.misplace_first = a->misplace_first;
   const int bn = pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   CUtensorMap m;
   const int kw = a->ksize * a->ksize * p.kpad;
-  int rc = tensor_map_2d(a->weight, a->n_out, kw, kw, bn, &m);
+  int rc = tensor_map_2d(a->weight, a->n_out, kw, kw, bn, &m, a->b_batched ? a->batch : 0);
   if (rc) return rc;
   // A operand: [a_rows][in_c] with row stride in_ld, gathered 4 rows at a time
   CUtensorMap ma;
@@ -267,8 +287,10 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   }();
   p.a_tma = a_tma_env && (reinterpret_cast<uintptr_t>(a->act) % 16 == 0);
   if (p.a_tma) {
-    const long long arows = a->a_compact ? (long long)a->rows_max
-                                         : (long long)a->batch * a->in_h * a->in_w;
+    const long long arows =
+        a->a_compact ? (a->sample_rows > 0 ? (long long)a->batch * a->out_h * a->out_w
+                                           : (long long)a->rows_max)
+                     : (long long)a->batch * a->in_h * a->in_w;
     if (arows >= (1ll << 31) - 1) {
       p.a_tma = 0;
     } else {
@@ -389,13 +411,181 @@ int laud_dilate_pixels(const uint8_t* coarse, int n, int h_in, int w_in, int s, 
 
 int laud_conv(const laud_conv_args* a, void* stream) { return run_conv(a, (cudaStream_t)stream); }
 
+static int round64(int v) { return (v + 63) / 64 * 64; }
+
+int laud_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c, const float* w1,
+                        int hidden, const float* w2, int d, int g, int cm, int cm_p,
+                        uint8_t* coarse, float* dvals, uint8_t* expanded, int* sel, int* count,
+                        void* stream) {
+  if (c % 8 || ld % 8 || ld < c) return fail(LAUD_ERR_SHAPE, "channels must be multiples of 8");
+  if (d < 1 || g < 1 || cm != d * g || cm > cm_p) return fail(LAUD_ERR_GRANULARITY, "bad D/G");
+  if ((size_t)(c + hidden + d) * 4 > 48 * 1024) return fail(LAUD_ERR_SHAPE, "masker too wide");
+  ProfScope ps(1, (cudaStream_t)stream);
+  return cuda_check(launch_channel_masker(x, x_f32, ld, n, hw, c, w1, hidden, w2, d, g, cm, cm_p,
+                                          coarse, dvals, expanded, sel, count,
+                                          (cudaStream_t)stream),
+                    "channel masker", 1);
+}
+
+size_t laud_channel_pack_bytes(int n, int c_in, int c_mid, int c_out) {
+  const size_t w1 = (size_t)c_mid * round64(c_in);
+  const size_t w2 = (size_t)c_mid * 9 * round64(c_mid);
+  const size_t w3 = (size_t)c_out * round64(c_mid);
+  return (size_t)n * (w1 + w2 + w3) * 2 + 256;
+}
+
+// Channel skipping (`reference.py:404-423`): per sample, conv1 over the kept
+// filters W1[sel], conv2 with W2[sel][:, sel], conv3 with W3[:, sel] — packed
+// per sample, run as dynamic-width tcgen05 GEMMs (ragged N / K per sample).
+static int channel_forward(const laud_block_args* a, cudaStream_t st) {
+  const int n = a->n, cmp = a->c_mid;
+  const int ho = (a->h_in - 1) / a->stride + 1, wo = (a->w_in - 1) / a->stride + 1;
+  if (!a->ch_sel || !a->ch_count || !a->ch_expanded || !a->wpack || !a->h1 || !a->h2)
+    return fail(LAUD_ERR_ARG, "channel workspace missing");
+  int rc;
+  if (a->given_chmask) {
+    if ((rc = cuda_check(launch_channel_lists(a->given_chmask, n, cmp, a->ch_sel, a->ch_count, st),
+                         "channel lists", 1)))
+      return rc;
+  } else {
+    if (!a->ch_w1 || !a->ch_w2 || !a->ch_coarse || a->ch_d < 1 || a->ch_groups < 1)
+      return fail(LAUD_ERR_ARG, "channel masker weights missing");
+    const int cm = a->ch_d * a->ch_groups;
+    if (cm > cmp) return fail(LAUD_ERR_GRANULARITY, "D*G exceeds the mid width");
+    ProfScope ps(1, st);
+    if ((rc = cuda_check(launch_channel_masker(a->x, 0, a->x_ld, n, a->h_in * a->w_in, a->c_in,
+                                               a->ch_w1, a->ch_hidden, a->ch_w2, a->ch_d,
+                                               a->ch_groups, cm, cmp, a->ch_coarse, a->ch_dvals,
+                                               a->ch_expanded, a->ch_sel, a->ch_count, st),
+                         "channel masker", 1)))
+      return rc;
+  }
+  // skip path
+  if (a->has_down) {
+    laud_conv_args d;
+    memset(&d, 0, sizeof(d));
+    d.row_mode = ROWS_DENSE;
+    d.rows_max = n * ho * wo;
+    d.batch = n;
+    d.out_h = ho;
+    d.out_w = wo;
+    d.act = a->x;
+    d.in_h = a->h_in;
+    d.in_w = a->w_in;
+    d.in_c = a->c_in;
+    d.in_ld = a->x_ld;
+    d.ksize = 1;
+    d.stride = a->stride;
+    d.weight = a->wd;
+    d.n_out = a->c_out;
+    d.scale = a->sd;
+    d.bias = a->bd;
+    d.out_mode = OUT_PIXEL;
+    d.out = a->out;
+    d.out_ld = a->c_out;
+    if ((rc = run_conv(&d, st))) return rc;
+  } else if (a->out != a->x) {
+    if ((rc = cuda_check(cudaMemcpyAsync(a->out, a->x, (size_t)n * ho * wo * a->c_out * 2,
+                                         cudaMemcpyDeviceToDevice, st),
+                         "skip copy", 0)))
+      return rc;
+  }
+  // per-sample packed weights
+  const int k1 = round64(a->c_in), k2 = round64(cmp);
+  char* wp = reinterpret_cast<char*>(a->wpack);
+  void* w1s = wp;
+  void* w2s = wp + (size_t)n * cmp * k1 * 2;
+  void* w3s = wp + (size_t)n * cmp * k1 * 2 + (size_t)n * cmp * 9 * k2 * 2;
+  {
+    ProfScope ps(3, st);
+    if ((rc = cuda_check(launch_pack_weights(a->w1, cmp, 1, k1, w1s, cmp, k1, a->ch_sel, a->ch_count,
+                                             cmp, 1, 0, n, st), "pack w1", 1)) ||
+        (rc = cuda_check(launch_pack_weights(a->w2, cmp, 9, k2, w2s, cmp, k2, a->ch_sel, a->ch_count,
+                                             cmp, 1, 1, n, st), "pack w2", 1)) ||
+        (rc = cuda_check(launch_pack_weights(a->w3, a->c_out, 1, k2, w3s, a->c_out, k2, a->ch_sel,
+                                             a->ch_count, cmp, 0, 1, n, st), "pack w3", 1)))
+      return rc;
+  }
+  const int sr1 = (a->h_in * a->w_in + 127) / 128 * 128;
+  const int sr2 = (ho * wo + 127) / 128 * 128;
+  laud_conv_args c1;
+  memset(&c1, 0, sizeof(c1));
+  c1.row_mode = ROWS_DENSE;
+  c1.sample_rows = sr1;
+  c1.rows_max = n * sr1;
+  c1.batch = n;
+  c1.out_h = a->h_in;
+  c1.out_w = a->w_in;
+  c1.act = a->x;
+  c1.in_h = a->h_in;
+  c1.in_w = a->w_in;
+  c1.in_c = a->c_in;
+  c1.in_ld = a->x_ld;
+  c1.ksize = 1;
+  c1.stride = 1;
+  c1.weight = w1s;
+  c1.b_batched = 1;
+  c1.n_out = cmp;
+  c1.chan_count = a->ch_count;
+  c1.n_dyn = 1;
+  c1.col_index = a->ch_sel;
+  c1.col_index_ld = cmp;
+  c1.scale = a->s1;
+  c1.bias = a->b1;
+  c1.relu = a->relu1;
+  c1.out_mode = OUT_ROW;
+  c1.out = a->h1;
+  c1.out_ld = cmp;
+  if ((rc = run_conv(&c1, st))) return rc;
+  laud_conv_args c2 = c1;
+  c2.sample_rows = sr2;
+  c2.rows_max = n * sr2;
+  c2.out_h = ho;
+  c2.out_w = wo;
+  c2.act = a->h1;
+  c2.in_c = cmp;
+  c2.in_ld = cmp;
+  c2.ksize = 3;
+  c2.stride = a->stride;
+  c2.pad = 1;
+  c2.weight = w2s;
+  c2.k_dyn = 1;
+  c2.scale = a->s2;
+  c2.bias = a->b2;
+  c2.relu = a->relu2;
+  c2.out = a->h2;
+  if ((rc = run_conv(&c2, st))) return rc;
+  laud_conv_args c3 = c2;
+  c3.act = a->h2;
+  c3.in_h = ho;
+  c3.in_w = wo;
+  c3.a_compact = 1;
+  c3.ksize = 1;
+  c3.stride = 1;
+  c3.pad = 0;
+  c3.weight = w3s;
+  c3.n_out = a->c_out;
+  c3.n_dyn = 0;
+  c3.col_index = nullptr;
+  c3.scale = a->s3;
+  c3.bias = a->b3;
+  c3.relu = a->relu_out;
+  c3.out_mode = OUT_PIXEL;
+  c3.out = a->out;
+  c3.out_ld = a->c_out;
+  c3.resid = a->out;
+  c3.resid_ld = a->c_out;
+  return run_conv(&c3, st);
+}
+
 int laud_block_forward(const laud_block_args* a, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!a || !a->x || !a->out || !a->w1 || !a->w2 || !a->w3)
     return fail(LAUD_ERR_ARG, "null pointer in block args");
-  if (a->paradigm == LAUD_PARADIGM_CHANNEL)
-    return fail(LAUD_ERR_UNSUPPORTED, "channel paradigm uses laud_channel_block");
-  if (a->groups != 1) return fail(LAUD_ERR_UNSUPPORTED, "grouped conv2 not supported yet");
+  if (a->groups != 1)
+    return fail(LAUD_ERR_UNSUPPORTED, a->paradigm == LAUD_PARADIGM_CHANNEL
+                                          ? "sparse channel execution requires groups == 1"
+                                          : "grouped conv2 not supported yet");
   if (a->stride != 1 && a->stride != 2) return fail(LAUD_ERR_ARG, "stride must be 1 or 2");
   if (a->stride > 1 && !a->has_down)
     return fail(LAUD_ERR_SHAPE, "a strided block needs a downsample path");
@@ -403,6 +593,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   const int ho = (a->h_in - 1) / a->stride + 1, wo = (a->w_in - 1) / a->stride + 1;
   if (!a->has_down && (a->c_in != a->c_out || a->x_ld != a->c_out))
     return fail(LAUD_ERR_SHAPE, "identity skip needs c_in == c_out == x_ld");
+  if (a->paradigm == LAUD_PARADIGM_CHANNEL) return channel_forward(a, st);
   const int n = a->n;
   int rc;
 

@@ -35,6 +35,7 @@ constexpr int NUM_THREADS = 14 * 32;
 
 struct RowPos {
   int n, y, x;
+  int pix;  // linear output pixel (n*out_h + y)*out_w + x
 };
 
 __device__ __forceinline__ int rows_valid(const ConvParams& p) {
@@ -63,15 +64,43 @@ __device__ __forceinline__ bool map_row(const ConvParams& p, int m, int nvalid, 
     int ly = l / p.patch_w;
     o.y = ci * p.patch_h + ly;
     o.x = cj * p.patch_w + (l - ly * p.patch_w);
+    o.pix = (o.n * p.out_h + o.y) * p.out_w + o.x;
     first_patch = (pi == 0);
     return true;
   }
-  int pix = (p.row_mode == ROWS_PIXEL) ? __ldg(p.list + m) : m;
+  int pix;
+  if (p.sample_rows > 0) {  // per-sample padded rows: one sample per M tile range
+    const int smp = m / p.sample_rows;
+    const int loc = m - smp * p.sample_rows;
+    if (loc >= hw) return false;
+    pix = smp * hw + loc;
+  } else {
+    pix = (p.row_mode == ROWS_PIXEL) ? __ldg(p.list + m) : m;
+  }
+  o.pix = pix;
   o.n = pix / hw;
   int r = pix - o.n * hw;
   o.y = r / p.out_w;
   o.x = r - o.y * p.out_w;
   return true;
+}
+
+// Per-tile schedule shared by every warp role (all roles skip the same tiles).
+struct TileInfo {
+  int m0, n0, sample, kpt, num_kb, kc;
+  bool skip;
+};
+template <int BN>
+__device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int t, int n_tiles) {
+  TileInfo ti;
+  ti.m0 = (t / n_tiles) * BM;
+  ti.n0 = (t % n_tiles) * BN;
+  ti.sample = p.sample_rows > 0 ? ti.m0 / p.sample_rows : 0;
+  ti.kc = p.chan_count ? __ldg(p.chan_count + ti.sample) : 0;
+  ti.skip = p.chan_count && p.n_dyn && ti.n0 >= ti.kc;
+  ti.kpt = (p.chan_count && p.k_dyn) ? (ti.kc + BK - 1) / BK : p.kpad / BK;
+  ti.num_kb = p.ksize * p.ksize * ti.kpt;
+  return ti;
 }
 
 template <int BN, int STAGES, int NSTG>
@@ -136,7 +165,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int kpt = p.kpad / BK;  // k-blocks per tap
 
   if (warp < 4) {
     // ------------------------------------------------------------ A producers
@@ -146,22 +174,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // One output row per thread; per (tap, channel block) every 4th lane issues
       // a TMA tile::gather4 of its 4 rows' source pixels (OOB index -> zeros).
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t / n_tiles) * BM;
+        const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+        if (ti.skip) continue;
+        const int m0 = ti.m0;
         RowPos rp;
         bool fp;
         const bool rv = map_row(p, m0 + tid, nvalid, rp, fp);
-        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
-          const int tap = kb / kpt;
-          const int c0 = (kb - tap * kpt) * BK;
+          const int tap = kb / ti.kpt;
+          const int c0 = (kb - tap * ti.kpt) * BK;
           const int ky = tap / p.ksize;
           const int kx = tap - ky * p.ksize;
           int row = p.a_rows;  // out of bounds -> zero fill
           if (rv) {
             if (p.a_compact) {
-              row = m0 + tid;
+              row = p.sample_rows > 0 ? rp.pix : m0 + tid;
             } else {
               const int iy = rp.y * p.stride + ky - p.pad;
               const int ix = rp.x * p.stride + kx - p.pad;
@@ -182,7 +212,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int rsub = tid >> 3;
     const __nv_bfloat16* act = reinterpret_cast<const __nv_bfloat16*>(p.act);
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t / n_tiles) * BM;
+      const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+      if (ti.skip) continue;
+      const int m0 = ti.m0;
       RowPos rp[8];
       bool rv[8];
 #pragma unroll
@@ -190,12 +222,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         bool fp;
         rv[i] = map_row(p, m0 + rsub + 16 * i, nvalid, rp[i], fp);
       }
-      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+      for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
         const int stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
         mbar_wait(&empty[stage], phase ^ 1);
-        const int tap = kb / kpt;
-        const int ch = (kb - tap * kpt) * BK + chunk * 8;
+        const int tap = kb / ti.kpt;
+        const int ch = (kb - tap * ti.kpt) * BK + chunk * 8;
         const int ky = tap / p.ksize;
         const int kx = tap - ky * p.ksize;
         const bool chv = ch < p.in_c;
@@ -207,7 +239,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           bool v = rv[i] && chv;
           const __nv_bfloat16* src = act;
           if (p.a_compact) {
-            src = act + (size_t)(m0 + r) * p.in_ld + ch;
+            src = act + (size_t)(p.sample_rows > 0 ? rp[i].pix : m0 + r) * p.in_ld + ch;
           } else {
             const int iy = rp[i].y * p.stride + ky - p.pad;
             const int ix = rp[i].x * p.stride + kx - p.pad;
@@ -225,14 +257,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       uint32_t it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int n0 = (t % n_tiles) * BN;
-        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+        if (ti.skip) continue;
+        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], L::B_STAGE_BYTES);
-          tma_load_2d(base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES, &tmap_b, &full[stage],
-                      kb * BK, n0);
+          const int tap = kb / ti.kpt;
+          const int kcoord = tap * p.kpad + (kb - tap * ti.kpt) * BK;  // packed per-tap stride kpad
+          const uint32_t dst = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
+          if (p.b_batched)
+            tma_load_3d(dst, &tmap_b, &full[stage], kcoord, ti.n0, ti.sample);
+          else
+            tma_load_2d(dst, &tmap_b, &full[stage], kcoord, ti.n0);
         }
       }
     }
@@ -240,13 +278,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
     uint32_t it = 0, local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+      if (ti.skip) continue;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      ++local;
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
-      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+      for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
         const int stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
         mbar_wait(&full[stage], phase);
@@ -302,7 +343,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ri.dst = 0;
       if (ri.valid) {
         if (p.out_mode == OUT_ROW) {
-          ri.dst = m;
+          ri.dst = p.sample_rows > 0 ? ri.rp.pix : m;
         } else {
           int y = ri.rp.y;
           if (p.misplace_first && ri.fp) y = (y + p.patch_h) % p.out_h;
@@ -312,7 +353,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       return ri;
     };
     auto prefetch = [&](int t, const RowInfo& ri, int buf) {
-      const int c_base = (t % n_tiles) * BN + col0;
+      const int c_base = (t % n_tiles) * BN + col0;  // n0 + col0
       const int vchunks = max(0, min(HALF, p.n_out - c_base)) >> 3;
       const uint32_t sbase = base_u32 + stg_off0 + buf * L::STG_BUF;
 #pragma unroll 4
@@ -328,16 +369,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
+    auto next_valid = [&](int t) {
+      while (t < tiles && tile_info<BN>(p, t, n_tiles).skip) t += gridDim.x;
+      return t;
+    };
     uint32_t local = 0;
-    int t = blockIdx.x;
-    RowInfo cur = row_info(t);
-    if (pre) prefetch(t, cur, 0);
-    for (; t < tiles; t += gridDim.x, ++local) {
+    int t = next_valid(blockIdx.x);
+    RowInfo cur;
+    if (t < tiles) {
+      cur = row_info(t);
+      if (pre) prefetch(t, cur, 0);
+    }
+    for (; t < tiles; ++local) {
+      const TileInfo ti = tile_info<BN>(p, t, n_tiles);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int buf = NSTG == 2 ? (local & 1) : 0;
       uint8_t* stg = base + stg_off0 + buf * L::STG_BUF;
-      const int c_base = (t % n_tiles) * BN + col0;      // first output channel of this warp
+      const int c_base = ti.n0 + col0;                     // first output channel of this warp
       const int nch = max(0, min(HALF, p.n_out - c_base));  // valid channels (multiple of 8)
       const int vchunks = nch >> 3;
       bool do_relu = p.relu != 0;
@@ -350,8 +399,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       for (int i = lane; i < HALF; i += 32) {
         const int c = c_base + i;
-        vsc[i] = (p.scale && c < p.n_out) ? __ldg(p.scale + c) : 1.f;
-        vbi[i] = (p.bias && c < p.n_out) ? __ldg(p.bias + c) : 0.f;
+        int src = c;
+        bool live = c < p.n_out;
+        if (p.col_index) {  // per-sample channel list: column c holds channel col_index[c]
+          live = live && c < ti.kc;
+          src = live ? __ldg(p.col_index + (size_t)ti.sample * p.col_index_ld + c) : 0;
+        }
+        vsc[i] = (p.scale && live) ? __ldg(p.scale + src) : 1.f;
+        vbi[i] = (p.bias && live) ? __ldg(p.bias + src) : 0.f;
       }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
@@ -363,7 +418,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int j = 0; j < HALF / 32; ++j) {
         if (j * 32 >= nch) break;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + j * 32, r);
+        if (ti.num_kb > 0) {
+          tmem_ld_32x32b_x32(tbase + j * 32, r);
+        } else {  // empty K (no channel kept): y = 0
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = 0u;
+        }
         if (!cur.valid) continue;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -425,7 +485,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_arrive(&acc_empty[acc]);
       __syncwarp();
       // next tile's rows; with two staging buffers its residual streams in now
-      const int tn = t + gridDim.x;
+      const int tn = next_valid(t + gridDim.x);
       RowInfo nxt = cur;
       if (tn < tiles) {
         nxt = row_info(tn);
@@ -445,6 +505,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (tn < tiles && pre && NSTG == 1) prefetch(tn, nxt, 0);
       cur = nxt;
+      t = tn;
     }
   }
 

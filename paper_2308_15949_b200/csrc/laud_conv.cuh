@@ -57,6 +57,14 @@ struct ConvParams {
   //      y *= chmask[n][channel]                      (channel, per sample).
   const unsigned char* ymask_coarse;
   const unsigned char* ymask_channel;
+  // ---- per-sample dynamic width (channel skipping, `reference.py:404-423`)
+  int sample_rows;         // >0: rows padded per sample (multiple of 128), one sample per tile
+  const int* chan_count;   // [N] kept channels k_n
+  int n_dyn;               // output columns >= k_n are skipped (N ragged)
+  int k_dyn;               // K per tap = roundup(k_n, 64) (K ragged)
+  int b_batched;           // B is [N][n_out][K] (3D tensor map, sample coordinate)
+  const int* col_index;    // [N][col_index_ld]: scale/bias index of output column c
+  int col_index_ld;
   // ---- fault hook (tests only): shift the first patch's destination one cell
   int misplace_first;
 };

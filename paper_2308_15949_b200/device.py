@@ -194,9 +194,41 @@ class DeviceBlock:
     def out_hw(self, h: int, w: int):
         return self.block.conv2.out_hw(h, w)
 
+    def set_channel_masker(self, w1, w2, g: int):
+        """Channel masker MLP (`reference.py:189-218`): w1 [h, C_in], w2 [2D, h], G."""
+        w1 = np.asarray(w1, dtype=np.float32)
+        w2 = np.asarray(w2, dtype=np.float32)
+        if w1.shape[1] > self.cin_p:
+            raise DeviceError("channel masker width exceeds the block input")
+        w1p = np.zeros((w1.shape[0], self.cin_p), np.float32)
+        w1p[:, : w1.shape[1]] = w1
+        dev = self.w1.device
+        self.ch_w1 = torch.from_numpy(w1p).to(dev)
+        self.ch_w2 = torch.from_numpy(np.ascontiguousarray(w2)).to(dev)
+        self.ch_hidden, self.ch_d, self.ch_g = w1.shape[0], w2.shape[0] // 2, int(g)
+
+    def _channel_args(self, a, n, ws, chmask):
+        cmp = self.cmid_p
+        d = getattr(self, "ch_d", 1)
+        a.ch_expanded = ptr(chmask) if chmask is not None else ptr(ws.get("ch_exp", n * cmp))
+        a.given_chmask = ptr(chmask)
+        self._ch_coarse = ws.get("ch_coarse", n * d)
+        self._ch_sel = ws.get("ch_sel", n * cmp * 4)
+        self._ch_count = ws.get("ch_count", n * 4)
+        self._ch_dvals = ws.get("ch_dvals", n * d * 4)
+        a.ch_coarse, a.ch_sel, a.ch_count = ptr(self._ch_coarse), ptr(self._ch_sel), ptr(self._ch_count)
+        a.ch_dvals = ptr(self._ch_dvals)
+        a.wpack = ptr(ws.get("wpack", _lib.lib().laud_channel_pack_bytes(n, self.cin_p, cmp, self.cout_p)))
+        if chmask is None:
+            if getattr(self, "ch_w1", None) is None:
+                raise DeviceError("no channel mask given and no channel masker weights set")
+            a.ch_w1, a.ch_w2 = ptr(self.ch_w1), ptr(self.ch_w2)
+            a.ch_hidden, a.ch_d, a.ch_groups = self.ch_hidden, self.ch_d, self.ch_g
+
     def forward(self, x: torch.Tensor, paradigm: str = "spatial", s: int = 1,
                 coarse: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
-                misplace_first: bool = False, stream=None, ws: Optional[Workspace] = None):
+                misplace_first: bool = False, stream=None, ws: Optional[Workspace] = None,
+                chmask: Optional[torch.Tensor] = None):
         """x: (N, H, W, cin_p) bf16 CUDA.  Returns (out, coarse, cell_list, cell_count)."""
         n, h, w, cl = x.shape
         if cl != self.cin_p or x.dtype != torch.bfloat16 or not x.is_contiguous():
@@ -220,6 +252,9 @@ class DeviceBlock:
         h2 = ws.get("h2", n * ho * wo * self.cmid_p * 2)
         lib = _lib.lib()
         partial_n = 1
+        if paradigm == "channel":
+            h2 = ws.get("h2", n * ho * wo * self.cmid_p * 2)
+            h1 = ws.get("h1", pix * self.cmid_p * 2)
         if coarse is None and paradigm in ("spatial", "layer"):
             if self.wdiff is None:
                 raise DeviceError("no mask given and no masker weights set")
@@ -241,5 +276,7 @@ class DeviceBlock:
             cell_count=C.c_void_p(counts.data_ptr()), pix_list=ptr(pix_list),
             pix_count=C.c_void_p(counts.data_ptr() + 4), h1=ptr(h1), h2=ptr(h2),
             partial=ptr(partial), scan=ptr(scan), misplace_first=int(misplace_first))
+        if paradigm == "channel":
+            self._channel_args(a, n, ws, chmask)
         _lib.check(lib.laud_block_forward(C.byref(a), stream_handle(stream)))
         return out, coarse_buf, cell_list, counts

@@ -99,7 +99,7 @@ def test_dilate_and_rates_matches_oracle():
 
 def _cases():
     meta = json.loads((G / "equivalence.json").read_text())
-    return [m for m in meta if m["paradigm"] in ("spatial", "layer")]
+    return meta
 
 
 @pytest.mark.parametrize("m", _cases(), ids=lambda m: m["key"])
@@ -108,8 +108,12 @@ def test_block_sparse_matches_oracle(m):
     case = O.EquivalenceCase(Paradigm(m["paradigm"]), m["channels"], m["height"], m["width"],
                              m["granularity"], m["seed"])
     block, mask, bw, x, cfg = O.case_inputs(case)
-    rmask = (R.SpatialMask(mask.coarse, mask.upsampled, mask.granularity)
-             if case.paradigm is Paradigm.SPATIAL else R.LayerMask(mask.decisions))
+    if case.paradigm is Paradigm.SPATIAL:
+        rmask = R.SpatialMask(mask.coarse, mask.upsampled, mask.granularity)
+    elif case.paradigm is Paradigm.CHANNEL:
+        rmask = R.ChannelMask(mask.coarse, mask.expanded, mask.granularity)
+    else:
+        rmask = R.LayerMask(mask.decisions)
     rbw = R.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
     y = R.block_forward_sparse(x, rbw, block, cfg, rmask)
     emu = O.block_forward_sparse(x, bw, block, cfg, mask, emulate_bf16=True)
@@ -183,3 +187,45 @@ def test_full_and_empty_masks_at_scale():
     y0 = R.block_forward_sparse(x, bw, blk, DynamicConfig(Paradigm.SPATIAL, spatial_granularity=2),
                                 R.SpatialMask(zeros, R.upsample_coarse(zeros, 2), 2))
     np.testing.assert_array_equal(y0, O.round_bf16(x))
+
+
+def test_channel_masker_matches_reference():
+    R = _R()
+    a = np.load(G / "maskers.npz")
+    for i in range(3):
+        x, w1, w2, g = a[f"ch{i}_x"], a[f"ch{i}_w1"], a[f"ch{i}_w2"], int(a[f"ch{i}_g"])
+        m = R.channel_masker_forward(x, (w1, w2), g)
+        # near-tie guard on the logit gap (fp32 device vs fp64 reference)
+        hid = np.maximum(x.mean(axis=(2, 3)) @ w1.T, 0.0)
+        lg = (hid @ w2.T).reshape(x.shape[0], -1, 2)
+        gap = lg[..., 0] - lg[..., 1]
+        scale = np.abs(hid) @ np.abs(w2.T).reshape(hid.shape[1], -1, 2).sum(-1) + 1e-30
+        safe = np.abs(gap) > 1e-5 * scale
+        assert np.array_equal(m.coarse[safe], a[f"ch{i}_coarse"][safe])
+        assert np.array_equal(m.expanded.shape, a[f"ch{i}_exp"].shape)
+        mt = R.channel_masker_forward(x, (w1, w2), g, mode="train", tau=0.5,
+                                      rng=np.random.default_rng(7 + i))
+        assert np.array_equal(mt.coarse[safe], a[f"ch{i}_train_coarse"][safe])
+        np.testing.assert_allclose(mt.soft, a[f"ch{i}_train_soft"], rtol=1e-3, atol=1e-5)
+
+
+@pytest.mark.parametrize("r", [0.0, 0.25, 0.5, 1.0])
+def test_channel_block_large(r):
+    """R101 s3 geometry (14x14x1024, mid 256), batch 4: exact-count channel masks."""
+    R = _R()
+    blk = BlockSpec(ConvLayerSpec(1024, 256, 1), ConvLayerSpec(256, 256, 3), ConvLayerSpec(256, 1024, 1),
+                    TensorShape(1024, 14, 14))
+    rng = np.random.default_rng(5)
+    bw = R.make_block_weights(blk, rng)
+    x = rng.standard_normal((4, 1024, 14, 14))
+    coarse = np.zeros((4, 256), bool)
+    for i in range(4):
+        coarse[i, rng.permutation(256)[: int(round(r * 256))]] = True
+    m = R.ChannelMask(coarse, coarse, 1)
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=1)
+    y = R.block_forward_sparse(x, bw, blk, cfg, m)
+    obw = O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
+    emu = O.block_forward_sparse(x, obw, blk, cfg, O.ChannelMask(coarse, coarse, 1), emulate_bf16=True)
+    assert _rel(y, emu) <= BF16_TOL
+    yd = R.block_forward_dense_masked(x, bw, blk, cfg, m)
+    assert _rel(y, yd) <= BF16_TOL
