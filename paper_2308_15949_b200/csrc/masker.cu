@@ -98,6 +98,58 @@ __global__ void __launch_bounds__(256) cell_dot_kernel(
   if (lane == 0) partial[item] = acc;
 }
 
+// Same as cell_dot_kernel for cells of <= 32*NPL chunks (one split): every
+// lane issues all of its NPL 16-byte loads before the first FMA, so a warp
+// keeps a whole cell (up to 8 KiB) in flight.
+template <int NPL>
+__global__ void __launch_bounds__(256) cell_dot_unrolled_kernel(
+    const __nv_bfloat16* __restrict__ x, int ld, int n, int h, int w, int c, int win, int cells_h,
+    int cells_w, const float* __restrict__ wdiff, float* __restrict__ partial) {
+  extern __shared__ float s_w[];
+  for (int i = threadIdx.x; i < c; i += blockDim.x) s_w[i] = wdiff[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cpp = c >> 3;
+  const int cell_chunks = win * win * cpp;
+  const int total = n * cells_h * cells_w;
+  const int cell = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (cell >= total) return;
+  const int cpi = cells_h * cells_w;
+  const int ni = cell / cpi;
+  const int cr = cell - ni * cpi;
+  const int ci = cr / cells_w, cj = cr - (cr / cells_w) * cells_w;
+  uint4 v[NPL];
+  int chv[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int q = lane + 32 * i;
+    chv[i] = -1;
+    v[i] = make_uint4(0, 0, 0, 0);
+    if (q < cell_chunks) {
+      const int px = q / cpp;
+      const int ch = (q - px * cpp) << 3;
+      const int py = px / win;
+      v[i] = __ldg(reinterpret_cast<const uint4*>(
+          x + ((size_t)(ni * h + ci * win + py) * w + cj * win + (px - py * win)) * ld + ch));
+      chv[i] = ch;
+    }
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    if (chv[i] < 0) continue;
+    const float* ww = s_w + chv[i];
+    float2 f;
+    f = unpack_bf16x2(v[i].x); acc = fmaf(f.x, ww[0], acc); acc = fmaf(f.y, ww[1], acc);
+    f = unpack_bf16x2(v[i].y); acc = fmaf(f.x, ww[2], acc); acc = fmaf(f.y, ww[3], acc);
+    f = unpack_bf16x2(v[i].z); acc = fmaf(f.x, ww[4], acc); acc = fmaf(f.y, ww[5], acc);
+    f = unpack_bf16x2(v[i].w); acc = fmaf(f.x, ww[6], acc); acc = fmaf(f.y, ww[7], acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) partial[cell] = acc;
+}
+
 // ---------------------------------------------------------------------------
 // flag sources for the compaction core
 // ---------------------------------------------------------------------------
@@ -390,7 +442,20 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
   }
   const long long items = (long long)total * splits;
   const int blocks = (int)((items + 7) / 8);
-  if (x_f32)
+  const int cell_chunks = win * win * (c / 8);
+  if (false && !x_f32 && splits == 1 && cell_chunks <= 512) {  // measured slower (occupancy)
+    auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+    const size_t sm = c * sizeof(float);
+    if (cell_chunks <= 128)
+      cell_dot_unrolled_kernel<4><<<blocks, 256, sm, stream>>>(xb, ld, n, h, w, c, win, cells_h,
+                                                               cells_w, wdiff, partial);
+    else if (cell_chunks <= 256)
+      cell_dot_unrolled_kernel<8><<<blocks, 256, sm, stream>>>(xb, ld, n, h, w, c, win, cells_h,
+                                                               cells_w, wdiff, partial);
+    else
+      cell_dot_unrolled_kernel<16><<<blocks, 256, sm, stream>>>(xb, ld, n, h, w, c, win, cells_h,
+                                                                cells_w, wdiff, partial);
+  } else if (x_f32)
     cell_dot_kernel<float><<<blocks, 256, c * sizeof(float), stream>>>(
         reinterpret_cast<const float*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff, splits,
         cps, partial);
