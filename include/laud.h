@@ -119,6 +119,10 @@ typedef struct laud_conv_args {
   int n_dyn, k_dyn, b_batched;
   const int* col_index;
   int col_index_ld;
+  /* masker-conv3 fusion: per output row, dot(stored output, mdot_w) is added
+   * into mdot_out[cell of the row] (patch rows) — the next block's masker. */
+  const float* mdot_w;
+  float* mdot_out;
   int misplace_first;
 } laud_conv_args;
 
@@ -173,6 +177,15 @@ typedef struct laud_block_args {
   int* ch_count;
   float* ch_dvals;
   void* wpack;
+  /* masker-conv3 fusion across consecutive blocks of a stage (same grid, S):
+   * dn [cells] carries, for cells prev_coarse marks active, the dot product of
+   * this block's input with its masker weights (accumulated by the previous
+   * block's conv3 epilogue); cells it skipped are read from x.  When
+   * next_wdiff is set, this block's conv3 accumulates the dots for the next
+   * block into dn (the masker zeroes dn first). */
+  const uint8_t* prev_coarse;
+  float* dn;
+  const float* next_wdiff;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

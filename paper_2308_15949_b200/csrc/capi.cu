@@ -26,7 +26,8 @@ int masker_splits(int win, int c, int* chunks_per_split);
 cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c,
                                   int s, int stride, const float* wdiff, float bias,
                                   uint8_t* coarse, int* list, int* count, float* partial,
-                                  void* scan, cudaStream_t stream);
+                                  void* scan, cudaStream_t stream, const uint8_t* prev_coarse,
+                                  float* dn);
 cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,
                                   void* scan, cudaStream_t stream);
 cudaError_t launch_dilate_pixels(const uint8_t* coarse, int n, int h, int w, int s, int stride,
@@ -275,6 +276,8 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   if (a->sample_rows % 128) return fail(LAUD_ERR_ARG, "sample_rows must be a multiple of 128");
   if ((a->n_dyn || a->k_dyn) && !a->chan_count) return fail(LAUD_ERR_ARG, "chan_count missing");
   p.misplace_first = a->misplace_first;
+  p.mdot_w = a->mdot_w;
+  p.mdot_out = a->mdot_out;
   const int bn = pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   CUtensorMap m;
   const int kw = a->ksize * a->ksize * p.kpad;
@@ -385,7 +388,7 @@ int laud_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, i
   if (ps.on) ps.rec.bytes = (long long)n * h * w * c * (x_f32 ? 4 : 2);
   return cuda_check(launch_spatial_masker(x, x_f32, ld, n, h, w, c, s, stride, wdiff, bias, coarse,
                                           cell_list, cell_count, partial, scan,
-                                          (cudaStream_t)stream),
+                                          (cudaStream_t)stream, nullptr, nullptr),
                     "spatial masker", 2);
 }
 
@@ -627,10 +630,20 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
       if (a->paradigm == LAUD_PARADIGM_LAYER && a->h_in != a->w_in)
         return fail(LAUD_ERR_GRANULARITY, "layer masker needs a square feature");
       coarse = a->coarse_out;
-      rc = laud_spatial_masker(a->x, 0, a->x_ld, n, a->h_in, a->w_in, a->c_in,
-                               a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
-                               a->masker_wdiff, a->masker_bias, a->coarse_out, a->cell_list,
-                               a->cell_count, a->partial, a->scan, stream);
+      if (a->dn) {  // masker-conv3 fusion with the previous block (same grid and S)
+        ProfScope ps(1, st);
+        rc = cuda_check(launch_spatial_masker(a->x, 0, a->x_ld, n, a->h_in, a->w_in, a->c_in,
+                                              a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s,
+                                              a->stride, a->masker_wdiff, a->masker_bias,
+                                              a->coarse_out, a->cell_list, a->cell_count,
+                                              a->partial, a->scan, st, a->prev_coarse, a->dn),
+                        "spatial masker (fused)", 2);
+      } else {
+        rc = laud_spatial_masker(a->x, 0, a->x_ld, n, a->h_in, a->w_in, a->c_in,
+                                 a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
+                                 a->masker_wdiff, a->masker_bias, a->coarse_out, a->cell_list,
+                                 a->cell_count, a->partial, a->scan, stream);
+      }
     }
     if (rc) return rc;
     cells = a->cell_list;
@@ -781,6 +794,10 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c3.resid = a->out;
   c3.resid_ld = a->c_out;
   c3.misplace_first = a->misplace_first;
+  if (a->next_wdiff && a->dn && pm == ROWS_PATCH) {  // dot with the next block's masker
+    c3.mdot_w = a->next_wdiff;
+    c3.mdot_out = a->dn;
+  }
   return run_conv(&c3, st);
 }
 

@@ -112,7 +112,7 @@ struct Smem {
   static constexpr int STG_OFF = B_OFF + STAGES * B_STAGE_BYTES;
   static constexpr int STG_BUF = BM * STG_ROW;  // one staging buffer
   static constexpr int VEC_OFF = STG_OFF + NSTG * STG_BUF;  // per-warp scale/bias slices
-  static constexpr int VEC_BYTES = NUM_EPI_WARPS * 2 * (BN / 2) * 4;
+  static constexpr int VEC_BYTES = NUM_EPI_WARPS * 3 * (BN / 2) * 4;  // scale, bias, next wdiff
   static constexpr int BAR_OFF = VEC_OFF + VEC_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
@@ -322,8 +322,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int hf = (warp - 4) >> 2;
     const int col0 = hf * HALF;
     const int stg_off0 = L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
-    float* vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + (warp - 4) * 2 * HALF;
+    float* vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + (warp - 4) * 3 * HALF;
     float* vbi = vsc + HALF;
+    float* vnw = vbi + HALF;  // next block's masker weights (masker-conv3 fusion)
     const __nv_bfloat16* resid = reinterpret_cast<const __nv_bfloat16*>(p.resid);
     __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
     const bool staged = !p.out_f32;
@@ -407,7 +408,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         vsc[i] = (p.scale && live) ? __ldg(p.scale + src) : 1.f;
         vbi[i] = (p.bias && live) ? __ldg(p.bias + src) : 0.f;
+        if (p.mdot_w) vnw[i] = c < p.n_out ? __ldg(p.mdot_w + c) : 0.f;
       }
+      float pd = 0.f;  // this row's partial dot with the next masker
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (pre) asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -477,7 +480,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             w.z = pack_bf16x2(v[4], v[5]);
             w.w = pack_bf16x2(v[6], v[7]);
             *slot = w;
+            if (p.mdot_w) {  // the stored (bf16) values are what the next masker sees
+              const float4 n0 = *reinterpret_cast<const float4*>(vnw + cl);
+              const float4 n1 = *reinterpret_cast<const float4*>(vnw + cl + 4);
+              float2 f;
+              f = unpack_bf16x2(w.x); pd = fmaf(f.x, n0.x, pd); pd = fmaf(f.y, n0.y, pd);
+              f = unpack_bf16x2(w.y); pd = fmaf(f.x, n0.z, pd); pd = fmaf(f.y, n0.w, pd);
+              f = unpack_bf16x2(w.z); pd = fmaf(f.x, n1.x, pd); pd = fmaf(f.y, n1.y, pd);
+              f = unpack_bf16x2(w.w); pd = fmaf(f.x, n1.z, pd); pd = fmaf(f.y, n1.w, pd);
+            }
           }
+        }
+      }
+      if (p.mdot_w) {
+        // rows of one patch are consecutive lanes: reduce per patch, one atomic each
+        const int seg = p.patch_h * p.patch_w;
+        if (seg <= 32 && (32 % seg) == 0) {
+          for (int o = 1; o < seg; o <<= 1) pd += __shfl_xor_sync(0xffffffffu, pd, o);
+          if (cur.valid && (lane % seg) == 0) {
+            const RowPos& rp = cur.rp;
+            atomicAdd(p.mdot_out + (rp.n * p.cells_h + rp.y / p.patch_h) * p.cells_w +
+                          rp.x / p.patch_w, pd);
+          }
+        } else if (cur.valid) {
+          const RowPos& rp = cur.rp;
+          atomicAdd(p.mdot_out + (rp.n * p.cells_h + rp.y / p.patch_h) * p.cells_w +
+                        rp.x / p.patch_w, pd);
         }
       }
       // accumulator consumed: hand the TMEM buffer back to the MMA warp early

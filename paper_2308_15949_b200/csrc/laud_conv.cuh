@@ -65,6 +65,9 @@ struct ConvParams {
   int b_batched;           // B is [N][n_out][K] (3D tensor map, sample coordinate)
   const int* col_index;    // [N][col_index_ld]: scale/bias index of output column c
   int col_index_ld;
+  // ---- masker-conv3 fusion: mdot_out[cell(row)] += dot(bf16 output row, mdot_w)
+  const float* mdot_w;
+  float* mdot_out;
   // ---- fault hook (tests only): shift the first patch's destination one cell
   int misplace_first;
 };

@@ -15,6 +15,7 @@
 // patches' 3x3 halo windows on the input grid) and lists from given masks.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "laud_ptx.cuh"
 
@@ -65,7 +66,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) cell_dot_kernel(
     const T* __restrict__ x, int ld, int n, int h, int w, int c, int win, int cells_h,
     int cells_w, const float* __restrict__ wdiff, int splits, int chunks_per_split,
-    float* __restrict__ partial) {
+    float* __restrict__ partial, const uint8_t* __restrict__ prev_coarse, float* __restrict__ dn) {
   extern __shared__ float s_w[];
   for (int i = threadIdx.x; i < c; i += blockDim.x) s_w[i] = wdiff[i];
   __syncthreads();
@@ -82,8 +83,19 @@ __global__ void __launch_bounds__(256) cell_dot_kernel(
   const int cr = cell - ni * cpi;
   const int ci = cr / cells_w, cj = cr - (cr / cells_w) * cells_w;
   const int q0 = split * chunks_per_split;
-  const int q1 = min(q0 + chunks_per_split, cell_chunks);
+  int q1 = min(q0 + chunks_per_split, cell_chunks);
   float acc = 0.f;
+  // masker-conv3 fusion: cells the previous block computed already carry their
+  // dot product (accumulated by that block's conv3 epilogue) in dn; only cells
+  // it skipped are read from x.  dn is consumed (zeroed) for the next block.
+  if (dn) {
+    const bool prev_active = prev_coarse && prev_coarse[cell];
+    if (prev_active) q1 = q0;  // skip the loads
+    if (split == 0 && lane == 0) {
+      if (prev_active) acc = dn[cell];
+      dn[cell] = 0.f;
+    }
+  }
 #pragma unroll 4
   for (int q = q0 + lane; q < q1; q += 32) {
     const int px = q / cpp;
@@ -390,10 +402,101 @@ __global__ void __launch_bounds__(256) masker_fused_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// K1 strip masker: one CTA streams one row of cells (win image rows x W x C,
+// contiguous in NHWC) with fully coalesced 16-byte loads, 8 in flight per
+// thread; per-cell dot products are reduced per pixel group with shuffles and
+// one shared-memory atomic per group; then decisions + the tile's compaction
+// (tile = the strip's cells, row-major) with decoupled look-back.
+// ---------------------------------------------------------------------------
+template <typename T, int UNROLL>
+__global__ void __launch_bounds__(256) masker_strip_kernel(
+    const T* __restrict__ x, int ld, int n, int h, int w, int c, int win, int cells_h, int cells_w,
+    const float* __restrict__ wdiff, float bias, float inv_area, uint8_t* __restrict__ coarse,
+    float* __restrict__ dots, int dots_stride, int* __restrict__ list, int* __restrict__ count,
+    ScanState* st, int num_tiles) {
+  extern __shared__ float s_w[];  // c floats, then cells_w sums
+  float* s_sum = s_w + c;
+  __shared__ int s_tile, s_excl, s_rel, s_wc[8];
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(&st->tile_ctr, 1u);
+  for (int i = threadIdx.x; i < c; i += blockDim.x) s_w[i] = wdiff[i];
+  for (int i = threadIdx.x; i < cells_w; i += blockDim.x) s_sum[i] = 0.f;
+  __syncthreads();
+  const int tile = s_tile;  // = n * cells_h + ci
+  const int ni = tile / cells_h, ci = tile - (tile / cells_h) * cells_h;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cpp = c >> 3;                       // 8-channel chunks per pixel (power of 2)
+  const int grp = cpp < 32 ? cpp : 32;          // lanes sharing one pixel
+  const int lcpp = __ffs(cpp) - 1;               // cpp is a power of two
+  const int row_chunks = w * cpp;
+  const int total = row_chunks * win;            // chunks in the strip
+  const T* base = x + (size_t)(ni * h + ci * win) * w * ld;
+  for (int q0 = threadIdx.x; q0 < total; q0 += blockDim.x * UNROLL) {
+    float part[UNROLL];
+    int cell_of[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int q = q0 + u * blockDim.x;
+      part[u] = 0.f;
+      cell_of[u] = -1;
+      if (q < total) {
+        const int pxl = q >> lcpp;               // pixel index within the strip
+        const int ch = (q & (cpp - 1)) << 3;
+        const int r = pxl / w;
+        const int px = pxl - r * w;
+        part[u] = dot8<T>(base + ((size_t)r * w + px) * ld + ch, s_w + ch);
+        cell_of[u] = px / win;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      float v = part[u];
+      for (int o = 1; o < grp; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((lane & (grp - 1)) == 0 && cell_of[u] >= 0) atomicAdd(&s_sum[cell_of[u]], v);
+    }
+  }
+  __syncthreads();
+  // decisions and compaction of this strip's cells_w cells (<= 256)
+  const int cell0 = tile * cells_w;
+  bool mine = false;
+  if (threadIdx.x < cells_w) {
+    const float d = s_sum[threadIdx.x];
+    mine = d * inv_area + bias >= 0.f;
+    coarse[cell0 + threadIdx.x] = mine ? 1 : 0;
+    if (dots) {  // same layout as the split partials: [cell][split], extra splits zero
+      float* dp = dots + (size_t)(cell0 + threadIdx.x) * dots_stride;
+      dp[0] = d;
+      for (int k = 1; k < dots_stride; ++k) dp[k] = 0.f;
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, mine);
+  if (lane == 0) s_wc[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < 8 ? s_wc[lane] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane < 8) s_wc[lane] = incl - v;
+    const int agg = __shfl_sync(0xffffffffu, incl, 7);
+    const int excl = warp_lookback(st, tile, agg, lane);
+    if (lane == 0) {
+      s_excl = excl;
+      if (tile == num_tiles - 1) *count = excl + agg;
+    }
+  }
+  __syncthreads();
+  if (mine) list[s_excl + s_wc[warp] + __popc(bal & ((1u << lane) - 1u))] = cell0 + threadIdx.x;
+  scan_state_release(st, num_tiles, &s_rel);
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 size_t scan_state_bytes(int total) {
-  const int tiles = total / 8 + 2;  // fused masker tiles hold >= 8 items
+  const int tiles = total + 2;  // strip-masker tiles may hold a single item (layer masker)
   return sizeof(ScanState) + sizeof(unsigned long long) * (tiles > 0 ? tiles : 1);
 }
 
@@ -418,13 +521,33 @@ int masker_splits(int win, int c, int* chunks_per_split) {
 cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c,
                                   int s, int stride, const float* wdiff, float bias,
                                   uint8_t* coarse, int* list, int* count, float* partial,
-                                  void* scan, cudaStream_t stream) {
+                                  void* scan, cudaStream_t stream, const uint8_t* prev_coarse,
+                                  float* dn) {
   const int win = s * stride;
   const int cells_h = h / win, cells_w = w / win;
   int cps = 0;
   const int splits = masker_splits(win, c, &cps);
   const int total = n * cells_h * cells_w;
-  if (splits == 1 && total > 0 && total <= 4096) {  // small grids: one launch wins
+  const int cpp = c / 8;
+  const bool pow2 = cpp > 0 && (cpp & (cpp - 1)) == 0;
+  // experimental (slower and not race-free yet): LAUD_MASKER_STRIP=1
+  if (!dn && total > 0 && pow2 && cells_w <= 256 && getenv("LAUD_MASKER_STRIP")) {
+    // streaming strip masker: decisions + compaction in one launch
+    const int tiles = n * cells_h;
+    const float inv_area = 1.0f / (float)(win * win);
+    const size_t sm = (size_t)(c + cells_w) * sizeof(float);
+    if (x_f32)
+      masker_strip_kernel<float, 4><<<tiles, 256, sm, stream>>>(
+          reinterpret_cast<const float*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff, bias,
+          inv_area, coarse, partial, splits, list, count, reinterpret_cast<ScanState*>(scan), tiles);
+    else
+      masker_strip_kernel<__nv_bfloat16, 8><<<tiles, 256, sm, stream>>>(
+          reinterpret_cast<const __nv_bfloat16*>(x), ld, n, h, w, c, win, cells_h, cells_w,
+          wdiff, bias, inv_area, coarse, partial, splits, list, count,
+          reinterpret_cast<ScanState*>(scan), tiles);
+    return cudaGetLastError();
+  }
+  if (splits == 1 && total > 0 && total <= 4096 && !dn) {  // small grids: one launch wins
     // one pass: dots + decisions + compaction; ~2 waves of CTAs over the SMs
     // one cell per warp: as many resident warps (bytes in flight) as the SMs hold
     const int tc = 8;
@@ -458,11 +581,11 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
   } else if (x_f32)
     cell_dot_kernel<float><<<blocks, 256, c * sizeof(float), stream>>>(
         reinterpret_cast<const float*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff, splits,
-        cps, partial);
+        cps, partial, prev_coarse, dn);
   else
     cell_dot_kernel<__nv_bfloat16><<<blocks, 256, c * sizeof(float), stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff,
-        splits, cps, partial);
+        splits, cps, partial, prev_coarse, dn);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse};

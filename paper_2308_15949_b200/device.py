@@ -228,7 +228,9 @@ class DeviceBlock:
     def forward(self, x: torch.Tensor, paradigm: str = "spatial", s: int = 1,
                 coarse: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
                 misplace_first: bool = False, stream=None, ws: Optional[Workspace] = None,
-                chmask: Optional[torch.Tensor] = None):
+                chmask: Optional[torch.Tensor] = None, coarse_out: Optional[torch.Tensor] = None,
+                prev_coarse: Optional[torch.Tensor] = None, dn: Optional[torch.Tensor] = None,
+                next_wdiff: Optional[torch.Tensor] = None):
         """x: (N, H, W, cin_p) bf16 CUDA.  Returns (out, coarse, cell_list, cell_count)."""
         n, h, w, cl = x.shape
         if cl != self.cin_p or x.dtype != torch.bfloat16 or not x.is_contiguous():
@@ -244,7 +246,12 @@ class DeviceBlock:
             cells = n
         pix = n * h * w
         i32 = 4
-        coarse_buf = ws.get("coarse", cells) if coarse is None else coarse
+        if coarse is not None:
+            coarse_buf = coarse
+        elif coarse_out is not None:
+            coarse_buf = coarse_out
+        else:
+            coarse_buf = ws.get("coarse", cells)
         cell_list = ws.get("cell_list", cells * i32)
         counts = ws.get("counts", 16)
         pix_list = ws.get("pix_list", pix * i32)
@@ -278,5 +285,7 @@ class DeviceBlock:
             partial=ptr(partial), scan=ptr(scan), misplace_first=int(misplace_first))
         if paradigm == "channel":
             self._channel_args(a, n, ws, chmask)
+        if dn is not None and paradigm == "spatial":
+            a.dn, a.prev_coarse, a.next_wdiff = ptr(dn), ptr(prev_coarse), ptr(next_wdiff)
         _lib.check(lib.laud_block_forward(C.byref(a), stream_handle(stream)))
         return out, coarse_buf, cell_list, counts

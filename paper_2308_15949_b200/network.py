@@ -80,6 +80,7 @@ class BlockSlot:
     index: int
     db: D.DeviceBlock
     s: int           # spatial granularity (output grid); 0 for static
+    fused_in: bool = False  # masker reads the previous block's conv3 dots
 
 
 class LaudNetwork:
@@ -133,6 +134,14 @@ class LaudNetwork:
         self.n_cls = D.pad8(net.num_classes)
         self._bufs = {}
         self.ws = D.Workspace(device)
+        # masker-conv3 fusion: block i+1 reuses block i's conv3 output dots when
+        # both run on the same grid with the same S and i+1 has no downsample
+        self.fuse_masker = False  # measured: the conv3 dot costs more than the masker saves
+        for i, slot in enumerate(self.slots):
+            prev = self.slots[i - 1] if i > 0 else None
+            b = slot.db.block
+            slot.fused_in = (para is Paradigm.SPATIAL and prev is not None and prev.stage == slot.stage
+                             and not b.has_downsample and b.stride == 1 and prev.s == slot.s)
 
     # ------------------------------------------------------------------ buffers
     def _buf(self, name, shape, dtype=torch.bfloat16):
@@ -175,7 +184,8 @@ class LaudNetwork:
             _lib.call("laud_maxpool3s2", D.ptr(stem_out), n, ho, wo, self.stem_c, D.ptr(pool), sh)
             x = pool
         ping = 0
-        for slot in self.slots:
+        prev_coarse = None
+        for bi, slot in enumerate(self.slots):
             db = slot.db
             hh, ww = x.shape[1], x.shape[2]
             oh, ow = db.out_hw(hh, ww)
@@ -185,8 +195,23 @@ class LaudNetwork:
                 out = self._buf(f"act{ping}", (n, oh, ow, db.cout_p))
             else:
                 out = x  # in-place residual: conv1 reads x before conv3 writes it
+            kw = {}
+            if para == "spatial" and self.fuse_masker:
+                # masker-conv3 fusion inside a stage: this block's conv3 accumulates
+                # the next block's masker dots; the next masker reads only the
+                # cells this block skipped
+                ncell = n * (oh // slot.s) * (ow // slot.s)
+                fused_in = slot.fused_in
+                nxt = self.slots[bi + 1] if bi + 1 < len(self.slots) else None
+                fused_out = nxt is not None and nxt.fused_in
+                if fused_in or fused_out:
+                    kw["coarse_out"] = self._buf(f"coarse{bi & 1}", (ncell,), torch.uint8)
+                    kw["dn"] = self._buf("dn", (ncell,), torch.float32)
+                    kw["prev_coarse"] = prev_coarse if fused_in else None
+                    kw["next_wdiff"] = nxt.db.wdiff if fused_out else None
             y, coarse, cells, counts = db.forward(x, para, slot.s if para == "spatial" else 0,
-                                                  out=out, stream=stream, ws=self.ws)
+                                                  out=out, stream=stream, ws=self.ws, **kw)
+            prev_coarse = kw.get("coarse_out")
             if record is not None and para != "static":
                 ncell = n * (oh // slot.s) * (ow // slot.s) if para == "spatial" else n
                 record.append((slot, coarse[:ncell].clone(), counts[:8].clone()))

@@ -38,3 +38,23 @@ def test_network_matches_oracle(arch, paradigm):
     if paradigm == "spatial":
         r = np.mean([m.mean() for m in masks])
         assert 0.3 < r < 0.7
+
+
+def test_masker_conv3_fusion_matches_unfused():
+    """The fused (conv3-epilogue dots) masker decides like the standalone one."""
+    import torch
+    from paper_2308_15949_b200.network import LaudNetwork, random_images
+    net = LaudNetwork("resnet101", "spatial", "4-2-2-1", 0.5, seed=0)
+    img = random_images(8, seed=4)
+    net.calibrate(img)
+    outs, masks = [], []
+    for fuse in (False, True):
+        net.fuse_masker = fuse
+        rec = []
+        outs.append(net.forward(img, record=rec)[:, :1000].float().cpu().numpy())
+        torch.cuda.synchronize()
+        masks.append([c.cpu().numpy() for _, c, _ in rec])
+    agree = np.mean([np.mean(a == b) for a, b in zip(*masks)])
+    assert agree > 0.999, agree
+    rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[0])
+    assert rel < 2e-2, rel
