@@ -47,7 +47,7 @@ def peaks():
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="laud", choices=["laud", "reference"])
     ap.add_argument("--arch", default="resnet101")
@@ -151,7 +151,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -228,9 +228,21 @@ def capture(torch, fn, warmup):
     return g, out
 
 
+def _alg(r):
+    """Algorithmic FLOPs and compulsory bytes of one conv-engine launch."""
+    flops = 2.0 * r.rows * r.n_out * r.k
+    cin = r.k // max(1, r.taps)
+    nbytes = 2.0 * r.rows * (cin + r.n_out * (2 if r.resid else 1))
+    return flops, nbytes
+
+
 def conv_roofline(torch, net, images, pk, pk_kind):
-    """Per-launch CUDA-event profile of one eager forward (outside timing)."""
-    import ctypes as C
+    """Per-launch CUDA-event profile of one eager forward (outside the timed region).
+
+    The roofline object describes the dominant launch shape of the conv engine
+    (largest total time in the step): achieved = algorithmic FLOPs (or bytes,
+    whichever bounds it) per launch / average launch duration of that shape.
+    """
     from paper_2308_15949_b200 import _lib
     lib = _lib.lib()
     torch.cuda.synchronize()
@@ -238,26 +250,47 @@ def conv_roofline(torch, net, images, pk, pk_kind):
     net.forward(images)
     recs = (_lib.ProfileRecord * 4096)()
     n = lib.laud_profile_end(recs, 4096)
-    convs = [r for r in recs[:n] if r.tag == 0]
-    maskers = [r for r in recs[:n] if r.tag == 1]
-    flops = sum(2.0 * r.rows * r.n_out * r.k for r in convs)
-    ms = sum(r.ms for r in convs)
-    all_ms = sum(r.ms for r in recs[:n])
-    ach = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    recs = recs[:n]
+    convs = [r for r in recs if r.tag == 0]
+    maskers = [r for r in recs if r.tag == 1]
+    all_ms = sum(r.ms for r in recs)
+    groups = {}
+    for r in convs:
+        key = (r.rows, r.n_out, r.k, r.taps, r.resid)
+        groups.setdefault(key, []).append(r)
+    key, grp = max(groups.items(), key=lambda kv: sum(x.ms for x in kv[1]))
+    flops, nbytes = _alg(grp[0])
+    avg_ms = sum(x.ms for x in grp) / len(grp)
+    peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    peak_b = pk["hbm_gbs"]
+    t_tensor = flops / (peak_t * 1e12)
+    t_hbm = nbytes / (peak_b * 1e9)
+    if t_tensor >= t_hbm:
+        bound, ach, peak, unit = "tensor", flops / (avg_ms * 1e-3) / 1e12, peak_t, "TFLOP/s"
+    else:
+        bound, ach, peak, unit = "hbm", nbytes / (avg_ms * 1e-3) / 1e9, peak_b, "GB/s"
+    tot_f = sum(_alg(r)[0] for r in convs)
+    tot_ms = sum(r.ms for r in convs)
+    # step-level roofline of the conv engine: slower of FLOPs and bytes per launch, summed
+    ideal_ms = sum(max(_alg(r)[0] / (peak_t * 1e12), _alg(r)[1] / (peak_b * 1e9)) for r in convs) * 1e3
     mb = sum(r.bytes for r in maskers)
     mms = sum(r.ms for r in maskers)
-    top = sorted(convs, key=lambda r: -r.ms)[:5]
+    rows, n_out, k, taps, resid = key
     return {
-        "kernel": "laud::conv_gemm_kernel (tcgen05 implicit-GEMM conv engine, all launches of one step)",
-        "bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
+        "kernel": f"laud::conv_gemm_kernel, dominant shape rows={rows} n_out={n_out} K={k} "
+                  f"taps={taps} resid={resid} ({len(grp)} launches/step)",
+        "bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
         "frac": round(ach / peak, 4), "traffic": None,
-        "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)",
-        "launches": len(convs), "avg_launch_us": round(1e3 * ms / max(1, len(convs)), 2),
-        "alg_flops_per_step": flops, "share_of_profiled_step": round(ms / all_ms, 3) if all_ms else None,
+        "peak_source": f"{pk_kind} MEASURED_PEAKS.json ({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})",
+        "alg_flops_per_launch": flops, "alg_bytes_per_launch": nbytes,
+        "avg_launch_us": round(avg_ms * 1e3, 2),
+        "share_of_profiled_step": round(sum(x.ms for x in grp) / all_ms, 3) if all_ms else None,
+        "engine_all_launches": {"launches": len(convs), "ms": round(tot_ms, 3),
+                                "tflops": round(tot_f / (tot_ms * 1e-3) / 1e12, 1),
+                                "roofline_ms": round(ideal_ms, 3),
+                                "frac_of_roofline": round(ideal_ms / tot_ms, 4),
+                                "share_of_step": round(tot_ms / all_ms, 3) if all_ms else None},
         "masker_gbs": round(mb / (mms * 1e-3) / 1e9, 1) if mms else None,
-        "top_launches_us_tflops": [[round(1e3 * r.ms, 1), round(2.0 * r.rows * r.n_out * r.k / (r.ms * 1e-3) / 1e12, 1)]
-                                   for r in top],
     }
 
 
@@ -402,9 +435,11 @@ def run_gpu(args):
     extra = {}
     roof = conv_roofline(torch, net, images, pk, pk_kind)
     prof = ROOT / "profiles" / "conv_traffic.json"
-    if prof.exists():
+    if prof.exists():  # ncu --set full dram bytes of the same launch shape (profiles/)
         try:
-            roof["traffic"] = json.loads(prof.read_text()).get("traffic_per_launch")
+            t = json.loads(prof.read_text())
+            if t.get("shape") == roof["kernel"].split(", ", 1)[1].split(" (")[0]:
+                roof["traffic"] = t.get("traffic_per_launch")
         except Exception:
             pass
     if rank == 0 and not args.no_baselines and ws == 1:

@@ -52,6 +52,7 @@ typedef struct laud_profile_record {
   int tag; /* 0 conv engine, 1 masker, 2 compaction/dilation, 3 glue */
   float ms;
   long long rows, n_out, k, bytes;
+  int taps, resid; /* conv: kernel taps, residual read in the epilogue */
 } laud_profile_record;
 void laud_profile_begin(void);
 int laud_profile_end(laud_profile_record* out, int max_records);

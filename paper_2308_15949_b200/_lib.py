@@ -62,7 +62,8 @@ class BlockArgs(C.Structure):
 class ProfileRecord(C.Structure):
     """Mirror of ``laud_profile_record`` (include/laud.h)."""
     _fields_ = [("tag", C.c_int), ("ms", C.c_float), ("rows", C.c_longlong),
-                ("n_out", C.c_longlong), ("k", C.c_longlong), ("bytes", C.c_longlong)]
+                ("n_out", C.c_longlong), ("k", C.c_longlong), ("bytes", C.c_longlong),
+                ("taps", C.c_int), ("resid", C.c_int)]
 
 
 _SIGS = {

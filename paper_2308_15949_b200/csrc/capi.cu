@@ -62,6 +62,7 @@ struct ProfRec {
   cudaEvent_t e0, e1;
   int snap;              // index of the count snapshot (-1: none)
   long long rows_per_count, rows_max, n_out, k_alg, bytes;
+  int taps, resid;
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
@@ -309,6 +310,8 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
     ps.rec.rows_max = a->rows_max;
     ps.rec.n_out = a->n_out;
     ps.rec.k_alg = (long long)a->ksize * a->ksize * a->in_c;
+    ps.rec.taps = a->ksize * a->ksize;
+    ps.rec.resid = a->resid != nullptr;
   }
   return cuda_check(launch_conv_gemm(ma, m, bn, p, num_sms(), st), "conv_gemm launch", 1);
 }
@@ -352,6 +355,8 @@ int laud_profile_end(laud_profile_record* out, int max_records) {
       out[n].n_out = r.n_out;
       out[n].k = r.k_alg;
       out[n].bytes = r.bytes;
+      out[n].taps = r.taps;
+      out[n].resid = r.resid;
       ++n;
     }
     cudaEventDestroy(r.e0);
