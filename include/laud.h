@@ -129,6 +129,11 @@ typedef struct laud_conv_args {
 
 int laud_conv(const laud_conv_args* a, void* stream);
 
+/* Debug only (tools/engine_trace.py): when dev_buf (16384 u64, device) is set,
+ * CTA 0 of every following conv launch records %globaltimer at its pipeline
+ * events; NULL turns it off.  Not for use on a timed path. */
+void laud_debug_set_trace(void* dev_buf);
+
 /* One bottleneck block forward — replaces `block_forward_sparse`
  * (reference.py:356-436) for SPATIAL / LAYER / STATIC.  Masks: either
  * given (`given_coarse`, uint8 per cell; spatial cells on the output grid,

@@ -68,6 +68,7 @@ class ProfileRecord(C.Structure):
 
 _SIGS = {
     "laud_profile_begin": (None, []),
+    "laud_debug_set_trace": (None, [_vp]),
     "laud_profile_end": (C.c_int, [C.POINTER(ProfileRecord), C.c_int]),
     "laud_version": (C.c_char_p, []),
     "laud_last_error": (C.c_char_p, []),

@@ -55,6 +55,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+unsigned long long* g_trace = nullptr;  // laud_debug_set_trace (tools only)
 
 // Optional per-launch CUDA-event profiling (laud_profile_*), off by default.
 struct ProfRec {
@@ -279,6 +280,12 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   p.misplace_first = a->misplace_first;
   p.mdot_w = a->mdot_w;
   p.mdot_out = a->mdot_out;
+  p.trace = g_trace;
+  static const int dbg_env = [] {
+    const char* e = getenv("LAUD_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  p.dbg = dbg_env;
   const int bn = pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   CUtensorMap m;
   const int kw = a->ksize * a->ksize * p.kpad;
@@ -301,7 +308,16 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
       p.a_tma = 0;
     } else {
       p.a_rows = (int)arows;
-      if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, 1, &ma))) return rc;
+      // contiguous A rows: compact rows, or a dense stride-1 1x1 conv on one grid
+      static const int a_tile_env = [] {
+        const char* e = getenv("LAUD_A_TILE");
+        return e ? atoi(e) : 1;
+      }();
+      p.a_tile = a_tile_env && a->ksize == 1 &&
+                 (a->a_compact || (a->row_mode == ROWS_DENSE && a->sample_rows == 0 &&
+                                   a->stride == 1 && a->pad == 0 && a->in_h == a->out_h &&
+                                   a->in_w == a->out_w));
+      if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, p.a_tile ? 128 : 1, &ma))) return rc;
     }
   }
   ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
@@ -364,6 +380,8 @@ int laud_profile_end(laud_profile_record* out, int max_records) {
   }
   return n;
 }
+
+void laud_debug_set_trace(void* dev_buf) { g_trace = static_cast<unsigned long long*>(dev_buf); }
 
 const char* laud_version(void) { return "laud-b200 0.1.0 (sm_100a, tcgen05)"; }
 const char* laud_last_error(void) { return g_err.c_str(); }

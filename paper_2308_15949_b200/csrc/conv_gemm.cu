@@ -28,10 +28,14 @@ namespace laud {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
-constexpr int NUM_EPI_WARPS = 8;   // warps 4..11
-constexpr int WARP_TMA = 12;
-constexpr int WARP_MMA = 13;
-constexpr int NUM_THREADS = 14 * 32;
+#ifndef LAUD_EPI_WARPS
+#define LAUD_EPI_WARPS 16
+#endif
+constexpr int WARP_TMA = 4;
+constexpr int WARP_MMA = 5;
+constexpr int FIRST_EPI = 6;
+constexpr int NUM_EPI_WARPS = LAUD_EPI_WARPS;  // warps 6 .. 6 + NUM_EPI_WARPS - 1
+constexpr int NUM_THREADS = (FIRST_EPI + NUM_EPI_WARPS) * 32;
 
 struct RowPos {
   int n, y, x;
@@ -85,6 +89,58 @@ __device__ __forceinline__ bool map_row(const ConvParams& p, int m, int nvalid, 
   return true;
 }
 
+// Raw list entry row m depends on (fetched early; map_row_raw resolves it).
+__device__ __forceinline__ int row_fetch(const ConvParams& p, int m) {
+  if (p.list == nullptr || p.sample_rows > 0 || p.row_mode == ROWS_DENSE) return 0;
+  int idx, lim;
+  if (p.row_mode == ROWS_PATCH) {
+    const int s2 = p.patch_h * p.patch_w;
+    idx = m / s2;
+    lim = (p.rows_max - 1) / s2;
+  } else {
+    idx = m;
+    lim = p.rows_max - 1;
+  }
+  return __ldg(p.list + min(idx, lim));  // unconditional: consumed later
+}
+__device__ __forceinline__ bool map_row_raw(const ConvParams& p, int m, int nvalid, int raw, RowPos& o,
+                                            bool& first_patch) {
+  first_patch = false;
+  if (m >= nvalid) return false;
+  const int hw = p.out_h * p.out_w;
+  if (p.row_mode == ROWS_PATCH) {
+    const int s2 = p.patch_h * p.patch_w;
+    const int pi = m / s2;
+    const int l = m - pi * s2;
+    const int cpi = p.cells_h * p.cells_w;
+    o.n = raw / cpi;
+    const int c = raw - o.n * cpi;
+    const int ci = c / p.cells_w;
+    const int cj = c - ci * p.cells_w;
+    const int ly = l / p.patch_w;
+    o.y = ci * p.patch_h + ly;
+    o.x = cj * p.patch_w + (l - ly * p.patch_w);
+    o.pix = (o.n * p.out_h + o.y) * p.out_w + o.x;
+    first_patch = (pi == 0);
+    return true;
+  }
+  int pix;
+  if (p.sample_rows > 0) {
+    const int smp = m / p.sample_rows;
+    const int loc = m - smp * p.sample_rows;
+    if (loc >= hw) return false;
+    pix = smp * hw + loc;
+  } else {
+    pix = (p.row_mode == ROWS_PIXEL) ? raw : m;
+  }
+  o.pix = pix;
+  o.n = pix / hw;
+  const int r = pix - o.n * hw;
+  o.y = r / p.out_w;
+  o.x = r - o.y * p.out_w;
+  return true;
+}
+
 // Per-tile schedule shared by every warp role (all roles skip the same tiles).
 struct TileInfo {
   int m0, n0, sample, kpt, num_kb, kc;
@@ -112,7 +168,8 @@ struct Smem {
   static constexpr int STG_OFF = B_OFF + STAGES * B_STAGE_BYTES;
   static constexpr int STG_BUF = BM * STG_ROW;  // one staging buffer
   static constexpr int VEC_OFF = STG_OFF + NSTG * STG_BUF;  // per-warp scale/bias slices
-  static constexpr int VEC_BYTES = NUM_EPI_WARPS * 3 * (BN / 2) * 4;  // scale, bias, next wdiff
+  static constexpr int EW_COLS = BN / (NUM_EPI_WARPS / 4);  // columns per epilogue warp
+  static constexpr int VEC_BYTES = NUM_EPI_WARPS * 3 * EW_COLS * 4;  // scale, bias, next wdiff
   static constexpr int BAR_OFF = VEC_OFF + VEC_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
@@ -139,6 +196,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  unsigned long long* const trc = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
   const int nvalid = rows_valid(p);
   const int n_tiles = (p.n_out + BN - 1) / BN;
   const int m_tiles = (nvalid + BM - 1) / BM;
@@ -170,7 +228,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ A producers
     const int tid = threadIdx.x;
     uint32_t it = 0;
-    if (p.a_tma) {
+    if (p.a_tile) {
+      // Contiguous rows (compact / dense 1x1): one 128 x 64 TMA box per stage.
+      if (tid == 0) {
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+          const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+          if (ti.skip) continue;
+          const int row0 = p.sample_rows > 0
+                               ? ti.sample * p.out_h * p.out_w + (ti.m0 - ti.sample * p.sample_rows)
+                               : ti.m0;
+          for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+            const int stage = it % STAGES;
+            const uint32_t phase = (it / STAGES) & 1;
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (trc && it < 4096) trc[TRACE_A + it] = global_ns();
+            const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
+            if (p.dbg & 8) {
+              mbar_arrive(&full[stage]);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES);
+              tma_load_2d(sA, &tmap_a, &full[stage], kb * BK, row0);
+            }
+          }
+        }
+      }
+    } else if (p.a_tma) {
       // One output row per thread; per (tap, channel block) every 4th lane issues
       // a TMA tile::gather4 of its 4 rows' source pixels (OOB index -> zeros).
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -184,6 +266,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (trc && tid == 0 && it < 4096) trc[TRACE_A + it] = global_ns();
           const int tap = kb / ti.kpt;
           const int c0 = (kb - tap * ti.kpt) * BK;
           const int ky = tap / p.ksize;
@@ -263,6 +346,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (trc && it < 4096) trc[TRACE_B + it] = global_ns();
+          if (p.dbg & 16) {
+            mbar_arrive(&full[stage]);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], L::B_STAGE_BYTES);
           const int tap = kb / ti.kpt;
           const int kcoord = tap * p.kpad + (kb - tap * ti.kpt) * BK;  // packed per-tap stride kpad
@@ -291,9 +379,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
         mbar_wait(&full[stage], phase);
+        if (trc && lane == 0 && it < 4096) trc[TRACE_MMA + it] = global_ns();
         fence_proxy_async_smem();
         tc_fence_after();
-        if (lane == 0) {
+        if (lane == 0 && !(p.dbg & 32)) {
           const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
           const uint32_t sB = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
 #pragma unroll
@@ -302,6 +391,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       (kb | k) != 0);
           }
           umma_commit(&empty[stage]);
+        } else if (lane == 0) {
+          mbar_arrive(&empty[stage]);
         }
         __syncwarp();
       }
@@ -309,26 +400,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 4-11)
-    // Warp e handles TMEM lane quadrant q = warp % 4 (rows 32q..32q+31) and
-    // column half hf of the tile.  Rows are staged through shared memory so
-    // the residual read and the destination write are coalesced 16-byte-per-
-    // lane row segments (a scattered destination row is contiguous in NHWC).
-    // With NSTG = 2 the residual of the next tile is prefetched (cp.async)
-    // into the other staging buffer while this tile is finished and stored.
-    constexpr int HALF = BN / 2;        // columns per warp
-    constexpr int CPR = HALF / 8;       // 16-byte chunks per staged half-row
+    // ------------------------------------------------------------ epilogue
+    // NUM_EPI_WARPS warps: warp w reads TMEM lane quadrant q = w % 4 (rows
+    // 32q..32q+31; the hardware restricts a warp to its quadrant) and column
+    // slice EW_COLS * ((w - FIRST_EPI) / 4) of the tile.  Lane i owns row
+    // 32q+i in the math (tcgen05.ld 32x32b: lane = row, registers = columns);
+    // rows are staged through shared memory so the residual read and the
+    // destination write are coalesced 16-byte-per-lane row segments (a
+    // scattered destination row is contiguous in NHWC).  With NSTG = 2 the
+    // residual of the next tile is prefetched (cp.async) into the other
+    // staging buffer while this tile is finished and stored.
+    constexpr int EW_COLS = L::EW_COLS;  // columns per warp
+    constexpr int CPR = EW_COLS / 8;     // 16-byte chunks per staged row slice
+    constexpr int CH = EW_COLS < 32 ? EW_COLS : 32;  // columns per TMEM load
     const int q = warp & 3;
-    const int hf = (warp - 4) >> 2;
-    const int col0 = hf * HALF;
+    const int ew = warp - FIRST_EPI;
+    const int col0 = (ew >> 2) * EW_COLS;
     const int stg_off0 = L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
-    float* vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + (warp - 4) * 3 * HALF;
-    float* vbi = vsc + HALF;
-    float* vnw = vbi + HALF;  // next block's masker weights (masker-conv3 fusion)
+    float* const vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + ew * 3 * EW_COLS;
+    float* const vbi_w = vsc + EW_COLS;
+    float* const vnw = vbi_w + EW_COLS;  // next block's masker weights (masker-conv3 fusion)
     const __nv_bfloat16* resid = reinterpret_cast<const __nv_bfloat16*>(p.resid);
     __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
     const bool staged = !p.out_f32;
     const bool pre = staged && resid != nullptr;
+    const bool has_scale = p.scale != nullptr || p.col_index != nullptr;
+    // the common epilogues (bias [+ residual] [+ ReLU]) take a branch-free path
+    const bool plain = staged && !has_scale && !p.ymask_channel && !p.ymask_coarse && !p.mdot_w;
+    // the whole bias vector lives in smem for the kernel when it fits (the
+    // per-warp vector slices are the fallback for scale / masker-dot / lists)
+    const bool cached = !has_scale && !p.mdot_w && p.n_out <= L::VEC_BYTES / 4;
+    float* const bias_cache = reinterpret_cast<float*>(base + L::VEC_OFF);
+    if (cached) {
+      for (int i = threadIdx.x - FIRST_EPI * 32; i < p.n_out; i += NUM_EPI_WARPS * 32)
+        bias_cache[i] = p.bias ? __ldg(p.bias + i) : 0.f;
+      asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+    }
 
     // per-row destination of tile t for this lane's row
     struct RowInfo {
@@ -337,10 +444,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       RowPos rp;
       bool fp;
     };
-    auto row_info = [&](int t) {
+    auto row_raw = [&](int t) { return row_fetch(p, (t / n_tiles) * BM + q * 32 + lane); };
+    auto row_info = [&](int t, int raw) {
       RowInfo ri;
       const int m = (t / n_tiles) * BM + q * 32 + lane;
-      ri.valid = map_row(p, m, nvalid, ri.rp, ri.fp);
+      ri.valid = map_row_raw(p, m, nvalid, raw, ri.rp, ri.fp);
       ri.dst = 0;
       if (ri.valid) {
         if (p.out_mode == OUT_ROW) {
@@ -354,8 +462,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       return ri;
     };
     auto prefetch = [&](int t, const RowInfo& ri, int buf) {
-      const int c_base = (t % n_tiles) * BN + col0;  // n0 + col0
-      const int vchunks = max(0, min(HALF, p.n_out - c_base)) >> 3;
+      const int c_base = (t % n_tiles) * BN + col0;
+      const int vchunks = max(0, min(EW_COLS, p.n_out - c_base)) >> 3;
       const uint32_t sbase = base_u32 + stg_off0 + buf * L::STG_BUF;
 #pragma unroll 4
       for (int idx = lane; idx < 32 * CPR; idx += 32) {
@@ -369,17 +477,56 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-
     auto next_valid = [&](int t) {
       while (t < tiles && tile_info<BN>(p, t, n_tiles).skip) t += gridDim.x;
       return t;
+    };
+    // per-column epilogue vectors of tile t: loads issued a tile ahead (into
+    // registers), written to the warp's smem slice once the previous tile's
+    // math is done
+    constexpr int VPL = (EW_COLS + 31) / 32;  // vector entries per lane
+    struct VecPre {
+      float sc[VPL], bi[VPL], nw[VPL];
+    };
+    auto vec_load = [&](int t) {
+      VecPre v;
+      const TileInfo tv = tile_info<BN>(p, t, n_tiles);
+      const int cb = tv.n0 + col0;
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int i = lane + 32 * u;
+        const int c = cb + i;
+        int src = c;
+        bool live = i < EW_COLS && c < p.n_out;
+        if (p.col_index) {  // per-sample channel list: column c holds channel col_index[c]
+          live = live && c < tv.kc;
+          src = live ? __ldg(p.col_index + (size_t)tv.sample * p.col_index_ld + c) : 0;
+        }
+        v.sc[u] = (p.scale && live) ? __ldg(p.scale + src) : 1.f;
+        v.bi[u] = (p.bias && live) ? __ldg(p.bias + src) : 0.f;
+        v.nw[u] = (p.mdot_w && live) ? __ldg(p.mdot_w + c) : 0.f;
+      }
+      return v;
+    };
+    auto vec_store = [&](const VecPre& v) {
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int i = lane + 32 * u;
+        if (i < EW_COLS) {
+          if (has_scale) vsc[i] = v.sc[u];
+          vbi_w[i] = v.bi[u];
+          if (p.mdot_w) vnw[i] = v.nw[u];
+        }
+      }
     };
     uint32_t local = 0;
     int t = next_valid(blockIdx.x);
     RowInfo cur;
     if (t < tiles) {
-      cur = row_info(t);
+      cur = row_info(t, row_raw(t));
       if (pre) prefetch(t, cur, 0);
+      if (!cached) vec_store(vec_load(t));
+      __syncwarp();
     }
     for (; t < tiles; ++local) {
       const TileInfo ti = tile_info<BN>(p, t, n_tiles);
@@ -387,8 +534,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (local >> 1) & 1;
       const int buf = NSTG == 2 ? (local & 1) : 0;
       uint8_t* stg = base + stg_off0 + buf * L::STG_BUF;
-      const int c_base = ti.n0 + col0;                     // first output channel of this warp
-      const int nch = max(0, min(HALF, p.n_out - c_base));  // valid channels (multiple of 8)
+      const int c_base = ti.n0 + col0;                        // first output channel of this warp
+      const int nch = max(0, min(EW_COLS, p.n_out - c_base));  // valid channels (multiple of 8)
       const int vchunks = nch >> 3;
       bool do_relu = p.relu != 0;
       float ymul = 1.f;
@@ -398,97 +545,153 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.relu_inactive_coarse) do_relu = p.relu_inactive_coarse[cell] == 0;
         if (p.ymask_coarse) ymul = p.ymask_coarse[cell] ? 1.f : 0.f;
       }
-      for (int i = lane; i < HALF; i += 32) {
-        const int c = c_base + i;
-        int src = c;
-        bool live = c < p.n_out;
-        if (p.col_index) {  // per-sample channel list: column c holds channel col_index[c]
-          live = live && c < ti.kc;
-          src = live ? __ldg(p.col_index + (size_t)ti.sample * p.col_index_ld + c) : 0;
-        }
-        vsc[i] = (p.scale && live) ? __ldg(p.scale + src) : 1.f;
-        vbi[i] = (p.bias && live) ? __ldg(p.bias + src) : 0.f;
-        if (p.mdot_w) vnw[i] = c < p.n_out ? __ldg(p.mdot_w + c) : 0.f;
+      // next tile's rows and vectors: issue the global loads now, use them later
+      const int tn = next_valid(t + gridDim.x);
+      RowInfo nxt = cur;
+      VecPre vpn;
+      int raw_n = 0;
+      if (tn < tiles) {
+        raw_n = row_raw(tn);
+        if (!cached) vpn = vec_load(tn);
       }
+      const float* const vbi = cached ? bias_cache + c_base : vbi_w;
       float pd = 0.f;  // this row's partial dot with the next masker
       mbar_wait(&acc_full[acc], acc_phase);
+      if (trc && ew == 0 && lane == 0 && local < 1024) trc[TRACE_EPI + 4 * local] = global_ns();
       tc_fence_after();
       if (pre) asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col0;
       uint8_t* my_row = stg + lane * L::STG_ROW;
-#pragma unroll 1
-      for (int j = 0; j < HALF / 32; ++j) {
-        if (j * 32 >= nch) break;
-        uint32_t r[32];
-        if (ti.num_kb > 0) {
-          tmem_ld_32x32b_x32(tbase + j * 32, r);
-        } else {  // empty K (no channel kept): y = 0
-#pragma unroll
-          for (int e = 0; e < 32; ++e) r[e] = 0u;
+      // generic 8-column step: affine, masks, residual, ReLU, store
+      auto finish8 = [&](const uint32_t* rv, int cl) {
+        float v[8];
+        const float4 b0 = *reinterpret_cast<const float4*>(vbi + cl);
+        const float4 b1 = *reinterpret_cast<const float4*>(vbi + cl + 4);
+        float4 s0 = make_float4(1.f, 1.f, 1.f, 1.f), s1 = s0;
+        if (has_scale) {
+          s0 = *reinterpret_cast<const float4*>(vsc + cl);
+          s1 = *reinterpret_cast<const float4*>(vsc + cl + 4);
         }
-        if (!cur.valid) continue;
+        v[0] = fmaf(__uint_as_float(rv[0]), s0.x, b0.x);
+        v[1] = fmaf(__uint_as_float(rv[1]), s0.y, b0.y);
+        v[2] = fmaf(__uint_as_float(rv[2]), s0.z, b0.z);
+        v[3] = fmaf(__uint_as_float(rv[3]), s0.w, b0.w);
+        v[4] = fmaf(__uint_as_float(rv[4]), s1.x, b1.x);
+        v[5] = fmaf(__uint_as_float(rv[5]), s1.y, b1.y);
+        v[6] = fmaf(__uint_as_float(rv[6]), s1.z, b1.z);
+        v[7] = fmaf(__uint_as_float(rv[7]), s1.w, b1.w);
+        if (p.ymask_channel) {
+          const uint2 mk = __ldg(reinterpret_cast<const uint2*>(
+              p.ymask_channel + (size_t)cur.rp.n * p.n_out + c_base + cl));
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int cl = j * 32 + g * 8;  // local column within this warp's half
-          if (cl >= nch) break;
-          float v[8];
-          const float4 s0 = *reinterpret_cast<const float4*>(vsc + cl);
-          const float4 s1 = *reinterpret_cast<const float4*>(vsc + cl + 4);
-          const float4 b0 = *reinterpret_cast<const float4*>(vbi + cl);
-          const float4 b1 = *reinterpret_cast<const float4*>(vbi + cl + 4);
-          v[0] = fmaf(__uint_as_float(r[g * 8 + 0]), s0.x, b0.x);
-          v[1] = fmaf(__uint_as_float(r[g * 8 + 1]), s0.y, b0.y);
-          v[2] = fmaf(__uint_as_float(r[g * 8 + 2]), s0.z, b0.z);
-          v[3] = fmaf(__uint_as_float(r[g * 8 + 3]), s0.w, b0.w);
-          v[4] = fmaf(__uint_as_float(r[g * 8 + 4]), s1.x, b1.x);
-          v[5] = fmaf(__uint_as_float(r[g * 8 + 5]), s1.y, b1.y);
-          v[6] = fmaf(__uint_as_float(r[g * 8 + 6]), s1.z, b1.z);
-          v[7] = fmaf(__uint_as_float(r[g * 8 + 7]), s1.w, b1.w);
-          if (p.ymask_channel) {
-            const uint2 mk = __ldg(reinterpret_cast<const uint2*>(
-                p.ymask_channel + (size_t)cur.rp.n * p.n_out + c_base + cl));
+          for (int e = 0; e < 8; ++e)
+            v[e] *= ((e < 4 ? (mk.x >> (8 * e)) : (mk.y >> (8 * (e - 4)))) & 0xff) ? 1.f : 0.f;
+        }
+        if (p.ymask_coarse) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              v[e] *= ((e < 4 ? (mk.x >> (8 * e)) : (mk.y >> (8 * (e - 4)))) & 0xff) ? 1.f : 0.f;
-          }
-          if (p.ymask_coarse) {
+          for (int e = 0; e < 8; ++e) v[e] *= ymul;
+        }
+        uint4* slot = reinterpret_cast<uint4*>(my_row + cl * 2);
+        if (pre) {
+          const uint4 rr = *slot;
+          float2 f;
+          f = unpack_bf16x2(rr.x); v[0] += f.x; v[1] += f.y;
+          f = unpack_bf16x2(rr.y); v[2] += f.x; v[3] += f.y;
+          f = unpack_bf16x2(rr.z); v[4] += f.x; v[5] += f.y;
+          f = unpack_bf16x2(rr.w); v[6] += f.x; v[7] += f.y;
+        }
+        if (do_relu) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] *= ymul;
-          }
-          uint4* slot = reinterpret_cast<uint4*>(my_row + cl * 2);
-          if (pre) {
-            const uint4 rr = *slot;
+          for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+        }
+        if (!staged) {
+          float* o = reinterpret_cast<float*>(p.out) + cur.dst * p.out_ld + c_base + cl;
+          reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], v[3]);
+          reinterpret_cast<float4*>(o)[1] = make_float4(v[4], v[5], v[6], v[7]);
+        } else {
+          uint4 w;
+          w.x = pack_bf16x2(v[0], v[1]);
+          w.y = pack_bf16x2(v[2], v[3]);
+          w.z = pack_bf16x2(v[4], v[5]);
+          w.w = pack_bf16x2(v[6], v[7]);
+          *slot = w;
+          if (p.mdot_w) {  // the stored (bf16) values are what the next masker sees
+            const float4 n0 = *reinterpret_cast<const float4*>(vnw + cl);
+            const float4 n1 = *reinterpret_cast<const float4*>(vnw + cl + 4);
             float2 f;
-            f = unpack_bf16x2(rr.x); v[0] += f.x; v[1] += f.y;
-            f = unpack_bf16x2(rr.y); v[2] += f.x; v[3] += f.y;
-            f = unpack_bf16x2(rr.z); v[4] += f.x; v[5] += f.y;
-            f = unpack_bf16x2(rr.w); v[6] += f.x; v[7] += f.y;
+            f = unpack_bf16x2(w.x); pd = fmaf(f.x, n0.x, pd); pd = fmaf(f.y, n0.y, pd);
+            f = unpack_bf16x2(w.y); pd = fmaf(f.x, n0.z, pd); pd = fmaf(f.y, n0.w, pd);
+            f = unpack_bf16x2(w.z); pd = fmaf(f.x, n1.x, pd); pd = fmaf(f.y, n1.y, pd);
+            f = unpack_bf16x2(w.w); pd = fmaf(f.x, n1.z, pd); pd = fmaf(f.y, n1.w, pd);
           }
-          if (do_relu) {
+        }
+      };
+      // branch-free CH-column step of the plain epilogue: y = acc + bias (+ resid), ReLU
+      auto plain_chunk = [&](const uint32_t* rv, int cl, bool with_resid, bool relu) {
+        uint4* slot = reinterpret_cast<uint4*>(my_row + cl * 2);
+        uint4 rr[CH / 8];
+        if (with_resid) {
+#pragma unroll
+          for (int g = 0; g < CH / 8; ++g) rr[g] = slot[g];
+        }
+#pragma unroll
+        for (int g = 0; g < CH / 8; ++g) {
+          const float4 b0 = *reinterpret_cast<const float4*>(vbi + cl + g * 8);
+          const float4 b1 = *reinterpret_cast<const float4*>(vbi + cl + g * 8 + 4);
+          float v[8];
+          v[0] = __uint_as_float(rv[g * 8 + 0]) + b0.x;
+          v[1] = __uint_as_float(rv[g * 8 + 1]) + b0.y;
+          v[2] = __uint_as_float(rv[g * 8 + 2]) + b0.z;
+          v[3] = __uint_as_float(rv[g * 8 + 3]) + b0.w;
+          v[4] = __uint_as_float(rv[g * 8 + 4]) + b1.x;
+          v[5] = __uint_as_float(rv[g * 8 + 5]) + b1.y;
+          v[6] = __uint_as_float(rv[g * 8 + 6]) + b1.z;
+          v[7] = __uint_as_float(rv[g * 8 + 7]) + b1.w;
+          if (with_resid) {
+            float2 f;
+            f = unpack_bf16x2(rr[g].x); v[0] += f.x; v[1] += f.y;
+            f = unpack_bf16x2(rr[g].y); v[2] += f.x; v[3] += f.y;
+            f = unpack_bf16x2(rr[g].z); v[4] += f.x; v[5] += f.y;
+            f = unpack_bf16x2(rr[g].w); v[6] += f.x; v[7] += f.y;
+          }
+          if (relu) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
           }
-          if (!staged) {
-            float* o = reinterpret_cast<float*>(p.out) + cur.dst * p.out_ld + c_base + cl;
-            reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], v[3]);
-            reinterpret_cast<float4*>(o)[1] = make_float4(v[4], v[5], v[6], v[7]);
+          uint4 w;
+          w.x = pack_bf16x2(v[0], v[1]);
+          w.y = pack_bf16x2(v[2], v[3]);
+          w.z = pack_bf16x2(v[4], v[5]);
+          w.w = pack_bf16x2(v[6], v[7]);
+          slot[g] = w;
+        }
+      };
+      const bool full = nch == EW_COLS;
+#pragma unroll 1
+      for (int j = 0; j < EW_COLS / CH; ++j) {
+        if (j * CH >= nch) break;
+        uint32_t r[CH];
+        if (ti.num_kb > 0 && !(p.dbg & 4)) {
+          tmem_ld_32x32b<CH>(tbase + j * CH, r);
+        } else {  // empty K (no channel kept): y = 0
+#pragma unroll
+          for (int e = 0; e < CH; ++e) r[e] = 0u;
+        }
+        if (!cur.valid || (p.dbg & 1)) continue;
+        if (plain && full) {
+          if (pre) {
+            if (do_relu) plain_chunk(r, j * CH, true, true);
+            else plain_chunk(r, j * CH, true, false);
           } else {
-            uint4 w;
-            w.x = pack_bf16x2(v[0], v[1]);
-            w.y = pack_bf16x2(v[2], v[3]);
-            w.z = pack_bf16x2(v[4], v[5]);
-            w.w = pack_bf16x2(v[6], v[7]);
-            *slot = w;
-            if (p.mdot_w) {  // the stored (bf16) values are what the next masker sees
-              const float4 n0 = *reinterpret_cast<const float4*>(vnw + cl);
-              const float4 n1 = *reinterpret_cast<const float4*>(vnw + cl + 4);
-              float2 f;
-              f = unpack_bf16x2(w.x); pd = fmaf(f.x, n0.x, pd); pd = fmaf(f.y, n0.y, pd);
-              f = unpack_bf16x2(w.y); pd = fmaf(f.x, n0.z, pd); pd = fmaf(f.y, n0.w, pd);
-              f = unpack_bf16x2(w.z); pd = fmaf(f.x, n1.x, pd); pd = fmaf(f.y, n1.y, pd);
-              f = unpack_bf16x2(w.w); pd = fmaf(f.x, n1.z, pd); pd = fmaf(f.y, n1.w, pd);
-            }
+            if (do_relu) plain_chunk(r, j * CH, false, true);
+            else plain_chunk(r, j * CH, false, false);
+          }
+        } else {
+#pragma unroll
+          for (int g = 0; g < CH / 8; ++g) {
+            if (j * CH + g * 8 >= nch) break;
+            finish8(r + g * 8, j * CH + g * 8);
           }
         }
       }
@@ -509,28 +712,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       // accumulator consumed: hand the TMEM buffer back to the MMA warp early
+      if (trc && ew == 0 && lane == 0 && local < 1024) trc[TRACE_EPI + 4 * local + 1] = global_ns();
       tc_fence_before();
       mbar_arrive(&acc_empty[acc]);
       __syncwarp();
-      // next tile's rows; with two staging buffers its residual streams in now
-      const int tn = next_valid(t + gridDim.x);
-      RowInfo nxt = cur;
       if (tn < tiles) {
-        nxt = row_info(tn);
+        nxt = row_info(tn, raw_n);
+        if (!cached) vec_store(vpn);  // this tile's vector reads are done (syncwarp above)
+        // with two staging buffers the next residual streams in now
         if (pre && NSTG == 2) prefetch(tn, nxt, (local + 1) & 1);
       }
-      if (staged && vchunks > 0) {
-#pragma unroll 4
-        for (int idx = lane; idx < 32 * CPR; idx += 32) {
-          const int r = idx / CPR, c = idx % CPR;
+      if (staged && vchunks > 0 && !(p.dbg & 2)) {
+        // row-major sweep of the staged 32 x EW_COLS slice: each instruction
+        // writes 32 / CPR whole row segments
+        constexpr int RPI = 32 / CPR;  // rows per warp instruction
+        const int cc = lane % CPR;
+        const int rr0 = lane / CPR;
+#pragma unroll 8
+        for (int it2 = 0; it2 < CPR; ++it2) {
+          const int r = it2 * RPI + rr0;
           const int rv = __shfl_sync(0xffffffffu, (int)cur.valid, r);
           const long long dr = __shfl_sync(0xffffffffu, cur.dst, r);
-          if (rv && c < vchunks)
-            *reinterpret_cast<uint4*>(outp + dr * p.out_ld + c_base + c * 8) =
-                *reinterpret_cast<const uint4*>(stg + r * L::STG_ROW + c * 16);
+          if (rv && cc < vchunks)
+            *reinterpret_cast<uint4*>(outp + dr * p.out_ld + c_base + cc * 8) =
+                *reinterpret_cast<const uint4*>(stg + r * L::STG_ROW + cc * 16);
         }
       }
       __syncwarp();
+      if (trc && ew == 0 && lane == 0 && local < 1024) trc[TRACE_EPI + 4 * local + 2] = global_ns();
       if (tn < tiles && pre && NSTG == 1) prefetch(tn, nxt, 0);
       cur = nxt;
       t = tn;
@@ -561,7 +770,12 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  static const int grid_env = [] {
+    const char* e = getenv("LAUD_GRID");  // debug: cap the persistent grid
+    return e ? atoi(e) : 0;
+  }();
   int grid = tiles_max < num_sms ? tiles_max : num_sms;
+  if (grid_env > 0 && grid > grid_env) grid = grid_env;
   if (grid < 1) grid = 1;
   conv_gemm_kernel<BN, STAGES, NSTG><<<grid, NUM_THREADS, L::ALLOC, stream>>>(tmap_a, tmap, p);
   return cudaGetLastError();

@@ -34,6 +34,7 @@ struct ConvParams {
   int in_ld;             // elements per pixel row (>= in_c, multiple of 8)
   int a_compact;         // 1: A row = m directly (1x1, taps must be 1)
   int a_tma;             // 1: A rows gathered with TMA tile::gather4 (else cp.async)
+  int a_tile;            // 1: the 128 A rows of a tile are contiguous: one 2D TMA box
   int a_rows;            // rows of the A tensor map (also the out-of-bounds marker)
   int ksize, stride, pad;
   int kpad;              // in_c rounded up to 64
@@ -70,6 +71,16 @@ struct ConvParams {
   float* mdot_out;
   // ---- fault hook (tests only): shift the first patch's destination one cell
   int misplace_first;
+  // ---- debug timeline (laud_debug_set_trace): CTA 0 records %globaltimer at
+  //      pipeline events; nullptr (always, outside tools/) = off
+  unsigned long long* trace;
+  int dbg;  // debug ablations (LAUD_DBG, tools only): 1 no math, 2 no stores, 4 no TMEM loads,
+           // 8 no A loads, 16 no B loads
 };
+
+// trace slots (CTA 0): MMA full-wait done per k-block, B-producer empty-wait
+// done per k-block, A-producer (warp 0) empty-wait done per k-block, epilogue
+// warp 4 per tile: acc_full done / stores done.
+constexpr int TRACE_MMA = 0, TRACE_B = 4096, TRACE_A = 8192, TRACE_EPI = 12288, TRACE_SLOTS = 16384;
 
 }  // namespace laud

@@ -1,0 +1,94 @@
+"""Time the conv engine on isolated shapes (CUDA events, L2 flushed per rep).
+
+usage: python tools/engine_probe.py [name ...]   (env LAUD_BN / LAUD_A_TMA apply)
+Prints one JSON line per shape: us, TFLOP/s, compulsory GB/s.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2308_15949_b200 import channel as CH  # noqa: E402
+
+
+def bf(*shape):
+    return (torch.randn(*shape, device="cuda") * 0.5).bfloat16()
+
+
+def shape_defs():
+    d = {}
+    # name: (rows/batch geometry, ...) -> dict of conv kwargs and alg flops/bytes
+    d["gemm_s3"] = dict(kind="gemm", m=148 * 128 * 2, n=256, k=2304)
+    d["gemm_s3_1w"] = dict(kind="gemm", m=148 * 128, n=256, k=2304)
+    d["gemm_k256_n1024"] = dict(kind="gemm", m=25088, n=1024, k=256)
+    d["gemm_k1024_n256"] = dict(kind="gemm", m=50176, n=256, k=1024)
+    d["tiny"] = dict(kind="gemm", m=128, n=256, k=64)
+    d["one_wave_k256"] = dict(kind="gemm", m=148 * 128, n=256, k=256)
+    d["two_wave_k256"] = dict(kind="gemm", m=2 * 148 * 128, n=256, k=256)
+    d["four_wave_k256"] = dict(kind="gemm", m=4 * 148 * 128, n=256, k=256)
+    d["conv2_s3"] = dict(kind="conv3x3", n=256, h=14, c=256)
+    d["conv2_s2"] = dict(kind="conv3x3", n=256, h=28, c=128)
+    d["conv2_s1"] = dict(kind="conv3x3", n=256, h=56, c=64)
+    d["conv1_s1"] = dict(kind="gemm", m=256 * 56 * 56, n=64, k=256)
+    d["conv3_s3"] = dict(kind="conv3", m=25088, n=1024, k=256)
+    d["conv3_s1"] = dict(kind="conv3", m=256 * 56 * 56 // 2, n=256, k=64)
+    return d
+
+
+def run(name, spec, flush, reps=20):
+    if spec["kind"] in ("gemm", "conv3"):
+        m, n, k = spec["m"], spec["n"], spec["k"]
+        a = bf(m, k)
+        w = bf(n, 1, k)
+        out = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+        resid = out if spec["kind"] == "conv3" else None
+        if resid is not None:
+            out.copy_(bf(m, n))
+        kw = dict(act=a, in_hw=(m, 1), in_c=k, in_ld=k, weight=w, n_out=n, out=out, out_ld=n,
+                  out_hw=(m, 1), batch=1, a_compact=1, resid=resid, resid_ld=n if resid is not None else 0,
+                  relu=1)
+        flops = 2.0 * m * n * k
+        nbytes = 2.0 * (m * k + n * k + m * n * (2 if resid is not None else 1))
+    else:
+        b, h, c = spec["n"], spec["h"], spec["c"]
+        a = bf(b, h, h, c)
+        w = bf(c, 9, c)
+        out = torch.empty(b * h * h, c, dtype=torch.bfloat16, device="cuda")
+        kw = dict(act=a, in_hw=(h, h), in_c=c, in_ld=c, weight=w, n_out=c, out=out, out_ld=c,
+                  out_hw=(h, h), batch=b, ksize=3, pad=1, relu=1, out_mode=CH.OUT_ROW)
+        m = b * h * h
+        flops = 2.0 * m * c * 9 * c
+        nbytes = 2.0 * (m * c * 2 + 9 * c * c)
+    for _ in range(3):
+        CH.conv(**kw)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        CH.conv(**kw)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    ms = ts[len(ts) // 2]
+    return dict(name=name, us=round(ms * 1e3, 2), tflops=round(flops / ms / 1e9, 1),
+                gbs=round(nbytes / ms / 1e6, 1), ideal_us_tensor=round(flops / 1.3841e15 * 1e6, 2),
+                ideal_us_hbm=round(nbytes / 6.55e12 * 1e6, 2),
+                env={k: os.environ.get(k) for k in ("LAUD_BN", "LAUD_A_TMA", "LAUD_CTA2") if os.environ.get(k)})
+
+
+def main():
+    torch.cuda.set_device(0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    defs = shape_defs()
+    names = sys.argv[1:] or list(defs)
+    for nm in names:
+        print(json.dumps(run(nm, defs[nm], flush)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
