@@ -51,13 +51,17 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="laud", choices=["laud", "reference"])
     ap.add_argument("--arch", default="resnet101")
-    ap.add_argument("--paradigm", default="spatial", choices=["spatial", "layer", "static"])
-    ap.add_argument("--plan", default="4-2-2-1")
+    ap.add_argument("--paradigm", default="spatial", choices=["spatial", "channel", "layer", "static"])
+    ap.add_argument("--plan", default=None, help="S per stage (spatial, default 4-2-2-1) or "
+                    "G per stage (channel, default 1-1-1-1)")
     ap.add_argument("--ratio", type=float, default=0.5)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--no-baselines", action="store_true", help="skip static / cuDNN / CPU / sweep legs")
     ap.add_argument("--cpu-images", type=int, default=2)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.plan is None:
+        a.plan = "1-1-1-1" if a.paradigm == "channel" else "4-2-2-1"
+    return a
 
 
 def dist_env():
@@ -101,9 +105,11 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2308_15949_b200.network import make_params
+    from paper_2308_15949_b200.network import add_channel_maskers, make_params
     params = make_params(args.arch, 0)
     plan = tuple(int(v) for v in args.plan.split("-"))
+    if args.paradigm == "channel":
+        add_channel_maskers(params, plan, 0)
     from oracle import laud_oracle as O
     img = np.random.default_rng(1).integers(0, 256, (1, 224, 224, 3), dtype=np.uint8)
     for _ in range(max(1, min(args.warmup, 1))):
@@ -336,13 +342,26 @@ def block_sweep(torch, args, flush):
         cells = (o.height // s) * (o.width // s)
         row = {}
         for r in (0.2, 0.5, 0.8, 1.0):
-            k = int(round(r * cells))
-            cz = np.zeros((n, cells), np.uint8)
-            for i in range(n):
-                cz[i, rng.permutation(cells)[:k]] = 1
-            coarse = torch.from_numpy(cz.reshape(-1)).cuda()
             xx = x.clone()
-            g, _ = capture(torch, lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp), 2)
+            if args.paradigm == "channel":
+                # exact-count per-sample channel masks (G = plan entry), SURVEY §8(d) config 4
+                cm, g_ = blk.conv2.out_channels, s
+                d = cm // g_
+                k = int(round(r * d))
+                mm = np.zeros((n, db.cmid_p), np.uint8)
+                for i in range(n):
+                    keep = np.repeat(np.isin(np.arange(d), rng.permutation(d)[:k]), g_)
+                    mm[i, :cm] = keep
+                chm = torch.from_numpy(mm.reshape(-1)).cuda()
+                fn = lambda: db.forward(xx, "channel", out=xx, ws=wsp, chmask=chm)  # noqa: E731
+            else:
+                k = int(round(r * cells))
+                cz = np.zeros((n, cells), np.uint8)
+                for i in range(n):
+                    cz[i, rng.permutation(cells)[:k]] = 1
+                coarse = torch.from_numpy(cz.reshape(-1)).cuda()
+                fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp)  # noqa: E731
+            g, _ = capture(torch, fn, 2)
             tot, _ = timed_graph(torch, g, 10, flush, torch.cuda.current_stream())
             row[str(r)] = round(1e3 * tot / 10, 1)
             del g
@@ -350,7 +369,7 @@ def block_sweep(torch, args, flush):
         g, _ = capture(torch, lambda: db.forward(xx, "static", out=xx, ws=wsp), 2)
         tot, _ = timed_graph(torch, g, 10, flush, torch.cuda.current_stream())
         row["static"] = round(1e3 * tot / 10, 1)
-        out[f"s{bp['stage']}b1_S{s}"] = row
+        out[f"s{bp['stage']}b1_{'G' if args.paradigm == 'channel' else 'S'}{s}"] = row
     return out
 
 

@@ -192,6 +192,9 @@ typedef struct laud_block_args {
   const uint8_t* prev_coarse;
   float* dn;
   const float* next_wdiff;
+  /* EXT: per-decision bias added to the channel masker's logit gap l0 - l1
+   * (nullable; calibrates the kept ratio like a trained FLOPs loss would). */
+  const float* ch_bias;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):
@@ -201,7 +204,7 @@ typedef struct laud_block_args {
 int laud_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c, const float* w1,
                         int hidden, const float* w2, int d, int g, int cm, int cm_p,
                         uint8_t* coarse, float* dvals, uint8_t* expanded, int* sel, int* count,
-                        void* stream);
+                        const float* bias, void* stream);
 
 /* Bytes of per-sample packed weights the channel paradigm needs. */
 size_t laud_channel_pack_bytes(int n, int c_in, int c_mid, int c_out);

@@ -199,8 +199,13 @@ def masker_hidden_width(d: int) -> int:
     return max(d // 16, 16)
 
 
-def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None) -> ChannelMask:
-    """GAP -> relu(W1) -> W2 -> interleaved (keep, skip) pairs (`reference.py:189-218`)."""
+def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None,
+                           bias: float = 0.0) -> ChannelMask:
+    """GAP -> relu(W1) -> W2 -> interleaved (keep, skip) pairs (`reference.py:189-218`).
+
+    ``bias`` (EXT, default 0 = reference) is added to the keep logit l0, i.e.
+    to every gap l0 - l1 (the device masker's calibration bias).
+    """
     w1, w2 = weights
     hidden_w, c = w1.shape
     if x.shape[1] != c:
@@ -210,6 +215,9 @@ def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None) 
     d = w2.shape[0] // 2
     hid = np.maximum(x.mean(axis=(2, 3)) @ w1.T, 0.0)
     logits = (hid @ w2.T).reshape(-1, d, 2)
+    if bias:
+        logits = logits.copy()
+        logits[..., 0] += bias
     coarse, soft = _decide(logits, mode, tau, rng)
     return ChannelMask(coarse, np.repeat(coarse, g, axis=1), g, soft)
 
@@ -767,6 +775,14 @@ def network_forward(params: dict, images_u8: np.ndarray, paradigm: str = "spatia
         if paradigm == "static":
             cfg = DynamicConfig(Paradigm.STATIC)
             mask = None
+        elif paradigm == "channel":
+            g = plan[bp["stage"] - 1]
+            cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=g)
+            if masks is not None:
+                c = np.asarray(masks[i]).reshape(x.shape[0], -1).astype(bool)
+                mask = ChannelMask(c, np.repeat(c, g, axis=1), g)
+            else:
+                mask = channel_masker_forward(x, (bp["ch_w1"], bp["ch_w2"]), g, bias=bias)
         elif paradigm == "layer":
             cfg = DynamicConfig(Paradigm.LAYER)
             if masks is not None:

@@ -55,7 +55,7 @@ class BlockArgs(C.Structure):
         ("misplace_first", C.c_int), ("ch_w1", _vp), ("ch_w2", _vp), ("ch_hidden", C.c_int),
         ("ch_d", C.c_int), ("ch_groups", C.c_int), ("given_chmask", _vp), ("ch_coarse", _vp),
         ("ch_expanded", _vp), ("ch_sel", _vp), ("ch_count", _vp), ("ch_dvals", _vp),
-        ("wpack", _vp), ("prev_coarse", _vp), ("dn", _vp), ("next_wdiff", _vp),
+        ("wpack", _vp), ("prev_coarse", _vp), ("dn", _vp), ("next_wdiff", _vp), ("ch_bias", _vp),
     ]
 
 
@@ -77,7 +77,7 @@ _SIGS = {
     "laud_masker_partial_floats": (C.c_size_t, [C.c_int] * 6),
     "laud_channel_pack_bytes": (C.c_size_t, [C.c_int] * 4),
     "laud_channel_masker": (C.c_int, [_vp] + [C.c_int] * 5 + [_vp, C.c_int, _vp] + [C.c_int] * 4
-                            + [_vp] * 6),
+                            + [_vp] * 7),
     "laud_spatial_masker": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.c_int, _vp, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp]),
     "laud_cells_from_mask": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp]),

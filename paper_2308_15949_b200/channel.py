@@ -114,7 +114,7 @@ def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None):
     cnt = torch.empty(n, dtype=torch.int32, device="cuda")
     _lib.call("laud_channel_masker", D.ptr(xd), 1, cp, n, h * w, cp, D.ptr(t_w1), hd, D.ptr(t_w2),
               d, g, cm, cmp, D.ptr(coarse), D.ptr(dvals), D.ptr(exp), D.ptr(sel), D.ptr(cnt),
-              D.stream_handle())
+              None, D.stream_handle())
     soft = None
     if mode == "inference":
         cz = coarse.view(n, d).bool().cpu().numpy()

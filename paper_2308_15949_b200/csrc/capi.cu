@@ -41,7 +41,7 @@ cudaError_t launch_gap(const void* x, int n, int hw, int c, void* y, cudaStream_
 cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c,
                                   const float* w1, int hd, const float* w2, int d, int g, int cm,
                                   int cm_p, uint8_t* coarse, float* dvals, uint8_t* expanded,
-                                  int* sel, int* count, cudaStream_t s);
+                                  int* sel, int* count, const float* bias, cudaStream_t s);
 cudaError_t launch_channel_lists(const uint8_t* expanded, int n, int cm_p, int* sel, int* count,
                                  cudaStream_t s);
 cudaError_t launch_pack_weights(const void* src, int src_rows, int taps, int src_k, void* dst,
@@ -444,13 +444,13 @@ static int round64(int v) { return (v + 63) / 64 * 64; }
 int laud_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c, const float* w1,
                         int hidden, const float* w2, int d, int g, int cm, int cm_p,
                         uint8_t* coarse, float* dvals, uint8_t* expanded, int* sel, int* count,
-                        void* stream) {
+                        const float* bias, void* stream) {
   if (c % 8 || ld % 8 || ld < c) return fail(LAUD_ERR_SHAPE, "channels must be multiples of 8");
   if (d < 1 || g < 1 || cm != d * g || cm > cm_p) return fail(LAUD_ERR_GRANULARITY, "bad D/G");
   if ((size_t)(c + hidden + d) * 4 > 48 * 1024) return fail(LAUD_ERR_SHAPE, "masker too wide");
   ProfScope ps(1, (cudaStream_t)stream);
   return cuda_check(launch_channel_masker(x, x_f32, ld, n, hw, c, w1, hidden, w2, d, g, cm, cm_p,
-                                          coarse, dvals, expanded, sel, count,
+                                          coarse, dvals, expanded, sel, count, bias,
                                           (cudaStream_t)stream),
                     "channel masker", 1);
 }
@@ -484,7 +484,8 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
     if ((rc = cuda_check(launch_channel_masker(a->x, 0, a->x_ld, n, a->h_in * a->w_in, a->c_in,
                                                a->ch_w1, a->ch_hidden, a->ch_w2, a->ch_d,
                                                a->ch_groups, cm, cmp, a->ch_coarse, a->ch_dvals,
-                                               a->ch_expanded, a->ch_sel, a->ch_count, st),
+                                               a->ch_expanded, a->ch_sel, a->ch_count, a->ch_bias,
+                                               st),
                          "channel masker", 1)))
       return rc;
   }

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) channel_masker_kernel(
     const T* __restrict__ x, int ld, int hw, int c, const float* __restrict__ w1, int hd,
     const float* __restrict__ w2, int d, int g, int cm, int cm_p, uint8_t* __restrict__ coarse,
     float* __restrict__ dvals, uint8_t* __restrict__ expanded, int* __restrict__ sel,
-    int* __restrict__ count) {
+    int* __restrict__ count, const float* __restrict__ bias) {
   extern __shared__ float sm[];
   float* gap = sm;
   float* hid = gap + c;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) channel_masker_kernel(
       l0 = fmaf(w2[(size_t)(2 * dd) * hd + j], hid[j], l0);
       l1 = fmaf(w2[(size_t)(2 * dd + 1) * hd + j], hid[j], l1);
     }
-    const float diff = l0 - l1;
+    const float diff = l0 - l1 + (bias ? bias[dd] : 0.f);  // EXT bias (calibration)
     dl[dd] = diff;
     coarse[(size_t)n * d + dd] = diff >= 0.f ? 1 : 0;
     if (dvals) dvals[(size_t)n * d + dd] = diff;
@@ -192,16 +192,16 @@ __global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ src, int s
 cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c,
                                   const float* w1, int hd, const float* w2, int d, int g, int cm,
                                   int cm_p, uint8_t* coarse, float* dvals, uint8_t* expanded,
-                                  int* sel, int* count, cudaStream_t s) {
+                                  int* sel, int* count, const float* bias, cudaStream_t s) {
   const size_t smem = (size_t)(c + hd + d) * sizeof(float);
   if (x_f32)
     channel_masker_kernel<float><<<n, 256, smem, s>>>(reinterpret_cast<const float*>(x), ld, hw, c,
                                                       w1, hd, w2, d, g, cm, cm_p, coarse, dvals,
-                                                      expanded, sel, count);
+                                                      expanded, sel, count, bias);
   else
     channel_masker_kernel<__nv_bfloat16><<<n, 256, smem, s>>>(
         reinterpret_cast<const __nv_bfloat16*>(x), ld, hw, c, w1, hd, w2, d, g, cm, cm_p, coarse,
-        dvals, expanded, sel, count);
+        dvals, expanded, sel, count, bias);
   return cudaGetLastError();
 }
 

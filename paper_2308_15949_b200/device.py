@@ -194,8 +194,11 @@ class DeviceBlock:
     def out_hw(self, h: int, w: int):
         return self.block.conv2.out_hw(h, w)
 
-    def set_channel_masker(self, w1, w2, g: int):
-        """Channel masker MLP (`reference.py:189-218`): w1 [h, C_in], w2 [2D, h], G."""
+    def set_channel_masker(self, w1, w2, g: int, bias: float = 0.0):
+        """Channel masker MLP (`reference.py:189-218`): w1 [h, C_in], w2 [2D, h], G.
+
+        ``bias`` (EXT, default 0 = reference) is added to every logit gap l0 - l1.
+        """
         w1 = np.asarray(w1, dtype=np.float32)
         w2 = np.asarray(w2, dtype=np.float32)
         if w1.shape[1] > self.cin_p:
@@ -206,6 +209,12 @@ class DeviceBlock:
         self.ch_w1 = torch.from_numpy(w1p).to(dev)
         self.ch_w2 = torch.from_numpy(np.ascontiguousarray(w2)).to(dev)
         self.ch_hidden, self.ch_d, self.ch_g = w1.shape[0], w2.shape[0] // 2, int(g)
+        self.set_channel_bias(bias)
+
+    def set_channel_bias(self, bias: float):
+        self.ch_bias_value = float(bias)
+        self.ch_bias = (torch.full((self.ch_d,), float(bias), dtype=torch.float32, device=self.ch_w1.device)
+                        if bias != 0.0 else None)
 
     def _channel_args(self, a, n, ws, chmask):
         cmp = self.cmid_p
@@ -223,6 +232,7 @@ class DeviceBlock:
             if getattr(self, "ch_w1", None) is None:
                 raise DeviceError("no channel mask given and no channel masker weights set")
             a.ch_w1, a.ch_w2 = ptr(self.ch_w1), ptr(self.ch_w2)
+            a.ch_bias = ptr(getattr(self, "ch_bias", None))
             a.ch_hidden, a.ch_d, a.ch_groups = self.ch_hidden, self.ch_d, self.ch_g
 
     def forward(self, x: torch.Tensor, paradigm: str = "spatial", s: int = 1,

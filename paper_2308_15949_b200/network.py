@@ -92,13 +92,15 @@ class LaudNetwork:
         params = make_params(arch, seed)
         self.params = params
         self.net = params["net"]
+        if paradigm == "channel":
+            add_channel_maskers(params, parse_plan(plan, self.net, Paradigm.CHANNEL).values, seed)
         self.paradigm = paradigm
         self.target_ratio = target_ratio
         self.device = torch.device(device)
         net = self.net
         para = Paradigm(paradigm)
-        if para is Paradigm.SPATIAL:
-            self.plan = parse_plan(plan, net, para).values
+        if para is Paradigm.SPATIAL or para is Paradigm.CHANNEL:
+            self.plan = parse_plan(plan, net, para).values  # S (spatial) or G (channel) per stage
         else:
             self.plan = tuple(net.stage_feature(i + 1).height for i in range(len(net.stages)))
         # stem: k x k / s2 conv over 3 channels via im2col (K = k*k*3 padded to 8)
@@ -127,6 +129,9 @@ class LaudNetwork:
             db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep,
                                masker_w=bp["masker_w"], device=device, fold_scale=True)
             s = self.plan[bp["stage"] - 1] if para is Paradigm.SPATIAL else 0
+            if para is Paradigm.CHANNEL:
+                g = self.plan[bp["stage"] - 1]
+                db.set_channel_masker(bp["ch_w1"], bp["ch_w2"], g)
             self.slots.append(BlockSlot(bp["stage"], bp["index"], db, s))
         fc_in = net.classifier_features
         self.fc_w = D.pack_weight(params["fc_w"][:, :, None, None], D.pad8(fc_in), device)
@@ -154,7 +159,7 @@ class LaudNetwork:
         return b[:numel].view(shape)
 
     def _block_paradigm(self, slot: BlockSlot) -> str:
-        return self.paradigm if self.paradigm in ("spatial", "layer") else "static"
+        return self.paradigm if self.paradigm in ("spatial", "layer", "channel") else "static"
 
     # ------------------------------------------------------------------ forward
     def forward(self, images: torch.Tensor, stream=None, record=None) -> torch.Tensor:
@@ -212,7 +217,9 @@ class LaudNetwork:
             y, coarse, cells, counts = db.forward(x, para, slot.s if para == "spatial" else 0,
                                                   out=out, stream=stream, ws=self.ws, **kw)
             prev_coarse = kw.get("coarse_out")
-            if record is not None and para != "static":
+            if record is not None and para == "channel":
+                record.append((slot, db._ch_coarse[: n * db.ch_d].clone(), db._ch_count[: 4 * n].clone()))
+            elif record is not None and para != "static":
                 ncell = n * (oh // slot.s) * (ow // slot.s) if para == "spatial" else n
                 record.append((slot, coarse[:ncell].clone(), counts[:8].clone()))
             x = y
@@ -234,6 +241,8 @@ class LaudNetwork:
         (1 - ratio) quantile (bias = -quantile).  Done once, outside timing.
         """
         ratio = self.target_ratio if ratio is None else ratio
+        if self.paradigm == "channel":
+            return self._calibrate_channel(images, ratio)
         if self.paradigm not in ("spatial", "layer"):
             return
         for slot in self.slots:
@@ -272,12 +281,48 @@ class LaudNetwork:
         torch.cuda.synchronize()
         return saved
 
+    def _calibrate_channel(self, images: torch.Tensor, ratio: float):
+        """Channel paradigm: per block, the bias on the masker's logit gaps that
+        keeps ``ratio`` of the D channel groups on the calibration batch."""
+        saved = []
+        orig_forward = D.DeviceBlock.forward
+
+        def hooked(db, x, paradigm="spatial", s=1, **kw):
+            if paradigm == "channel":
+                n, h, w, cp = x.shape
+                d, cmp = db.ch_d, db.cmid_p
+                dv = torch.empty(n * d, dtype=torch.float32, device=x.device)
+                tmp8 = torch.empty(n * max(d, cmp), dtype=torch.uint8, device=x.device)
+                exp = torch.empty(n * cmp, dtype=torch.uint8, device=x.device)
+                sel = torch.empty(n * cmp, dtype=torch.int32, device=x.device)
+                cnt = torch.empty(n, dtype=torch.int32, device=x.device)
+                _lib.call("laud_channel_masker", D.ptr(x), 0, cp, n, h * w, cp, D.ptr(db.ch_w1),
+                          db.ch_hidden, D.ptr(db.ch_w2), d, db.ch_g, d * db.ch_g, cmp, D.ptr(tmp8),
+                          D.ptr(dv), D.ptr(exp), D.ptr(sel), D.ptr(cnt), None, D.stream_handle())
+                q = torch.quantile(dv.double(), 1.0 - ratio).item()
+                db.set_channel_bias(-q)
+                saved.append(-q)
+            return orig_forward(db, x, paradigm, s, **kw)
+
+        D.DeviceBlock.forward = hooked
+        try:
+            self.forward(images)
+        finally:
+            D.DeviceBlock.forward = orig_forward
+        torch.cuda.synchronize()
+        return saved
+
     def masker_biases(self):
+        if self.paradigm == "channel":
+            return [getattr(slot.db, "ch_bias_value", 0.0) for slot in self.slots]
         return [slot.db.masker_bias for slot in self.slots]
 
     def set_masker_biases(self, biases):
         for slot, b in zip(self.slots, biases):
-            slot.db.masker_bias = float(b)
+            if self.paradigm == "channel":
+                slot.db.set_channel_bias(float(b))
+            else:
+                slot.db.masker_bias = float(b)
 
     def rate_stats(self, images: torch.Tensor):
         """Per-block measured activation ratio (host sync; not for timing)."""
@@ -286,10 +331,33 @@ class LaudNetwork:
         torch.cuda.synchronize()
         out = []
         for slot, coarse, counts in rec:
+            if self.paradigm == "channel":
+                out.append(dict(stage=slot.stage, index=slot.index, g=slot.db.ch_g,
+                                r=float(coarse.float().mean().item()),
+                                kept=int(counts.view(torch.int32).sum().item())))
+                continue
             out.append(dict(stage=slot.stage, index=slot.index, s=slot.s,
                             r=float(coarse.float().mean().item()),
                             patches=int(counts.view(torch.int32)[0].item())))
         return out
+
+
+def add_channel_maskers(params: dict, gplan, seed: int = 0) -> dict:
+    """Channel-masker MLP weights per block (`reference.py:189-223`): G from the
+    stage's plan entry, D = C_mid / G, hidden h = max(D // 16, 16); w1 [h, C_in]
+    ~ N(0, 1/C_in), w2 [2D, h] ~ N(0, 1/h).  Stored in ``params["blocks"]`` so the
+    oracle composer runs the same maskers."""
+    rng = np.random.default_rng(seed + 7919)
+    for bp in params["blocks"]:
+        blk = bp["block"]
+        g = int(gplan[bp["stage"] - 1])
+        d = blk.conv2.out_channels // g
+        h = max(d // 16, 16)
+        ci = blk.input_shape.channels
+        bp["ch_g"] = g
+        bp["ch_w1"] = rng.standard_normal((h, ci)) / np.sqrt(ci)
+        bp["ch_w2"] = rng.standard_normal((2 * d, h)) / np.sqrt(h)
+    return params
 
 
 def random_images(n: int, h: int = 224, w: int = 224, seed: int = 0, device="cuda") -> torch.Tensor:

@@ -27,17 +27,31 @@ def _net(arch, paradigm, plan="4-2-2-1", ratio=0.5):
     return net, img.cpu().numpy(), logits[:, :1000].double().cpu().numpy(), masks
 
 
-@pytest.mark.parametrize("arch,paradigm", [("resnet50", "spatial"), ("resnet101", "spatial"),
-                                           ("resnet50", "layer"), ("resnet50", "static")])
-def test_network_matches_oracle(arch, paradigm):
-    net, img, logits, masks = _net(arch, paradigm)
+@pytest.mark.parametrize("arch,paradigm,plan", [
+    ("resnet50", "spatial", "4-2-2-1"), ("resnet101", "spatial", "4-2-2-1"),
+    ("resnet50", "layer", "4-2-2-1"), ("resnet50", "static", "4-2-2-1"),
+    ("resnet50", "channel", "1-1-1-1"), ("resnet50", "channel", "2-2-2-2")])
+def test_network_matches_oracle(arch, paradigm, plan):
+    net, img, logits, masks = _net(arch, paradigm, plan)
     plan = tuple(net.plan)
     ref = O.network_forward(net.params, img, paradigm, plan, masks=masks or None, emulate_bf16=True)
     rel = np.linalg.norm(logits - ref) / np.linalg.norm(ref)
     assert rel < 2e-2, rel
-    if paradigm == "spatial":
+    if paradigm in ("spatial", "channel"):
         r = np.mean([m.mean() for m in masks])
         assert 0.3 < r < 0.7
+
+
+def test_channel_network_decisions_match_oracle_maskers():
+    """Channel network: every block's device masker decisions (with its
+    calibration bias) equal the oracle masker on the same block input."""
+    net, img, logits, masks = _net("resnet50", "channel", "2-2-2-2")
+    rec = []
+    O.network_forward(net.params, img, "channel", tuple(net.plan), biases=net.masker_biases(),
+                      emulate_bf16=True, record=rec)
+    agree = np.mean([np.mean(np.asarray(m.coarse).reshape(-1) == g.reshape(-1).astype(bool))
+                     for m, g in zip(rec, masks)])
+    assert agree > 0.99, agree
 
 
 def test_masker_conv3_fusion_matches_unfused():
