@@ -300,13 +300,18 @@ def conv_roofline(torch, net, images, pk, pk_kind):
     }
 
 
-def static_cudnn_ms(torch, batch, steps, warmup, flush):
-    """torchvision ResNet-101, channels_last bf16, CUDA graph: the library static baseline."""
+TV_MODELS = {"resnet50": "resnet50", "resnet101": "resnet101", "regnety-400mf": "regnet_y_400mf",
+             "regnety-800mf": "regnet_y_800mf", "regnety-1.6gf": "regnet_y_1_6gf"}
+
+
+def static_cudnn_ms(torch, batch, steps, warmup, flush, arch="resnet101"):
+    """torchvision static model of the same arch (RegNetY includes its SE blocks),
+    channels_last bf16, CUDA graph: the library (cuDNN) static baseline."""
     try:
         import torchvision
     except Exception:
         return None
-    m = torchvision.models.resnet101().cuda().eval().to(memory_format=torch.channels_last).bfloat16()
+    m = getattr(torchvision.models, TV_MODELS[arch])().cuda().eval().to(memory_format=torch.channels_last).bfloat16()
     x = torch.randn(batch, 3, 224, 224, device="cuda").bfloat16().to(memory_format=torch.channels_last)
     with torch.no_grad():
         g, _ = capture(torch, lambda: m(x), warmup)
@@ -469,7 +474,7 @@ def run_gpu(args):
         static_ms = s_tot / max(3, args.steps // 2)
         del sg, snet
         torch.cuda.empty_cache()
-        cud = static_cudnn_ms(torch, args.batch, max(3, args.steps // 2), 2, flush)
+        cud = static_cudnn_ms(torch, args.batch, max(3, args.steps // 2), 2, flush, args.arch)
         extra["static_inhouse_ms"] = round(static_ms, 3)
         extra["static_cudnn_ms"] = round(cud, 3) if cud else None
         extra["latency_reduction_vs_static_inhouse"] = round(1 - ms_step / static_ms, 4)

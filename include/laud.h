@@ -96,7 +96,7 @@ typedef struct laud_conv_args {
   int in_h, in_w, in_c, in_ld;
   int a_compact;
   int ksize, stride, pad;
-  const void* weight; /* packed [n_out][ksize*ksize][kpad(in_c)] bf16 */
+  const void* weight; /* packed [n_out][ksize*ksize][kpad(in_c) (+64 grouped)] bf16 */
   int n_out;
   const float* scale;
   const float* bias;
@@ -125,6 +125,12 @@ typedef struct laud_conv_args {
   const float* mdot_w;
   float* mdot_out;
   int misplace_first;
+  /* grouped convolution (RegNet conv2): groups > 1 with in_c / groups and
+   * n_out / groups channels per group (in_c / groups a multiple of 8); the
+   * weight is the dense block-diagonal [n_out][taps][kpad(in_c) + 64] (zeros
+   * outside the group; the extra 64 zero columns let an output tile's K
+   * window run past the last group).  0 or 1 = dense. */
+  int groups;
 } laud_conv_args;
 
 int laud_conv(const laud_conv_args* a, void* stream);

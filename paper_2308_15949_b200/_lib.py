@@ -36,7 +36,7 @@ class ConvArgs(C.Structure):
         ("ymask_coarse", _vp), ("ymask_channel", _vp), ("sample_rows", C.c_int),
         ("chan_count", _vp), ("n_dyn", C.c_int), ("k_dyn", C.c_int), ("b_batched", C.c_int),
         ("col_index", _vp), ("col_index_ld", C.c_int), ("mdot_w", _vp), ("mdot_out", _vp),
-        ("misplace_first", C.c_int),
+        ("misplace_first", C.c_int), ("groups", C.c_int),
     ]
 
 

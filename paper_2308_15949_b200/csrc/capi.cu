@@ -253,7 +253,17 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   p.ksize = a->ksize;
   p.stride = a->stride;
   p.pad = a->pad;
-  p.kpad = round_up(a->in_c, 64);
+  p.groups = a->groups > 1 ? a->groups : 1;
+  if (p.groups > 1) {
+    if (a->in_c % p.groups || a->n_out % p.groups || (a->in_c / p.groups) % 8)
+      return fail(LAUD_ERR_SHAPE, "grouped conv: in_c (%d) / n_out (%d) must split into %d groups "
+                  "of multiples of 8 input channels", a->in_c, a->n_out, p.groups);
+    if (a->a_compact || a->sample_rows || a->chan_count)
+      return fail(LAUD_ERR_UNSUPPORTED, "grouped conv: no compact / per-sample modes");
+    p.gw_in = a->in_c / p.groups;
+    p.gw_out = a->n_out / p.groups;
+  }
+  p.kpad = round_up(a->in_c, 64) + (p.groups > 1 ? 64 : 0);
   p.num_kb = a->ksize * a->ksize * p.kpad / 64;
   p.n_out = a->n_out;
   p.scale = a->scale;
@@ -286,7 +296,8 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
     return e ? atoi(e) : 0;
   }();
   p.dbg = dbg_env;
-  const int bn = pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
+  // grouped: narrow tiles keep the block-diagonal K window short
+  const int bn = p.groups > 1 ? 64 : pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   CUtensorMap m;
   const int kw = a->ksize * a->ksize * p.kpad;
   int rc = tensor_map_2d(a->weight, a->n_out, kw, kw, bn, &m, a->b_batched ? a->batch : 0);
@@ -611,10 +622,9 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!a || !a->x || !a->out || !a->w1 || !a->w2 || !a->w3)
     return fail(LAUD_ERR_ARG, "null pointer in block args");
-  if (a->groups != 1)
-    return fail(LAUD_ERR_UNSUPPORTED, a->paradigm == LAUD_PARADIGM_CHANNEL
-                                          ? "sparse channel execution requires groups == 1"
-                                          : "grouped conv2 not supported yet");
+  if (a->groups < 1) return fail(LAUD_ERR_ARG, "groups must be >= 1");
+  if (a->groups != 1 && a->paradigm == LAUD_PARADIGM_CHANNEL)  // reference.py:405-406
+    return fail(LAUD_ERR_UNSUPPORTED, "sparse channel execution requires groups == 1");
   if (a->stride != 1 && a->stride != 2) return fail(LAUD_ERR_ARG, "stride must be 1 or 2");
   if (a->stride > 1 && !a->has_down)
     return fail(LAUD_ERR_SHAPE, "a strided block needs a downsample path");
@@ -790,6 +800,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c2.pad = 1;
   c2.weight = a->w2;
   c2.n_out = a->c_mid;
+  c2.groups = a->groups;
   c2.scale = a->s2;
   c2.bias = a->b2;
   c2.relu = a->relu2;
@@ -800,6 +811,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
 
   // ---------------------------------------------------------------- conv3 + scatter-add
   laud_conv_args c3 = c2;
+  c3.groups = 1;
   c3.act = a->h2;
   c3.in_h = ho;
   c3.in_w = wo;

@@ -144,6 +144,7 @@ __device__ __forceinline__ bool map_row_raw(const ConvParams& p, int m, int nval
 // Per-tile schedule shared by every warp role (all roles skip the same tiles).
 struct TileInfo {
   int m0, n0, sample, kpt, num_kb, kc;
+  int c_lo;  // first input channel of the tile's K window (grouped convs)
   bool skip;
 };
 template <int BN>
@@ -155,6 +156,13 @@ __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int t, int n_
   ti.kc = p.chan_count ? __ldg(p.chan_count + ti.sample) : 0;
   ti.skip = p.chan_count && p.n_dyn && ti.n0 >= ti.kc;
   ti.kpt = (p.chan_count && p.k_dyn) ? (ti.kc + BK - 1) / BK : p.kpad / BK;
+  ti.c_lo = 0;
+  if (p.groups > 1) {  // the input channels of the groups this N tile touches
+    const int g0 = ti.n0 / p.gw_out;
+    const int g1 = min(p.groups, (min(ti.n0 + BN, p.n_out) + p.gw_out - 1) / p.gw_out);
+    ti.c_lo = g0 * p.gw_in;
+    ti.kpt = ((g1 - g0) * p.gw_in + BK - 1) / BK;
+  }
   ti.num_kb = p.ksize * p.ksize * ti.kpt;
   return ti;
 }
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mbar_arrive(&full[stage]);
             } else {
               mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES);
-              tma_load_2d(sA, &tmap_a, &full[stage], kb * BK, row0);
+              tma_load_2d(sA, &tmap_a, &full[stage], ti.c_lo + kb * BK, row0);
             }
           }
         }
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (trc && tid == 0 && it < 4096) trc[TRACE_A + it] = global_ns();
           const int tap = kb / ti.kpt;
-          const int c0 = (kb - tap * ti.kpt) * BK;
+          const int c0 = ti.c_lo + (kb - tap * ti.kpt) * BK;
           const int ky = tap / p.ksize;
           const int kx = tap - ky * p.ksize;
           int row = p.a_rows;  // out of bounds -> zero fill
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t phase = (it / STAGES) & 1;
         mbar_wait(&empty[stage], phase ^ 1);
         const int tap = kb / ti.kpt;
-        const int ch = (kb - tap * ti.kpt) * BK + chunk * 8;
+        const int ch = ti.c_lo + (kb - tap * ti.kpt) * BK + chunk * 8;
         const int ky = tap / p.ksize;
         const int kx = tap - ky * p.ksize;
         const bool chv = ch < p.in_c;
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           mbar_arrive_expect_tx(&full[stage], L::B_STAGE_BYTES);
           const int tap = kb / ti.kpt;
-          const int kcoord = tap * p.kpad + (kb - tap * ti.kpt) * BK;  // packed per-tap stride kpad
+          const int kcoord = tap * p.kpad + ti.c_lo + (kb - tap * ti.kpt) * BK;  // per-tap stride kpad
           const uint32_t dst = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
           if (p.b_batched)
             tma_load_3d(dst, &tmap_b, &full[stage], kcoord, ti.n0, ti.sample);

@@ -37,7 +37,9 @@ struct ConvParams {
   int a_tile;            // 1: the 128 A rows of a tile are contiguous: one 2D TMA box
   int a_rows;            // rows of the A tensor map (also the out-of-bounds marker)
   int ksize, stride, pad;
-  int kpad;              // in_c rounded up to 64
+  int kpad;              // in_c rounded up to 64 (+64 for grouped convs)
+  int groups;            // > 1: block-diagonal weights; per N tile a K window of its groups
+  int gw_in, gw_out;     // channels per group (input, output)
   int num_kb;            // ksize*ksize*kpad/64
   // ---- output
   int n_out;             // output channels (multiple of 8)

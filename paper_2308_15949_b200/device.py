@@ -66,11 +66,24 @@ def from_device_nhwc(t: torch.Tensor, c: int) -> np.ndarray:
     return t[..., :c].permute(0, 3, 1, 2).double().cpu().numpy()
 
 
-def pack_weight(w, c_in_pad: int, device="cuda") -> torch.Tensor:
-    """[c_out, c_in, k, k] (numpy or torch) -> [c_out, k*k, kpad(c_in_pad)] bf16 on device."""
+def pack_weight(w, c_in_pad: int, device="cuda", groups: int = 1) -> torch.Tensor:
+    """[c_out, c_in / groups, k, k] (numpy or torch) -> [c_out, k*k, kpad(c_in_pad)] bf16 on device.
+
+    Grouped weights are expanded block-diagonally (zeros outside the group)
+    into kpad(c_in_pad) + 64 columns, the layout the engine's per-tile K
+    windows read (include/laud.h, laud_conv_args.groups).
+    """
     wt = torch.as_tensor(np.asarray(w) if isinstance(w, np.ndarray) else w, dtype=torch.float32)
+    co, cig, kh, kw = wt.shape
+    if groups > 1:
+        ci = cig * groups
+        dense = torch.zeros((co, ci, kh, kw), dtype=torch.float32)
+        gw_out = co // groups
+        for g in range(groups):
+            dense[g * gw_out:(g + 1) * gw_out, g * cig:(g + 1) * cig] = wt[g * gw_out:(g + 1) * gw_out]
+        wt = dense
     co, ci, kh, kw = wt.shape
-    out = torch.zeros((pad8(co), kh * kw, kpad(c_in_pad)), dtype=torch.float32)
+    out = torch.zeros((pad8(co), kh * kw, kpad(c_in_pad) + (64 if groups > 1 else 0)), dtype=torch.float32)
     out[:co, :, :ci] = wt.permute(0, 2, 3, 1).reshape(co, kh * kw, ci)
     return out.to(device=device, dtype=torch.bfloat16).contiguous()
 
@@ -158,8 +171,6 @@ class DeviceBlock:
         self.c_in, self.c_mid, self.c_out = (block.conv1.in_channels, block.conv1.out_channels,
                                              block.conv3.out_channels)
         self.cin_p, self.cmid_p, self.cout_p = pad8(self.c_in), pad8(self.c_mid), pad8(self.c_out)
-        if block.conv2.groups != 1:
-            raise DeviceError("grouped conv2 is not supported by the CUDA path yet")
         ep = epilogue or Epilogue()
         if fold_scale:
             # inference BN folding: per-output-channel scale goes into the weights
@@ -168,7 +179,10 @@ class DeviceBlock:
             ep = Epilogue(None, ep.b1, ep.relu1, None, ep.b2, ep.relu2, None, ep.b3, None, ep.bd,
                           ep.relu_out)
         self.w1 = pack_weight(w1, self.cin_p, device)
-        self.w2 = pack_weight(w2, self.cmid_p, device)
+        self.groups = block.conv2.groups
+        if self.groups > 1 and self.cmid_p != self.c_mid:
+            raise DeviceError("grouped conv2 needs a mid width that is a multiple of 8")
+        self.w2 = pack_weight(w2, self.cmid_p, device, groups=self.groups)
         self.w3 = pack_weight(w3, self.cmid_p, device)
         self.wd = pack_weight(w_down, self.cin_p, device) if w_down is not None else None
         self.ep = ep

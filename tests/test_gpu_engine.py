@@ -97,3 +97,22 @@ def test_compaction_matches_argwhere():
         plan = R.build_gather_plan(coarse)
         assert plan.indices == tuple(tuple(int(v) for v in r) for r in np.argwhere(coarse))
         assert plan.patch_count == int(coarse.sum())
+
+
+@pytest.mark.parametrize("c,groups,stride,n,h", [
+    (48, 2, 1, 2, 8), (120, 5, 2, 2, 14), (336, 14, 1, 1, 14), (888, 37, 2, 1, 14), (64, 8, 1, 2, 9)])
+def test_grouped_conv_matches_torch(c, groups, stride, n, h):
+    """Block-diagonal grouped 3x3 conv (RegNet conv2): per-tile K windows."""
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(c + groups)
+    x = torch.randn(n, h, h, c, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(c, c // groups, 3, 3, generator=g) / np.sqrt(9 * c // groups)).to(torch.bfloat16).float()
+    wp = D.pack_weight(w, c, groups=groups)
+    ho = (h + 2 - 3) // stride + 1
+    out = torch.empty(n, ho, ho, c, dtype=torch.bfloat16, device="cuda")
+    CH.conv(act=x, in_hw=(h, h), in_c=c, in_ld=c, weight=wp, n_out=c, out=out, out_ld=c,
+            out_hw=(ho, ho), batch=n, ksize=3, stride=stride, pad=1, groups=groups)
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.cuda(), stride=stride, padding=1,
+                                     groups=groups).permute(0, 2, 3, 1)
+    err = (out.float() - ref).norm() / ref.norm()
+    assert err < 6e-3, float(err)

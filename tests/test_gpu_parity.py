@@ -229,3 +229,39 @@ def test_channel_block_large(r):
     assert _rel(y, emu) <= BF16_TOL
     yd = R.block_forward_dense_masked(x, bw, blk, cfg, m)
     assert _rel(y, yd) <= BF16_TOL
+
+
+@pytest.mark.parametrize("stage,index,paradigm", [(1, 0, "spatial"), (2, 1, "spatial"), (3, 0, "spatial"),
+                                                   (3, 1, "spatial"), (4, 1, "spatial"), (3, 1, "layer"),
+                                                   (2, 0, "static")])
+def test_regnet_grouped_block_matches_oracle(stage, index, paradigm):
+    """RegNetY-1.6GF blocks (grouped conv2, group width 24) through the drop-in."""
+    R = _R()
+    from paper_2308_15949_b200.zoo import build_network
+    net = build_network("regnety-1.6gf")
+    block = [b.block for b in net.blocks if b.stage == stage and b.index == index][0]
+    s = (4, 4, 2, 1)[stage - 1]
+    rng = np.random.default_rng(stage * 10 + index)
+    bw = R.make_block_weights(block, rng)
+    n = 2
+    ci = block.input_shape
+    x = rng.standard_normal((n, ci.channels, ci.height, ci.width))
+    o = block.output_shape
+    if paradigm == "spatial":
+        coarse = rng.random((n, o.height // s, o.width // s)) < 0.5
+        cfg = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=s)
+        m, om = R.SpatialMask(coarse, R.upsample_coarse(coarse, s), s), O.SpatialMask(coarse, O.upsample_coarse(coarse, s), s)
+    elif paradigm == "layer":
+        d = np.array([True, False])
+        cfg = DynamicConfig(Paradigm.LAYER)
+        m, om = R.LayerMask(d), O.LayerMask(d)
+    else:
+        cfg = DynamicConfig(Paradigm.STATIC)
+        m = om = None
+    y = R.block_forward_sparse(x, bw, block, cfg, m)
+    obw = O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
+    emu = O.block_forward_sparse(x, obw, block, cfg, om, emulate_bf16=True)
+    ref = O.block_forward_sparse(x, obw, block, cfg, om)
+    assert block.conv2.groups > 1
+    assert _rel(y, emu) <= BF16_TOL, _rel(y, emu)
+    assert _rel(y, ref) <= 1e-2
