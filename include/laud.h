@@ -131,6 +131,9 @@ typedef struct laud_conv_args {
    * outside the group; the extra 64 zero columns let an output tile's K
    * window run past the last group).  0 or 1 = dense. */
   int groups;
+  /* fp32 mode: act / weight / resid / out are fp32 (weight in the same packed
+   * layout), computed with fp32 FFMA (the 1e-5 numerics path). */
+  int fp32;
 } laud_conv_args;
 
 int laud_conv(const laud_conv_args* a, void* stream);
@@ -201,6 +204,9 @@ typedef struct laud_block_args {
   /* EXT: per-decision bias added to the channel masker's logit gap l0 - l1
    * (nullable; calibrates the kept ratio like a trained FLOPs loss would). */
   const float* ch_bias;
+  /* fp32 mode: x / out / h1 / h2 fp32 and fp32 weights (same packed layouts);
+   * every conv on the fp32 FFMA engine (1e-5 numerics path). */
+  int fp32;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

@@ -36,7 +36,7 @@ class ConvArgs(C.Structure):
         ("ymask_coarse", _vp), ("ymask_channel", _vp), ("sample_rows", C.c_int),
         ("chan_count", _vp), ("n_dyn", C.c_int), ("k_dyn", C.c_int), ("b_batched", C.c_int),
         ("col_index", _vp), ("col_index_ld", C.c_int), ("mdot_w", _vp), ("mdot_out", _vp),
-        ("misplace_first", C.c_int), ("groups", C.c_int),
+        ("misplace_first", C.c_int), ("groups", C.c_int), ("fp32", C.c_int),
     ]
 
 
@@ -55,7 +55,7 @@ class BlockArgs(C.Structure):
         ("misplace_first", C.c_int), ("ch_w1", _vp), ("ch_w2", _vp), ("ch_hidden", C.c_int),
         ("ch_d", C.c_int), ("ch_groups", C.c_int), ("given_chmask", _vp), ("ch_coarse", _vp),
         ("ch_expanded", _vp), ("ch_sel", _vp), ("ch_count", _vp), ("ch_dvals", _vp),
-        ("wpack", _vp), ("prev_coarse", _vp), ("dn", _vp), ("next_wdiff", _vp), ("ch_bias", _vp),
+        ("wpack", _vp), ("prev_coarse", _vp), ("dn", _vp), ("next_wdiff", _vp), ("ch_bias", _vp), ("fp32", C.c_int),
     ]
 
 

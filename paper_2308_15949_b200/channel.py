@@ -25,7 +25,7 @@ def conv(*, act, in_hw, in_c, in_ld, weight, n_out, out, out_ld, out_hw, batch, 
          pad=0, row_mode=ROWS_DENSE, rows_max=None, lst=None, count=None, patch=(1, 1),
          cells=(1, 1), a_compact=0, scale=None, bias=None, relu=0, out_mode=OUT_PIXEL, out_f32=0,
          resid=None, resid_ld=0, relu_inactive=None, ymask_coarse=None, ymask_channel=None,
-         misplace_first=0, groups=1, stream=None):
+         misplace_first=0, groups=1, fp32=0, stream=None):
     """One call of the implicit-GEMM engine (``laud_conv``)."""
     a = _lib.ConvArgs(
         row_mode=row_mode, list=D.ptr(lst), count=D.ptr(count),
@@ -37,7 +37,7 @@ def conv(*, act, in_hw, in_c, in_ld, weight, n_out, out, out_ld, out_hw, batch, 
         out_mode=out_mode, out=D.ptr(out), out_ld=out_ld, out_f32=out_f32, resid=D.ptr(resid),
         resid_ld=resid_ld, relu_inactive_coarse=D.ptr(relu_inactive),
         ymask_coarse=D.ptr(ymask_coarse), ymask_channel=D.ptr(ymask_channel),
-        misplace_first=misplace_first, groups=groups)
+        misplace_first=misplace_first, groups=groups, fp32=fp32)
     _lib.check(_lib.lib().laud_conv(C.byref(a), D.stream_handle(stream)))
 
 
@@ -48,27 +48,29 @@ def dense_block(db: D.DeviceBlock, x: torch.Tensor, ymask: Optional[torch.Tensor
     ho, wo = db.out_hw(h, w)
     blk = db.block
     v = db.vec
-    out = torch.empty((n, ho, wo, db.cout_p), dtype=torch.bfloat16, device=x.device)
-    h1 = torch.empty((n, h, w, db.cmid_p), dtype=torch.bfloat16, device=x.device)
-    h2 = torch.empty((n * ho * wo, db.cmid_p), dtype=torch.bfloat16, device=x.device)
+    dt = getattr(db, "dtype", torch.bfloat16)
+    f32 = int(dt == torch.float32)
+    out = torch.empty((n, ho, wo, db.cout_p), dtype=dt, device=x.device)
+    h1 = torch.empty((n, h, w, db.cmid_p), dtype=dt, device=x.device)
+    h2 = torch.empty((n * ho * wo, db.cmid_p), dtype=dt, device=x.device)
     if blk.has_downsample:
         conv(act=x, in_hw=(h, w), in_c=db.cin_p, in_ld=db.cin_p, weight=db.wd, n_out=db.cout_p,
              out=out, out_ld=db.cout_p, out_hw=(ho, wo), batch=n, stride=blk.stride,
-             scale=v["sd"], bias=v["bd"], stream=stream)
+             scale=v["sd"], bias=v["bd"], fp32=f32, stream=stream)
     else:
         out.copy_(x)
     conv(act=x, in_hw=(h, w), in_c=db.cin_p, in_ld=db.cin_p, weight=db.w1, n_out=db.cmid_p,
          out=h1, out_ld=db.cmid_p, out_hw=(h, w), batch=n, scale=v["s1"], bias=v["b1"],
-         relu=int(db.ep.relu1), ymask_channel=chmask, stream=stream)
+         relu=int(db.ep.relu1), ymask_channel=chmask, fp32=f32, stream=stream)
     conv(act=h1, in_hw=(h, w), in_c=db.cmid_p, in_ld=db.cmid_p, weight=db.w2, n_out=db.cmid_p,
          out=h2, out_ld=db.cmid_p, out_hw=(ho, wo), batch=n, ksize=3, stride=blk.stride, pad=1,
          scale=v["s2"], bias=v["b2"], relu=int(db.ep.relu2), out_mode=OUT_ROW,
-         ymask_channel=chmask, groups=getattr(db, "groups", 1), stream=stream)
+         ymask_channel=chmask, groups=getattr(db, "groups", 1), fp32=f32, stream=stream)
     cells = (ho // patch[0], wo // patch[1])
     conv(act=h2, in_hw=(ho, wo), in_c=db.cmid_p, in_ld=db.cmid_p, weight=db.w3, n_out=db.cout_p,
          out=out, out_ld=db.cout_p, out_hw=(ho, wo), batch=n, a_compact=1, scale=v["s3"],
          bias=v["b3"], relu=int(db.ep.relu_out), resid=out, resid_ld=db.cout_p, patch=patch,
-         cells=cells, ymask_coarse=ymask, stream=stream)
+         cells=cells, ymask_coarse=ymask, fp32=f32, stream=stream)
     return out
 
 
@@ -138,6 +140,6 @@ def channel_block_sparse(x, bw, block, mask):
     db = R.device_block(bw, block)
     mm = np.zeros((n, db.cmid_p), np.uint8)
     mm[:, : m.shape[1]] = m
-    xd = D.to_device_nhwc(x)
+    xd = D.to_device_nhwc(x, dtype=db.dtype)
     y, *_ = db.forward(xd, "channel", chmask=torch.from_numpy(mm.reshape(-1)).cuda())
     return D.from_device_nhwc(y, block.output_shape.channels)

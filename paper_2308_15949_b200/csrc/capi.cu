@@ -21,6 +21,7 @@
 namespace laud {
 cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn,
                              const ConvParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t stream);
 size_t scan_state_bytes(int total);
 int masker_splits(int win, int c, int* chunks_per_split);
 cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c,
@@ -296,6 +297,15 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
     return e ? atoi(e) : 0;
   }();
   p.dbg = dbg_env;
+  if (a->fp32) {  // fp32 mode: SIMT FFMA engine, same rows/epilogues (conv_f32.cu)
+    if (a->sample_rows || a->chan_count || a->b_batched || a->col_index || a->mdot_w)
+      return fail(LAUD_ERR_UNSUPPORTED, "fp32 mode: no per-sample / dynamic-width convs");
+    if ((reinterpret_cast<uintptr_t>(a->act) | reinterpret_cast<uintptr_t>(a->weight)) & 15)
+      return fail(LAUD_ERR_ARG, "fp32 mode: 16-byte aligned activations and weights");
+    p.weight_f32 = a->weight;
+    ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
+    return cuda_check(launch_conv_f32(p, st), "conv_f32 launch", 1);
+  }
   // grouped: narrow tiles keep the block-diagonal K window short
   const int bn = p.groups > 1 ? 64 : pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   CUtensorMap m;
@@ -492,7 +502,7 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
     const int cm = a->ch_d * a->ch_groups;
     if (cm > cmp) return fail(LAUD_ERR_GRANULARITY, "D*G exceeds the mid width");
     ProfScope ps(1, st);
-    if ((rc = cuda_check(launch_channel_masker(a->x, 0, a->x_ld, n, a->h_in * a->w_in, a->c_in,
+    if ((rc = cuda_check(launch_channel_masker(a->x, a->fp32, a->x_ld, n, a->h_in * a->w_in, a->c_in,
                                                a->ch_w1, a->ch_hidden, a->ch_w2, a->ch_d,
                                                a->ch_groups, cm, cmp, a->ch_coarse, a->ch_dvals,
                                                a->ch_expanded, a->ch_sel, a->ch_count, a->ch_bias,
@@ -504,6 +514,7 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
   if (a->has_down) {
     laud_conv_args d;
     memset(&d, 0, sizeof(d));
+    d.fp32 = a->fp32;
     d.row_mode = ROWS_DENSE;
     d.rows_max = n * ho * wo;
     d.batch = n;
@@ -525,10 +536,77 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
     d.out_ld = a->c_out;
     if ((rc = run_conv(&d, st))) return rc;
   } else if (a->out != a->x) {
-    if ((rc = cuda_check(cudaMemcpyAsync(a->out, a->x, (size_t)n * ho * wo * a->c_out * 2,
+    if ((rc = cuda_check(cudaMemcpyAsync(a->out, a->x, (size_t)n * ho * wo * a->c_out * (a->fp32 ? 4 : 2),
                                          cudaMemcpyDeviceToDevice, st),
                          "skip copy", 0)))
       return rc;
+  }
+  if (a->fp32) {
+    // fp32 mode: the dense-masked schedule of the same algebra (reference.py:336-339):
+    // h1 and h2 are zero on the dropped channels, so conv3 sums only the kept ones.
+    laud_conv_args c1;
+    memset(&c1, 0, sizeof(c1));
+    c1.fp32 = 1;
+    c1.row_mode = ROWS_DENSE;
+    c1.rows_max = n * a->h_in * a->w_in;
+    c1.batch = n;
+    c1.out_h = a->h_in;
+    c1.out_w = a->w_in;
+    c1.patch_h = c1.patch_w = c1.cells_h = c1.cells_w = 1;
+    c1.act = a->x;
+    c1.in_h = a->h_in;
+    c1.in_w = a->w_in;
+    c1.in_c = a->c_in;
+    c1.in_ld = a->x_ld;
+    c1.ksize = 1;
+    c1.stride = 1;
+    c1.weight = a->w1;
+    c1.n_out = cmp;
+    c1.scale = a->s1;
+    c1.bias = a->b1;
+    c1.relu = a->relu1;
+    c1.ymask_channel = a->ch_expanded;
+    c1.out_mode = OUT_PIXEL;
+    c1.out = a->h1;
+    c1.out_ld = cmp;
+    if ((rc = run_conv(&c1, st))) return rc;
+    laud_conv_args c2 = c1;
+    c2.rows_max = n * ho * wo;
+    c2.out_h = ho;
+    c2.out_w = wo;
+    c2.act = a->h1;
+    c2.in_c = cmp;
+    c2.in_ld = cmp;
+    c2.ksize = 3;
+    c2.stride = a->stride;
+    c2.pad = 1;
+    c2.weight = a->w2;
+    c2.scale = a->s2;
+    c2.bias = a->b2;
+    c2.relu = a->relu2;
+    c2.out_mode = OUT_ROW;
+    c2.out = a->h2;
+    if ((rc = run_conv(&c2, st))) return rc;
+    laud_conv_args c3 = c2;
+    c3.act = a->h2;
+    c3.in_h = ho;
+    c3.in_w = wo;
+    c3.a_compact = 1;
+    c3.ksize = 1;
+    c3.stride = 1;
+    c3.pad = 0;
+    c3.weight = a->w3;
+    c3.n_out = a->c_out;
+    c3.ymask_channel = nullptr;
+    c3.scale = a->s3;
+    c3.bias = a->b3;
+    c3.relu = a->relu_out;
+    c3.out_mode = OUT_PIXEL;
+    c3.out = a->out;
+    c3.out_ld = a->c_out;
+    c3.resid = a->out;
+    c3.resid_ld = a->c_out;
+    return run_conv(&c3, st);
   }
   // per-sample packed weights
   const int k1 = round64(a->c_in), k2 = round64(cmp);
@@ -550,6 +628,7 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
   const int sr2 = (ho * wo + 127) / 128 * 128;
   laud_conv_args c1;
   memset(&c1, 0, sizeof(c1));
+  c1.fp32 = a->fp32;
   c1.row_mode = ROWS_DENSE;
   c1.sample_rows = sr1;
   c1.rows_max = n * sr1;
@@ -666,14 +745,14 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
       coarse = a->coarse_out;
       if (a->dn) {  // masker-conv3 fusion with the previous block (same grid and S)
         ProfScope ps(1, st);
-        rc = cuda_check(launch_spatial_masker(a->x, 0, a->x_ld, n, a->h_in, a->w_in, a->c_in,
+        rc = cuda_check(launch_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in,
                                               a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s,
                                               a->stride, a->masker_wdiff, a->masker_bias,
                                               a->coarse_out, a->cell_list, a->cell_count,
                                               a->partial, a->scan, st, a->prev_coarse, a->dn),
                         "spatial masker (fused)", 2);
       } else {
-        rc = laud_spatial_masker(a->x, 0, a->x_ld, n, a->h_in, a->w_in, a->c_in,
+        rc = laud_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in,
                                  a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
                                  a->masker_wdiff, a->masker_bias, a->coarse_out, a->cell_list,
                                  a->cell_count, a->partial, a->scan, stream);
@@ -693,6 +772,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   if (a->has_down) {
     laud_conv_args d;
     memset(&d, 0, sizeof(d));
+    d.fp32 = a->fp32;
     d.row_mode = ROWS_DENSE;
     d.rows_max = n * ho * wo;
     d.batch = n;
@@ -727,7 +807,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     }
     if ((rc = run_conv(&d, st))) return rc;
   } else if (a->out != a->x) {
-    if ((rc = cuda_check(cudaMemcpyAsync(a->out, a->x, (size_t)n * ho * wo * a->c_out * 2,
+    if ((rc = cuda_check(cudaMemcpyAsync(a->out, a->x, (size_t)n * ho * wo * a->c_out * (a->fp32 ? 4 : 2),
                                          cudaMemcpyDeviceToDevice, st),
                          "skip copy", 0)))
       return rc;
@@ -736,6 +816,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   // ---------------------------------------------------------------- conv1
   laud_conv_args c1;
   memset(&c1, 0, sizeof(c1));
+  c1.fp32 = a->fp32;
   c1.batch = n;
   c1.out_h = a->h_in;
   c1.out_w = a->w_in;
@@ -779,6 +860,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   // ---------------------------------------------------------------- conv2 (3x3 over patches)
   laud_conv_args c2;
   memset(&c2, 0, sizeof(c2));
+  c2.fp32 = a->fp32;
   c2.row_mode = pm;
   c2.list = cells;
   c2.count = cells_n;

@@ -76,6 +76,7 @@ struct ConvParams {
   // ---- debug timeline (laud_debug_set_trace): CTA 0 records %globaltimer at
   //      pipeline events; nullptr (always, outside tools/) = off
   unsigned long long* trace;
+  const void* weight_f32;  // fp32 mode: packed fp32 weights (conv_f32.cu)
   int dbg;  // debug ablations (LAUD_DBG, tools only): 1 no math, 2 no stores, 4 no TMEM loads,
            // 8 no A loads, 16 no B loads
 };

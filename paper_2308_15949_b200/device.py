@@ -66,7 +66,7 @@ def from_device_nhwc(t: torch.Tensor, c: int) -> np.ndarray:
     return t[..., :c].permute(0, 3, 1, 2).double().cpu().numpy()
 
 
-def pack_weight(w, c_in_pad: int, device="cuda", groups: int = 1) -> torch.Tensor:
+def pack_weight(w, c_in_pad: int, device="cuda", groups: int = 1, dtype=torch.bfloat16) -> torch.Tensor:
     """[c_out, c_in / groups, k, k] (numpy or torch) -> [c_out, k*k, kpad(c_in_pad)] bf16 on device.
 
     Grouped weights are expanded block-diagonally (zeros outside the group)
@@ -85,7 +85,7 @@ def pack_weight(w, c_in_pad: int, device="cuda", groups: int = 1) -> torch.Tenso
     co, ci, kh, kw = wt.shape
     out = torch.zeros((pad8(co), kh * kw, kpad(c_in_pad) + (64 if groups > 1 else 0)), dtype=torch.float32)
     out[:co, :, :ci] = wt.permute(0, 2, 3, 1).reshape(co, kh * kw, ci)
-    return out.to(device=device, dtype=torch.bfloat16).contiguous()
+    return out.to(device=device, dtype=dtype).contiguous()
 
 
 def fvec(v, n: int, fill: float, device="cuda") -> torch.Tensor:
@@ -165,8 +165,12 @@ class DeviceBlock:
     """Packed weights + epilogue vectors of one bottleneck block."""
 
     def __init__(self, block: BlockSpec, w1, w2, w3, w_down=None, epilogue: Optional[Epilogue] = None,
-                 masker_w=None, masker_bias: float = 0.0, device="cuda", fold_scale: bool = False):
+                 masker_w=None, masker_bias: float = 0.0, device="cuda", fold_scale: bool = False,
+                 dtype=torch.bfloat16):
         require_cuda()
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise DeviceError("compute dtype must be bf16 (tcgen05) or fp32 (FFMA numerics mode)")
+        self.dtype = dtype
         self.block = block
         self.c_in, self.c_mid, self.c_out = (block.conv1.in_channels, block.conv1.out_channels,
                                              block.conv3.out_channels)
@@ -178,13 +182,13 @@ class DeviceBlock:
             w_down = _fold(w_down, ep.sd) if w_down is not None else None
             ep = Epilogue(None, ep.b1, ep.relu1, None, ep.b2, ep.relu2, None, ep.b3, None, ep.bd,
                           ep.relu_out)
-        self.w1 = pack_weight(w1, self.cin_p, device)
+        self.w1 = pack_weight(w1, self.cin_p, device, dtype=dtype)
         self.groups = block.conv2.groups
         if self.groups > 1 and self.cmid_p != self.c_mid:
             raise DeviceError("grouped conv2 needs a mid width that is a multiple of 8")
-        self.w2 = pack_weight(w2, self.cmid_p, device, groups=self.groups)
-        self.w3 = pack_weight(w3, self.cmid_p, device)
-        self.wd = pack_weight(w_down, self.cin_p, device) if w_down is not None else None
+        self.w2 = pack_weight(w2, self.cmid_p, device, groups=self.groups, dtype=dtype)
+        self.w3 = pack_weight(w3, self.cmid_p, device, dtype=dtype)
+        self.wd = pack_weight(w_down, self.cin_p, device, dtype=dtype) if w_down is not None else None
         self.ep = ep
         self.vec = {}
         for k, n, fill in (("s1", self.c_mid, 1.0), ("b1", self.c_mid, 0.0), ("s2", self.c_mid, 1.0),
@@ -257,12 +261,13 @@ class DeviceBlock:
                 next_wdiff: Optional[torch.Tensor] = None):
         """x: (N, H, W, cin_p) bf16 CUDA.  Returns (out, coarse, cell_list, cell_count)."""
         n, h, w, cl = x.shape
-        if cl != self.cin_p or x.dtype != torch.bfloat16 or not x.is_contiguous():
-            raise DeviceError("x must be contiguous NHWC bf16 with pad8(C_in) channels")
+        if cl != self.cin_p or x.dtype != self.dtype or not x.is_contiguous():
+            raise DeviceError(f"x must be contiguous NHWC {self.dtype} with pad8(C_in) channels")
+        esz = 4 if self.dtype == torch.float32 else 2
         ho, wo = self.out_hw(h, w)
         blk = self.block
         if out is None:
-            out = torch.empty((n, ho, wo, self.cout_p), dtype=torch.bfloat16, device=x.device)
+            out = torch.empty((n, ho, wo, self.cout_p), dtype=self.dtype, device=x.device)
         ws = ws or workspace(x.device)
         if paradigm == "spatial":
             cells = n * (ho // s) * (wo // s) if s >= 1 and ho % s == 0 and wo % s == 0 else n
@@ -279,13 +284,10 @@ class DeviceBlock:
         cell_list = ws.get("cell_list", cells * i32)
         counts = ws.get("counts", 16)
         pix_list = ws.get("pix_list", pix * i32)
-        h1 = ws.get("h1", pix * self.cmid_p * 2)
-        h2 = ws.get("h2", n * ho * wo * self.cmid_p * 2)
+        h1 = ws.get("h1", pix * self.cmid_p * esz)
+        h2 = ws.get("h2", n * ho * wo * self.cmid_p * esz)
         lib = _lib.lib()
         partial_n = 1
-        if paradigm == "channel":
-            h2 = ws.get("h2", n * ho * wo * self.cmid_p * 2)
-            h1 = ws.get("h1", pix * self.cmid_p * 2)
         if coarse is None and paradigm in ("spatial", "layer"):
             if self.wdiff is None:
                 raise DeviceError("no mask given and no masker weights set")
@@ -306,7 +308,8 @@ class DeviceBlock:
             given_coarse=ptr(coarse), coarse_out=ptr(coarse_buf), cell_list=ptr(cell_list),
             cell_count=C.c_void_p(counts.data_ptr()), pix_list=ptr(pix_list),
             pix_count=C.c_void_p(counts.data_ptr() + 4), h1=ptr(h1), h2=ptr(h2),
-            partial=ptr(partial), scan=ptr(scan), misplace_first=int(misplace_first))
+            partial=ptr(partial), scan=ptr(scan), misplace_first=int(misplace_first),
+            fp32=int(self.dtype == torch.float32))
         if paradigm == "channel":
             self._channel_args(a, n, ws, chmask)
         if dn is not None and paradigm == "spatial":

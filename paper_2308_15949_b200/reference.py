@@ -279,12 +279,29 @@ class _Key:  # BlockWeights is frozen+eq; key device copies on identity
     pass
 
 
+_PRECISION = {"dtype": torch.bfloat16}
+
+
+def set_precision(name: str) -> None:
+    """EXT: compute precision of the block executors — "bf16" (default: bf16
+    storage, fp32 tcgen05 accumulation; 1e-3 gate) or "fp32" (fp32 storage and
+    FFMA; the north star's 1e-5 gate).  Maskers always decide in fp32."""
+    if name not in ("bf16", "fp32"):
+        raise ValueError(f"precision must be 'bf16' or 'fp32', got {name!r}")
+    _PRECISION["dtype"] = torch.float32 if name == "fp32" else torch.bfloat16
+
+
+def get_precision() -> str:
+    return "fp32" if _PRECISION["dtype"] == torch.float32 else "bf16"
+
+
 def device_block(bw: BlockWeights, block: BlockSpec) -> D.DeviceBlock:
-    """Packed device copy of ``bw`` (cached per BlockWeights object)."""
+    """Packed device copy of ``bw`` (cached per BlockWeights object and precision)."""
+    dt = _PRECISION["dtype"]
     cache = bw.__dict__.get("_laud_dev")
-    if cache is not None and cache[0] == block:
+    if cache is not None and cache[0] == block and cache[1].dtype == dt:
         return cache[1]
-    db = D.DeviceBlock(block, bw.w1, bw.w2, bw.w3, bw.w_down)
+    db = D.DeviceBlock(block, bw.w1, bw.w2, bw.w3, bw.w_down, dtype=dt)
     object.__setattr__(bw, "_laud_dev", (block, db))
     return db
 
@@ -337,7 +354,7 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
         from . import channel as CH
         return CH.channel_block_sparse(x, bw, block, mask)
     db = device_block(bw, block)
-    xd = D.to_device_nhwc(x)
+    xd = D.to_device_nhwc(x, dtype=db.dtype)
     out = block.output_shape
     if p is Paradigm.SPATIAL:
         _check_spatial_mask(mask, block, n)
@@ -367,7 +384,7 @@ def block_forward_dense_masked(x, bw: BlockWeights, block: BlockSpec, cfg: Dynam
     n = x.shape[0]
     p = cfg.paradigm
     db = device_block(bw, block)
-    xd = D.to_device_nhwc(x)
+    xd = D.to_device_nhwc(x, dtype=db.dtype)
     out = block.output_shape
     ymask = None
     chmask = None

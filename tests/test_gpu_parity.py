@@ -265,3 +265,60 @@ def test_regnet_grouped_block_matches_oracle(stage, index, paradigm):
     assert block.conv2.groups > 1
     assert _rel(y, emu) <= BF16_TOL, _rel(y, emu)
     assert _rel(y, ref) <= 1e-2
+
+
+FP32_TOL = 1e-5
+
+
+@pytest.fixture
+def fp32_mode():
+    R = _R()
+    R.set_precision("fp32")
+    yield R
+    R.set_precision("bf16")
+
+
+@pytest.mark.parametrize("m", _cases(), ids=lambda m: m["key"])
+def test_fp32_mode_block_matches_reference(m, fp32_mode):
+    """fp32 mode (FFMA engine): <= 1e-5 norm-relative vs the reference's fp64 output."""
+    R = fp32_mode
+    case = O.EquivalenceCase(Paradigm(m["paradigm"]), m["channels"], m["height"], m["width"],
+                             m["granularity"], m["seed"])
+    block, mask, bw, x, cfg = O.case_inputs(case)
+    if case.paradigm is Paradigm.SPATIAL:
+        rmask = R.SpatialMask(mask.coarse, mask.upsampled, mask.granularity)
+    elif case.paradigm is Paradigm.CHANNEL:
+        rmask = R.ChannelMask(mask.coarse, mask.expanded, mask.granularity)
+    else:
+        rmask = R.LayerMask(mask.decisions)
+    rbw = R.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
+    y = R.block_forward_sparse(x, rbw, block, cfg, rmask)
+    ref = np.load(G / "equivalence.npz")[m["key"] + "__sparse"]
+    assert _rel(y, ref) <= FP32_TOL, _rel(y, ref)
+    yd = R.block_forward_dense_masked(x, rbw, block, cfg, rmask)
+    assert _rel(yd, ref) <= FP32_TOL, _rel(yd, ref)
+
+
+def test_fp32_mode_config1_and_regnet(fp32_mode):
+    """BASELINE config 1 block and a grouped RegNetY block in fp32 mode vs fp64."""
+    R = fp32_mode
+    from paper_2308_15949_b200.zoo import build_network
+    a = np.load(G / "config1.npz")
+    block = [b.block for b in build_network("resnet50").blocks if b.stage == 3 and b.index == 1][0]
+    rng = np.random.default_rng(0)
+    bw = R.make_block_weights(block, rng)
+    x = rng.standard_normal((1, 1024, 14, 14))
+    mw = rng.standard_normal((2, 1024, 1, 1)) / np.sqrt(1024)
+    m = R.spatial_masker_forward(x, mw, 2)
+    cfg = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=2)
+    y = R.block_forward_sparse(x, bw, block, cfg, m)
+    assert _rel(y, a["y"]) <= FP32_TOL, _rel(y, a["y"])
+    rb = [b.block for b in build_network("regnety-1.6gf").blocks if b.stage == 3 and b.index == 0][0]
+    rng = np.random.default_rng(5)
+    rbw = R.make_block_weights(rb, rng)
+    xi = rng.standard_normal((2, rb.input_shape.channels, rb.input_shape.height, rb.input_shape.width))
+    coarse = rng.random((2, 7, 7)) < 0.5
+    om = O.SpatialMask(coarse, O.upsample_coarse(coarse, 2), 2)
+    yr = R.block_forward_sparse(xi, rbw, rb, cfg, R.SpatialMask(coarse, R.upsample_coarse(coarse, 2), 2))
+    ref = O.block_forward_sparse(xi, O.BlockWeights(rbw.w1, rbw.w2, rbw.w3, rbw.w_down), rb, cfg, om)
+    assert _rel(yr, ref) <= FP32_TOL, _rel(yr, ref)
