@@ -20,7 +20,7 @@
 
 namespace laud {
 cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn,
-                             const ConvParams& p, int num_sms, cudaStream_t stream);
+                             const ConvParams& p, int num_sms, cudaStream_t stream, int pair);
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t stream);
 size_t scan_state_bytes(int total);
 int masker_splits(int win, int c, int* chunks_per_split);
@@ -308,10 +308,8 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   }
   // grouped: narrow tiles keep the block-diagonal K window short
   const int bn = p.groups > 1 ? 64 : pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
-  CUtensorMap m;
   const int kw = a->ksize * a->ksize * p.kpad;
-  int rc = tensor_map_2d(a->weight, a->n_out, kw, kw, bn, &m, a->b_batched ? a->batch : 0);
-  if (rc) return rc;
+  int rc;
   // A operand: [a_rows][in_c] with row stride in_ld, gathered 4 rows at a time
   CUtensorMap ma;
   memset(&ma, 0, sizeof(ma));
@@ -341,6 +339,24 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
       if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, p.a_tile ? 128 : 1, &ma))) return rc;
     }
   }
+  // gathered (non-contiguous, non-compact) A rows: split across TMA gather4 and cp.async
+  static const int hybrid_env = [] {  // opt-in: measured slower on B200 (conv2 85 -> 93 us)
+    const char* e = getenv("LAUD_A_HYBRID");
+    return e ? atoi(e) : 0;
+  }();
+  p.a_hybrid = hybrid_env && p.a_tma && !p.a_tile && !a->a_compact;
+  // CTA pairs (cta_group::2, M = 256): long-K wide tiles with contiguous A rows and
+  // enough rows to fill the TPCs (measured: short K loses, gathered A gains nothing)
+  static const int pair_env = [] {
+    const char* e = getenv("LAUD_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  const long long pair_tiles = (long long)((a->rows_max + 255) / 256) * ((a->n_out + bn - 1) / bn);
+  const int pair = pair_env && bn == 256 && p.a_tile && kw >= 1024 && !a->sample_rows &&
+                   !a->chan_count && !a->b_batched && p.groups == 1 && pair_tiles >= num_sms() / 2;
+  CUtensorMap m;
+  if ((rc = tensor_map_2d(a->weight, a->n_out, kw, kw, pair ? bn / 2 : bn, &m, a->b_batched ? a->batch : 0)))
+    return rc;
   ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
   if (ps.on) {
     ps.rec.rows_per_count = a->row_mode == ROWS_PATCH ? (long long)p.patch_h * p.patch_w : 1;
@@ -350,7 +366,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
     ps.rec.taps = a->ksize * a->ksize;
     ps.rec.resid = a->resid != nullptr;
   }
-  return cuda_check(launch_conv_gemm(ma, m, bn, p, num_sms(), st), "conv_gemm launch", 1);
+  return cuda_check(launch_conv_gemm(ma, m, bn, p, num_sms(), st, pair), "conv_gemm launch", 1);
 }
 
 }  // namespace

@@ -96,10 +96,11 @@ struct TileInfo {
   int c_lo;  // first input channel of the tile's K window (grouped convs)
   bool skip;
 };
-template <int BN>
-__device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int t, int n_tiles) {
+template <int BN, bool PAIR = false>
+__device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int t, int n_tiles, int rank = 0) {
   TileInfo ti;
-  ti.m0 = (t / n_tiles) * BM;
+  // a pair tile is 256 rows: CTA `rank` of the pair owns rows 128*rank ..
+  ti.m0 = (t / n_tiles) * (PAIR ? 2 * BM : BM) + (PAIR ? rank * BM : 0);
   ti.n0 = (t % n_tiles) * BN;
   ti.sample = p.sample_rows > 0 ? ti.m0 / p.sample_rows : 0;
   ti.kc = p.chan_count ? __ldg(p.chan_count + ti.sample) : 0;
@@ -116,9 +117,9 @@ __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int t, int n_
   return ti;
 }
 
-template <int BN, int STAGES, int NSTG>
+template <int BN, int STAGES, int NSTG, bool PAIR = false>
 struct Smem {
-  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int B_STAGE_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's B rows
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
   static constexpr int STG_ROW = BN * 2 + 16;  // padded: conflict-free row-per-lane access
@@ -135,11 +136,17 @@ struct Smem {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 
-template <int BN, int STAGES, int NSTG>
+template <int BN, int STAGES, int NSTG, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      const ConvParams p) {
-  using L = Smem<BN, STAGES, NSTG>;
+  using L = Smem<BN, STAGES, NSTG, PAIR>;
+  // PAIR: a cluster of 2 CTAs on one TPC runs M = 256 tiles with
+  // tcgen05.mma.cta_group::2 issued by the leader (rank 0); each CTA loads
+  // its 128 A rows and half of B, so per-SM operand traffic per MMA halves.
+  const int rank = PAIR ? (int)cluster_ctarank() : 0;
+  const int t_begin = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base_u32 = (raw_u32 + 1023u) & ~1023u;
@@ -156,18 +163,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   unsigned long long* const trc = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
   const int nvalid = rows_valid(p);
   const int n_tiles = (p.n_out + BN - 1) / BN;
-  const int m_tiles = (nvalid + BM - 1) / BM;
+  const int m_tiles = (nvalid + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
   const int tiles = m_tiles * n_tiles;
-  if ((int)blockIdx.x >= tiles) return;  // uniform for the whole CTA
+  if (t_begin >= tiles) return;  // uniform for the whole CTA (and pair)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], p.a_tma ? 2 : 128 + 1);
+      // arrivals: A expect_tx (TMA) or 128 cp.async threads, hybrid both halves, + B
+      mbar_init(&full[s], p.a_hybrid ? 1 + 64 + 1 : (p.a_tma ? 2 : 128 + 1));
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], NUM_EPI_WARPS * 32);
+      mbar_init(&acc_empty[a], (PAIR ? 2 : 1) * NUM_EPI_WARPS);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -175,11 +183,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch_desc(&tmap_b);
     if (p.a_tma) tma_prefetch_desc(&tmap_a);
   }
-  if (warp == WARP_MMA) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  if (warp == WARP_MMA) {
+    if constexpr (PAIR)
+      tmem_alloc_pair<L::TMEM_COLS>(tmem_slot);
+    else
+      tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // barrier inits visible cluster-wide before any remote arrive
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // TMA completions go to the (leader's) full barrier; expect_tx only on the leader
+  auto full_tx = [&](int stage) -> uint32_t {
+    return PAIR ? mapa_shared(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
+  };
+  constexpr uint32_t XMUL = PAIR ? 2u : 1u;  // the leader expects both CTAs' bytes
+  const bool leader = rank == 0;
 
   if (warp < 4) {
     // ------------------------------------------------------------ A producers
@@ -188,8 +210,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (p.a_tile) {
       // Contiguous rows (compact / dense 1x1): one 128 x 64 TMA box per stage.
       if (tid == 0) {
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-          const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+        for (int t = t_begin; t < tiles; t += t_step) {
+          const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
           if (ti.skip) continue;
           const int row0 = p.sample_rows > 0
                                ? ti.sample * p.out_h * p.out_w + (ti.m0 - ti.sample * p.sample_rows)
@@ -201,7 +223,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (trc && it < 4096) trc[TRACE_A + it] = global_ns();
             const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
             if (p.dbg & 8) {
-              mbar_arrive(&full[stage]);
+              if (leader) mbar_arrive(&full[stage]);
+            } else if constexpr (PAIR) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], XMUL * A_STAGE_BYTES);
+              tma_load_2d_pair(sA, &tmap_a, full_tx(stage), ti.c_lo + kb * BK, row0);
             } else {
               mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES);
               tma_load_2d(sA, &tmap_a, &full[stage], ti.c_lo + kb * BK, row0);
@@ -209,11 +234,74 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+    } else if (p.a_hybrid) {
+      // Gathered rows split across two copy engines: rows 0-63 by TMA
+      // tile::gather4 (warps 0-1), rows 64-127 by cp.async through the LSU
+      // (warps 2-3, each thread one 16-byte chunk of 8 rows): the TMA unit's
+      // per-instruction rate no longer bounds the A stream alone.
+      const __nv_bfloat16* act = reinterpret_cast<const __nv_bfloat16*>(p.act);
+      const bool tma_half = tid < 64;
+      const int chunk = tid & 7, rsub = (tid - 64) >> 3;  // cp.async half: rows 64 + rsub + 8 i
+      for (int t = t_begin; t < tiles; t += t_step) {
+        const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
+        if (ti.skip) continue;
+        const int m0 = ti.m0;
+        RowPos rp[8];
+        bool rv[8];
+        if (tma_half) {
+          bool fp;
+          rv[0] = map_row(p, m0 + tid, nvalid, rp[0], fp);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            bool fp;
+            rv[i] = map_row(p, m0 + 64 + rsub + 8 * i, nvalid, rp[i], fp);
+          }
+        }
+        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (trc && tid == 0 && it < 4096) trc[TRACE_A + it] = global_ns();
+          const int tap = kb / ti.kpt;
+          const int c0 = ti.c_lo + (kb - tap * ti.kpt) * BK;
+          const int ky = tap / p.ksize;
+          const int kx = tap - ky * p.ksize;
+          const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
+          if (tma_half) {
+            int row = p.a_rows;  // out of bounds -> zero fill
+            if (rv[0]) {
+              const int iy = rp[0].y * p.stride + ky - p.pad;
+              const int ix = rp[0].x * p.stride + kx - p.pad;
+              if (iy >= 0 && iy < p.in_h && ix >= 0 && ix < p.in_w) row = (rp[0].n * p.in_h + iy) * p.in_w + ix;
+            }
+            const int r1 = __shfl_down_sync(0xffffffffu, row, 1);
+            const int r2 = __shfl_down_sync(0xffffffffu, row, 2);
+            const int r3 = __shfl_down_sync(0xffffffffu, row, 3);
+            if (tid == 0) mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES / 2);
+            if ((lane & 3) == 0) tma_gather4(sA + tid * 128, &tmap_a, &full[stage], c0, row, r1, r2, r3);
+          } else {
+            const int ch = c0 + chunk * 8;
+            const bool chv = ch < p.in_c;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 64 + rsub + 8 * i;
+              const uint32_t dst = sA + r * 128 + ((chunk ^ (r & 7)) << 4);
+              const int iy = rp[i].y * p.stride + ky - p.pad;
+              const int ix = rp[i].x * p.stride + kx - p.pad;
+              const bool v = rv[i] && chv && iy >= 0 && iy < p.in_h && ix >= 0 && ix < p.in_w;
+              const __nv_bfloat16* src = act + ((size_t)(rp[i].n * p.in_h + iy) * p.in_w + ix) * p.in_ld + ch;
+              cp_async_16(dst, v ? (const void*)src : (const void*)act, v ? 16u : 0u);
+            }
+            cp_async_mbar_arrive_noinc(&full[stage]);
+          }
+        }
+      }
     } else if (p.a_tma) {
       // One output row per thread; per (tap, channel block) every 4th lane issues
       // a TMA tile::gather4 of its 4 rows' source pixels (OOB index -> zeros).
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+      for (int t = t_begin; t < tiles; t += t_step) {
+        const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
         if (ti.skip) continue;
         const int m0 = ti.m0;
         RowPos rp;
@@ -243,16 +331,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int r2 = __shfl_down_sync(0xffffffffu, row, 2);
           const int r3 = __shfl_down_sync(0xffffffffu, row, 3);
           const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
-          if (tid == 0) mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES);
-          if ((lane & 3) == 0) tma_gather4(sA + tid * 128, &tmap_a, &full[stage], c0, row, r1, r2, r3);
+          if (tid == 0 && leader) mbar_arrive_expect_tx(&full[stage], XMUL * A_STAGE_BYTES);
+          if ((lane & 3) == 0) {
+            if constexpr (PAIR)
+              tma_gather4_pair(sA + tid * 128, &tmap_a, full_tx(stage), c0, row, r1, r2, r3);
+            else
+              tma_gather4(sA + tid * 128, &tmap_a, &full[stage], c0, row, r1, r2, r3);
+          }
         }
       }
     } else {
     const int chunk = tid & 7;
     const int rsub = tid >> 3;
     const __nv_bfloat16* act = reinterpret_cast<const __nv_bfloat16*>(p.act);
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+    for (int t = t_begin; t < tiles; t += t_step) {
+      const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
       if (ti.skip) continue;
       const int m0 = ti.m0;
       RowPos rp[8];
@@ -296,8 +389,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ B producer (TMA)
     if (lane == 0) {
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+      for (int t = t_begin; t < tiles; t += t_step) {
+        const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
         if (ti.skip) continue;
         for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
           const int stage = it % STAGES;
@@ -305,26 +398,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (trc && it < 4096) trc[TRACE_B + it] = global_ns();
           if (p.dbg & 16) {
-            mbar_arrive(&full[stage]);
+            if (leader) mbar_arrive(&full[stage]);
             continue;
           }
-          mbar_arrive_expect_tx(&full[stage], L::B_STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], XMUL * L::B_STAGE_BYTES);
           const int tap = kb / ti.kpt;
           const int kcoord = tap * p.kpad + ti.c_lo + (kb - tap * ti.kpt) * BK;  // per-tap stride kpad
           const uint32_t dst = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
-          if (p.b_batched)
+          if constexpr (PAIR) {  // this CTA's half of the tile's B rows
+            tma_load_2d_pair(dst, &tmap_b, full_tx(stage), kcoord, ti.n0 + rank * (BN / 2));
+          } else if (p.b_batched) {
             tma_load_3d(dst, &tmap_b, &full[stage], kcoord, ti.n0, ti.sample);
-          else
+          } else {
             tma_load_2d(dst, &tmap_b, &full[stage], kcoord, ti.n0);
+          }
         }
       }
     }
   } else if (warp == WARP_MMA) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    // (PAIR: the leader issues M = 256 MMAs for both CTAs; the peer's warp idles)
+    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * BM : BM, BN);
     uint32_t it = 0, local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+    for (int t = t_begin; t < tiles && leader; t += t_step) {
+      const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
       if (ti.skip) continue;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -344,16 +441,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sB = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16(tmem_d, umma_sdesc_sw128(sA + k * 32), umma_sdesc_sw128(sB + k * 32), idesc,
-                      (kb | k) != 0);
+            if constexpr (PAIR)
+              umma_bf16_pair(tmem_d, umma_sdesc_sw128(sA + k * 32), umma_sdesc_sw128(sB + k * 32), idesc,
+                             (kb | k) != 0);
+            else
+              umma_bf16(tmem_d, umma_sdesc_sw128(sA + k * 32), umma_sdesc_sw128(sB + k * 32), idesc,
+                        (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (PAIR)
+            umma_commit_pair(&empty[stage]);  // frees the stage in both CTAs
+          else
+            umma_commit(&empty[stage]);
         } else if (lane == 0) {
           mbar_arrive(&empty[stage]);
         }
         __syncwarp();
       }
-      if (lane == 0) umma_commit(&acc_full[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR)
+          umma_commit_pair(&acc_full[acc]);
+        else
+          umma_commit(&acc_full[acc]);
+      }
       __syncwarp();
     }
   } else {
@@ -401,10 +510,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       RowPos rp;
       bool fp;
     };
-    auto row_raw = [&](int t) { return row_fetch(p, (t / n_tiles) * BM + q * 32 + lane); };
+    constexpr int MT = PAIR ? 2 * BM : BM;  // rows per (pair) tile
+    auto row_raw = [&](int t) { return row_fetch(p, (t / n_tiles) * MT + rank * BM + q * 32 + lane); };
     auto row_info = [&](int t, int raw) {
       RowInfo ri;
-      const int m = (t / n_tiles) * BM + q * 32 + lane;
+      const int m = (t / n_tiles) * MT + rank * BM + q * 32 + lane;
       ri.valid = map_row_raw(p, m, nvalid, raw, ri.rp, ri.fp);
       ri.dst = 0;
       if (ri.valid) {
@@ -435,7 +545,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto next_valid = [&](int t) {
-      while (t < tiles && tile_info<BN>(p, t, n_tiles).skip) t += gridDim.x;
+      while (t < tiles && tile_info<BN, PAIR>(p, t, n_tiles, rank).skip) t += t_step;
       return t;
     };
     // per-column epilogue vectors of tile t: loads issued a tile ahead (into
@@ -447,7 +557,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     auto vec_load = [&](int t) {
       VecPre v;
-      const TileInfo tv = tile_info<BN>(p, t, n_tiles);
+      const TileInfo tv = tile_info<BN, PAIR>(p, t, n_tiles, rank);
       const int cb = tv.n0 + col0;
 #pragma unroll
       for (int u = 0; u < VPL; ++u) {
@@ -477,7 +587,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     };
     uint32_t local = 0;
-    int t = next_valid(blockIdx.x);
+    int t = next_valid(t_begin);
     RowInfo cur;
     if (t < tiles) {
       cur = row_info(t, row_raw(t));
@@ -486,7 +596,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
     }
     for (; t < tiles; ++local) {
-      const TileInfo ti = tile_info<BN>(p, t, n_tiles);
+      const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int buf = NSTG == 2 ? (local & 1) : 0;
@@ -503,7 +613,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.ymask_coarse) ymul = p.ymask_coarse[cell] ? 1.f : 0.f;
       }
       // next tile's rows and vectors: issue the global loads now, use them later
-      const int tn = next_valid(t + gridDim.x);
+      const int tn = next_valid(t + t_step);
       RowInfo nxt = cur;
       VecPre vpn;
       int raw_n = 0;
@@ -671,7 +781,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // accumulator consumed: hand the TMEM buffer back to the MMA warp early
       if (trc && ew == 0 && lane == 0 && local < 1024) trc[TRACE_EPI + 4 * local + 1] = global_ns();
       tc_fence_before();
-      mbar_arrive(&acc_empty[acc]);
+      __syncwarp();
+      if (lane == 0) {  // one arrive per warp, on the leader's barrier
+        if constexpr (PAIR)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&acc_empty[acc]), 0));
+        else
+          mbar_arrive(&acc_empty[acc]);
+      }
       __syncwarp();
       if (tn < tiles) {
         nxt = row_info(tn, raw_n);
@@ -704,10 +820,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // the peer's smem / barriers must outlive the leader's last use
+  else
+    __syncthreads();
   if (warp == WARP_MMA) {
     tc_fence_after();
-    tmem_dealloc<L::TMEM_COLS>(tmem_base);
+    if constexpr (PAIR)
+      tmem_dealloc_pair<L::TMEM_COLS>(tmem_base);
+    else
+      tmem_dealloc<L::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -715,15 +837,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // host side
 // ---------------------------------------------------------------------------
 
-template <int BN, int STAGES, int NSTG>
+template <int BN, int STAGES, int NSTG, bool PAIR = false>
 static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const ConvParams& p, int tiles_max,
                              int num_sms, cudaStream_t stream) {
-  using L = Smem<BN, STAGES, NSTG>;
+  using L = Smem<BN, STAGES, NSTG, PAIR>;
   static_assert(L::ALLOC <= 227 * 1024, "shared memory budget");
+  auto kern = conv_gemm_kernel<BN, STAGES, NSTG, PAIR>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, NSTG>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -731,16 +853,41 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
     const char* e = getenv("LAUD_GRID");  // debug: cap the persistent grid
     return e ? atoi(e) : 0;
   }();
-  int grid = tiles_max < num_sms ? tiles_max : num_sms;
+  // persistent grid: one CTA (PAIR: one CTA pair per TPC) per SM
+  const int units = PAIR ? num_sms / 2 : num_sms;
+  int grid = tiles_max < units ? tiles_max : units;
   if (grid_env > 0 && grid > grid_env) grid = grid_env;
   if (grid < 1) grid = 1;
-  conv_gemm_kernel<BN, STAGES, NSTG><<<grid, NUM_THREADS, L::ALLOC, stream>>>(tmap_a, tmap, p);
-  return cudaGetLastError();
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * grid, 1, 1);
+    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = L::ALLOC;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmap_a, tmap, p);
+  } else {
+    kern<<<grid, NUM_THREADS, L::ALLOC, stream>>>(tmap_a, tmap, p);
+    return cudaGetLastError();
+  }
 }
 
+// pair = 1: BN = 256 tiles of 256 rows on CTA pairs (cta_group::2); the B
+// tensor map's box is then BN / 2 rows (each CTA loads half).
 cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, int pair) {
   const int n_tiles = (p.n_out + bn - 1) / bn;
+  if (pair) {
+    if (bn != 256) return cudaErrorInvalidValue;
+    const int tiles_max = ((p.rows_max + 2 * BM - 1) / (2 * BM)) * n_tiles;
+    return launch_bn<256, 4, 1, true>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+  }
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
   switch (bn) {
     case 64: return launch_bn<64, 6, 2>(tmap_a, tmap, p, tiles_max, num_sms, stream);

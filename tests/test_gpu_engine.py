@@ -116,3 +116,54 @@ def test_grouped_conv_matches_torch(c, groups, stride, n, h):
                                      groups=groups).permute(0, 2, 3, 1)
     err = (out.float() - ref).norm() / ref.norm()
     assert err < 6e-3, float(err)
+
+
+@pytest.mark.parametrize("cin,cout,k,stride,n,h", [
+    (256, 1024, 1, 1, 128, 14), (256, 256, 3, 1, 128, 14), (512, 1024, 1, 2, 64, 28), (128, 512, 1, 1, 32, 28)])
+def test_cta_pair_tiles_match_torch(cin, cout, k, stride, n, h):
+    """Shapes large enough for the cta_group::2 (M = 256 pair) tiles."""
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(cin + cout + k + n)
+    x = torch.randn(n, h, h, cin, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(cout, cin, k, k, generator=g) / np.sqrt(cin * k * k)).to(torch.bfloat16).float()
+    b = torch.randn(cout, generator=g).cuda()
+    ho = (h + 2 * (k // 2) - k) // stride + 1
+    res = torch.randn(n, ho, ho, cout, generator=g).cuda().to(torch.bfloat16)
+    out = res.clone()
+    CH.conv(act=x, in_hw=(h, h), in_c=cin, in_ld=cin, weight=D.pack_weight(w, cin), n_out=cout, out=out,
+            out_ld=cout, out_hw=(ho, ho), batch=n, ksize=k, stride=stride, pad=k // 2, bias=b, relu=1,
+            resid=out, resid_ld=cout)
+    ref = torch.relu(_torch_conv_nhwc(x, w.cuda(), stride, k // 2) + b + res.float())
+    err = (out.float() - ref).norm() / ref.norm()
+    assert err < 6e-3, float(err)
+
+
+def test_cta_pair_patch_rows_scatter():
+    """Pair tiles over an active-patch list (S = 2) with scatter-add into the residual."""
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(11)
+    n, h, c, co, s = 128, 14, 256, 1024, 2
+    cells_per = (h // s) ** 2
+    rng = np.random.default_rng(0)
+    cz = rng.random(n * cells_per) < 0.6
+    cells = np.flatnonzero(cz).astype(np.int32)
+    lst = torch.from_numpy(cells).cuda()
+    cnt = torch.tensor([len(cells)], dtype=torch.int32, device="cuda")
+    rows = torch.randn(len(cells) * s * s, c, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(co, c, 1, 1, generator=g) / np.sqrt(c)).to(torch.bfloat16).float()
+    base = torch.randn(n, h, h, co, generator=g).cuda().to(torch.bfloat16)
+    out = base.clone()
+    CH.conv(act=rows, in_hw=(h, h), in_c=c, in_ld=c, weight=D.pack_weight(w, c), n_out=co, out=out,
+            out_ld=co, out_hw=(h, h), batch=n, a_compact=1, row_mode=CH.ROWS_PATCH, rows_max=n * h * h,
+            lst=lst, count=cnt, patch=(s, s), cells=(h // s, h // s), resid=out, resid_ld=co)
+    y = rows.float() @ w.cuda().reshape(co, c).t()
+    exp = base.float().clone()
+    for pi, cell in enumerate(cells.tolist()):
+        ni, r = divmod(cell, cells_per)
+        ci, cj = divmod(r, h // s)
+        blk = y[pi * s * s:(pi + 1) * s * s].reshape(s, s, co)
+        exp[ni, ci * s:(ci + 1) * s, cj * s:(cj + 1) * s] += blk
+    err = (out.float() - exp).norm() / exp.norm()
+    assert err < 6e-3, float(err)
+    untouched = ~torch.from_numpy(np.repeat(np.repeat(cz.reshape(n, h // s, h // s), s, 1), s, 2)).cuda()
+    assert torch.equal(out[untouched], base[untouched])
