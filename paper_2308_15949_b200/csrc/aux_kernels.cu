@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "laud_launch.cuh"
 #include "laud_ptx.cuh"
 
 namespace laud {
@@ -17,6 +18,8 @@ __global__ void stem_im2col_kernel(const uint8_t* __restrict__ img, int n, int h
                                    int pad, int ho, int wo, const float* __restrict__ mean,
                                    const float* __restrict__ inv_std,
                                    __nv_bfloat16* __restrict__ cols, int cols_ld) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   constexpr int SEG = (K * 3 + 7) / 8 * 8;
   const float m0 = mean[0], m1 = mean[1], m2 = mean[2];
   const float s0 = inv_std[0], s1 = inv_std[1], s2 = inv_std[2];
@@ -62,6 +65,8 @@ __global__ void stem_im2col_kernel(const uint8_t* __restrict__ img, int n, int h
 // 3x3 window, stride 2, pad 1 (padding never wins: -inf).
 __global__ void maxpool3s2_kernel(const __nv_bfloat16* __restrict__ x, int n, int h, int w, int c,
                                   int ho, int wo, __nv_bfloat16* __restrict__ y) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   const int c8 = c / 8;
   const long long total = (long long)n * ho * wo * c8;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -103,6 +108,8 @@ __global__ void maxpool3s2_kernel(const __nv_bfloat16* __restrict__ x, int n, in
 // y[n][c] = mean over hw pixels; one CTA per (n, 256-channel slice).
 __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int hw, int c,
                            __nv_bfloat16* __restrict__ y) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   const int ni = blockIdx.y;
   const int ch = blockIdx.x * blockDim.x + threadIdx.x;
   if (ch >= c) return;
@@ -121,10 +128,10 @@ cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, i
   auto* c = reinterpret_cast<__nv_bfloat16*>(cols);
   switch (k) {
     case 7:
-      stem_im2col_kernel<7><<<blocks, 256, 0, s>>>(img, n, h, w, stride, pad, ho, wo, mean, inv_std, c, cols_ld);
+      launch_k(stem_im2col_kernel<7>, dim3(blocks), dim3(256), 0, s, img, n, h, w, stride, pad, ho, wo, mean, inv_std, c, cols_ld);
       break;
     case 3:
-      stem_im2col_kernel<3><<<blocks, 256, 0, s>>>(img, n, h, w, stride, pad, ho, wo, mean, inv_std, c, cols_ld);
+      launch_k(stem_im2col_kernel<3>, dim3(blocks), dim3(256), 0, s, img, n, h, w, stride, pad, ho, wo, mean, inv_std, c, cols_ld);
       break;
     default:
       return cudaErrorInvalidValue;
@@ -136,14 +143,14 @@ cudaError_t launch_maxpool3s2(const void* x, int n, int h, int w, int c, void* y
   const int ho = (h - 1) / 2 + 1, wo = (w - 1) / 2 + 1;
   const long long total = (long long)n * ho * wo * (c / 8);
   const int blocks = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
-  maxpool3s2_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(x), n, h, w, c,
+  launch_k(maxpool3s2_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(x), n, h, w, c,
                                            ho, wo, reinterpret_cast<__nv_bfloat16*>(y));
   return cudaGetLastError();
 }
 
 cudaError_t launch_gap(const void* x, int n, int hw, int c, void* y, cudaStream_t s) {
   dim3 grid((c + 255) / 256, n);
-  gap_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(x), hw, c,
+  launch_k(gap_kernel, dim3(grid), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(x), hw, c,
                                   reinterpret_cast<__nv_bfloat16*>(y));
   return cudaGetLastError();
 }

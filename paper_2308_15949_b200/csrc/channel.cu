@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "laud_launch.cuh"
 #include "laud_ptx.cuh"
 
 namespace laud {
@@ -40,6 +41,8 @@ __global__ void __launch_bounds__(256) channel_masker_kernel(
     const float* __restrict__ w2, int d, int g, int cm, int cm_p, uint8_t* __restrict__ coarse,
     float* __restrict__ dvals, uint8_t* __restrict__ expanded, int* __restrict__ sel,
     int* __restrict__ count, const float* __restrict__ bias) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   extern __shared__ float sm[];
   float* gap = sm;
   float* hid = gap + c;
@@ -127,6 +130,8 @@ __global__ void __launch_bounds__(256) channel_masker_kernel(
 // Kept-channel lists from a caller-supplied expanded mask [N][cm_p].
 __global__ void channel_lists_kernel(const uint8_t* __restrict__ expanded, int cm_p,
                                      int* __restrict__ sel, int* __restrict__ count) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   const int n = blockIdx.x;
   const int lane = threadIdx.x;  // one warp
   int base = 0;
@@ -147,6 +152,8 @@ __global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ src, int s
                                     int src_k, __nv_bfloat16* __restrict__ dst, int dst_rows,
                                     int dst_k, const int* __restrict__ sel, const int* __restrict__ count,
                                     int sel_ld, int row_sel, int col_sel, int n_samples) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   const long long per = (long long)dst_rows * taps * (dst_k / 8);
   const long long total = per * n_samples;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
@@ -195,11 +202,11 @@ cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int h
                                   int* sel, int* count, const float* bias, cudaStream_t s) {
   const size_t smem = (size_t)(c + hd + d) * sizeof(float);
   if (x_f32)
-    channel_masker_kernel<float><<<n, 256, smem, s>>>(reinterpret_cast<const float*>(x), ld, hw, c,
+    launch_k(channel_masker_kernel<float>, dim3(n), dim3(256), smem, s, reinterpret_cast<const float*>(x), ld, hw, c,
                                                       w1, hd, w2, d, g, cm, cm_p, coarse, dvals,
                                                       expanded, sel, count, bias);
   else
-    channel_masker_kernel<__nv_bfloat16><<<n, 256, smem, s>>>(
+    launch_k(channel_masker_kernel<__nv_bfloat16>, dim3(n), dim3(256), smem, s, 
         reinterpret_cast<const __nv_bfloat16*>(x), ld, hw, c, w1, hd, w2, d, g, cm, cm_p, coarse,
         dvals, expanded, sel, count, bias);
   return cudaGetLastError();
@@ -207,7 +214,7 @@ cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int h
 
 cudaError_t launch_channel_lists(const uint8_t* expanded, int n, int cm_p, int* sel, int* count,
                                  cudaStream_t s) {
-  channel_lists_kernel<<<n, 32, 0, s>>>(expanded, cm_p, sel, count);
+  launch_k(channel_lists_kernel, dim3(n), dim3(32), 0, s, expanded, cm_p, sel, count);
   return cudaGetLastError();
 }
 
@@ -216,7 +223,7 @@ cudaError_t launch_pack_weights(const void* src, int src_rows, int taps, int src
                                 int sel_ld, int row_sel, int col_sel, int n, cudaStream_t s) {
   const long long total = (long long)n * dst_rows * taps * (dst_k / 8);
   const int blocks = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
-  pack_weights_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(
+  launch_k(pack_weights_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s, 
       reinterpret_cast<const __nv_bfloat16*>(src), src_rows, taps, src_k,
       reinterpret_cast<__nv_bfloat16*>(dst), dst_rows, dst_k, sel, count, sel_ld, row_sel, col_sel,
       n);

@@ -14,6 +14,8 @@
 #include <cstdint>
 
 #include "laud_conv.cuh"
+#include "laud_launch.cuh"
+#include "laud_ptx.cuh"
 #include "laud_rows.cuh"
 
 namespace laud {
@@ -23,6 +25,8 @@ constexpr int FM = 64, FN = 64, FK = 16;
 }
 
 __global__ void __launch_bounds__(256) conv_f32_kernel(const ConvParams p) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   __shared__ float As[FK][FM + 4];
   __shared__ float Bs[FK][FN + 4];
   const int tid = threadIdx.x;
@@ -134,8 +138,7 @@ __global__ void __launch_bounds__(256) conv_f32_kernel(const ConvParams p) {
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t stream) {
   dim3 grid((p.rows_max + FM - 1) / FM, (p.n_out + FN - 1) / FN);
   if (grid.x == 0 || grid.y == 0) return cudaSuccess;
-  conv_f32_kernel<<<grid, 256, 0, stream>>>(p);
-  return cudaGetLastError();
+  return launch_k(conv_f32_kernel, grid, dim3(256), 0, stream, p);
 }
 
 }  // namespace laud

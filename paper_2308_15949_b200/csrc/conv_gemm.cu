@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "laud_conv.cuh"
+#include "laud_launch.cuh"
 #include "laud_ptx.cuh"
 #include "laud_rows.cuh"
 
@@ -161,12 +162,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   unsigned long long* const trc = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
-  const int nvalid = rows_valid(p);
-  const int n_tiles = (p.n_out + BN - 1) / BN;
-  const int m_tiles = (nvalid + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
-  const int tiles = m_tiles * n_tiles;
-  if (t_begin >= tiles) return;  // uniform for the whole CTA (and pair)
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // arrivals: A expect_tx (TMA) or 128 cp.async threads, hybrid both halves, + B
@@ -202,8 +197,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   };
   constexpr uint32_t XMUL = PAIR ? 2u : 1u;  // the leader expects both CTAs' bytes
   const bool leader = rank == 0;
+  // PDL: everything above overlaps the previous kernel's tail; from here on the
+  // row counts / activations it produced are read
+  pdl_wait();
+  pdl_trigger();
+  const int nvalid = rows_valid(p);
+  const int n_tiles = (p.n_out + BN - 1) / BN;
+  const int m_tiles = (nvalid + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
+  const int tiles = m_tiles * n_tiles;
 
-  if (warp < 4) {
+  if (t_begin >= tiles) {
+    // no tile for this CTA (uniform across the pair): straight to teardown
+  } else if (warp < 4) {
     // ------------------------------------------------------------ A producers
     const int tid = threadIdx.x;
     uint32_t it = 0;
@@ -864,17 +869,18 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
     cfg.blockDim = dim3(NUM_THREADS, 1, 1);
     cfg.dynamicSmemBytes = L::ALLOC;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, tmap_a, tmap, p);
   } else {
-    kern<<<grid, NUM_THREADS, L::ALLOC, stream>>>(tmap_a, tmap, p);
-    return cudaGetLastError();
+    return launch_k(kern, dim3(grid), dim3(NUM_THREADS), L::ALLOC, stream, tmap_a, tmap, p);
   }
 }
 

@@ -10,6 +10,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---------------------------------------------------------------- PDL (laud_launch.cuh)
+// wait until the preceding kernels of the stream completed (memory visible);
+// no-op when the kernel was not launched with programmatic serialization
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next kernel's CTAs be scheduled (they still pdl_wait for our completion)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier
 #ifndef LAUD_TRYWAIT_HINT
 #define LAUD_TRYWAIT_HINT ""  // e.g. ", 0x989680": suspend-time hint (ns)

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "laud_launch.cuh"
 #include "laud_ptx.cuh"
 
 namespace laud {
@@ -67,6 +68,8 @@ __global__ void __launch_bounds__(256) cell_dot_kernel(
     const T* __restrict__ x, int ld, int n, int h, int w, int c, int win, int cells_h,
     int cells_w, const float* __restrict__ wdiff, int splits, int chunks_per_split,
     float* __restrict__ partial, const uint8_t* __restrict__ prev_coarse, float* __restrict__ dn) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   extern __shared__ float s_w[];
   for (int i = threadIdx.x; i < c; i += blockDim.x) s_w[i] = wdiff[i];
   __syncthreads();
@@ -267,6 +270,8 @@ __global__ void __launch_bounds__(CT_THREADS) compact_kernel(Flag flag, int tota
                                                              int* __restrict__ list,
                                                              int* __restrict__ count,
                                                              ScanState* st, int num_tiles) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   __shared__ int s_tile;
   __shared__ int s_warp[CT_THREADS / 32];
   __shared__ int s_excl;
@@ -325,6 +330,8 @@ __global__ void __launch_bounds__(256) masker_fused_kernel(
     const float* __restrict__ wdiff, float bias, float inv_area, int tc, uint8_t* __restrict__ coarse,
     float* __restrict__ dots, int* __restrict__ list, int* __restrict__ count, ScanState* st,
     int num_tiles) {
+  pdl_wait();  // PDL: predecessors' outputs visible from here
+  pdl_trigger();
   extern __shared__ float s_w[];           // c floats
   __shared__ unsigned char s_flag[256];
   __shared__ int s_tile, s_excl, s_rel;
@@ -505,7 +512,7 @@ static cudaError_t launch_compact(const Flag& f, int total, int* list, int* coun
                                   cudaStream_t stream) {
   const int tiles = (total + CT_TILE - 1) / CT_TILE;
   if (tiles == 0) return cudaMemsetAsync(count, 0, sizeof(int), stream);
-  compact_kernel<Flag><<<tiles, CT_THREADS, 0, stream>>>(f, total, list, count,
+  launch_k(compact_kernel<Flag>, dim3(tiles), dim3(CT_THREADS), 0, stream, f, total, list, count,
                                                          reinterpret_cast<ScanState*>(scan), tiles);
   return cudaGetLastError();
 }
@@ -554,11 +561,11 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
     const int tiles = (total + tc - 1) / tc;
     const float inv_area = 1.0f / (float)(win * win);
     if (x_f32)
-      masker_fused_kernel<float><<<tiles, 256, c * sizeof(float), stream>>>(
+      launch_k(masker_fused_kernel<float>, dim3(tiles), dim3(256), c * sizeof(float), stream, 
           reinterpret_cast<const float*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff, bias,
           inv_area, tc, coarse, partial, list, count, reinterpret_cast<ScanState*>(scan), tiles);
     else
-      masker_fused_kernel<__nv_bfloat16><<<tiles, 256, c * sizeof(float), stream>>>(
+      launch_k(masker_fused_kernel<__nv_bfloat16>, dim3(tiles), dim3(256), c * sizeof(float), stream, 
           reinterpret_cast<const __nv_bfloat16*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff,
           bias, inv_area, tc, coarse, partial, list, count, reinterpret_cast<ScanState*>(scan), tiles);
     return cudaGetLastError();
@@ -579,11 +586,11 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
       cell_dot_unrolled_kernel<16><<<blocks, 256, sm, stream>>>(xb, ld, n, h, w, c, win, cells_h,
                                                                 cells_w, wdiff, partial);
   } else if (x_f32)
-    cell_dot_kernel<float><<<blocks, 256, c * sizeof(float), stream>>>(
+    launch_k(cell_dot_kernel<float>, dim3(blocks), dim3(256), c * sizeof(float), stream, 
         reinterpret_cast<const float*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff, splits,
         cps, partial, prev_coarse, dn);
   else
-    cell_dot_kernel<__nv_bfloat16><<<blocks, 256, c * sizeof(float), stream>>>(
+    launch_k(cell_dot_kernel<__nv_bfloat16>, dim3(blocks), dim3(256), c * sizeof(float), stream, 
         reinterpret_cast<const __nv_bfloat16*>(x), ld, n, h, w, c, win, cells_h, cells_w, wdiff,
         splits, cps, partial, prev_coarse, dn);
   cudaError_t e = cudaGetLastError();

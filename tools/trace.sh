@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-python tools/engine_probe.py tiny one_wave_k256 two_wave_k256 four_wave_k256 > gpurun_out/probe_waves.log 2>&1
-LAUD_DBG=59 python tools/engine_probe.py tiny one_wave_k256 two_wave_k256 four_wave_k256 >> gpurun_out/probe_waves.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+LAUD_PDL=0 timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines > gpurun_out/bench_nopdl.log 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines > gpurun_out/bench_quick.log 2>&1
