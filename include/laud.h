@@ -207,6 +207,10 @@ typedef struct laud_block_args {
   /* fp32 mode: x / out / h1 / h2 fp32 and fp32 weights (same packed layouts);
    * every conv on the fp32 FFMA engine (1e-5 numerics path). */
   int fp32;
+  /* spatial: run conv1 densely on the input grid (the reference's own
+   * schedule, reference.py:385) instead of on the dilated pixel list — cheaper
+   * when the dilated set covers most pixels (S <= 2 at ratio >= 0.4). */
+  int conv1_dense;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

@@ -852,7 +852,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c1.out = a->h1;
   c1.out_ld = a->c_mid;
   c1.rows_max = n * a->h_in * a->w_in;
-  if (pm == ROWS_DENSE) {
+  if (pm == ROWS_DENSE || (a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense)) {
     c1.row_mode = ROWS_DENSE;
   } else if (a->paradigm == LAUD_PARADIGM_LAYER) {
     c1.row_mode = ROWS_PATCH;  // whole images of the active samples

@@ -198,6 +198,7 @@ class DeviceBlock:
             self.vec[k] = fvec(v, n, fill, device) if v is not None else None
         self.wdiff = None
         self.masker_bias = float(masker_bias)
+        self.conv1_dense = False  # spatial conv1 on the dilated pixel list (see laud.h)
         if masker_w is not None:
             self.set_masker(masker_w, masker_bias)
 
@@ -258,7 +259,7 @@ class DeviceBlock:
                 misplace_first: bool = False, stream=None, ws: Optional[Workspace] = None,
                 chmask: Optional[torch.Tensor] = None, coarse_out: Optional[torch.Tensor] = None,
                 prev_coarse: Optional[torch.Tensor] = None, dn: Optional[torch.Tensor] = None,
-                next_wdiff: Optional[torch.Tensor] = None):
+                next_wdiff: Optional[torch.Tensor] = None, conv1_dense: Optional[bool] = None):
         """x: (N, H, W, cin_p) bf16 CUDA.  Returns (out, coarse, cell_list, cell_count)."""
         n, h, w, cl = x.shape
         if cl != self.cin_p or x.dtype != self.dtype or not x.is_contiguous():
@@ -309,7 +310,8 @@ class DeviceBlock:
             cell_count=C.c_void_p(counts.data_ptr()), pix_list=ptr(pix_list),
             pix_count=C.c_void_p(counts.data_ptr() + 4), h1=ptr(h1), h2=ptr(h2),
             partial=ptr(partial), scan=ptr(scan), misplace_first=int(misplace_first),
-            fp32=int(self.dtype == torch.float32))
+            fp32=int(self.dtype == torch.float32),
+            conv1_dense=int(self.conv1_dense if conv1_dense is None else conv1_dense))
         if paradigm == "channel":
             self._channel_args(a, n, ws, chmask)
         if dn is not None and paradigm == "spatial":

@@ -132,6 +132,10 @@ class LaudNetwork:
             if para is Paradigm.CHANNEL:
                 g = self.plan[bp["stage"] - 1]
                 db.set_channel_masker(bp["ch_w1"], bp["ch_w2"], g)
+            # conv1 schedule: the dilated pixel set covers most of the input for
+            # S <= 2 at ratio >= 0.4 (r_dil ~0.9 at r = 0.5), where the dense
+            # conv1 (contiguous TMA rows, no dilation pass) is cheaper
+            db.conv1_dense = para is Paradigm.SPATIAL and s <= 2 and target_ratio >= 0.4
             self.slots.append(BlockSlot(bp["stage"], bp["index"], db, s))
         fc_in = net.classifier_features
         self.fc_w = D.pack_weight(params["fc_w"][:, :, None, None], D.pad8(fc_in), device)

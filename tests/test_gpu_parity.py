@@ -322,3 +322,25 @@ def test_fp32_mode_config1_and_regnet(fp32_mode):
     yr = R.block_forward_sparse(xi, rbw, rb, cfg, R.SpatialMask(coarse, R.upsample_coarse(coarse, 2), 2))
     ref = O.block_forward_sparse(xi, O.BlockWeights(rbw.w1, rbw.w2, rbw.w3, rbw.w_down), rb, cfg, om)
     assert _rel(yr, ref) <= FP32_TOL, _rel(yr, ref)
+
+
+@pytest.mark.parametrize("stage,s", [(3, 2), (2, 2), (4, 1), (1, 4)])
+def test_dense_conv1_schedule_is_bitwise_identical(stage, s):
+    """conv1 on the dense grid (reference.py:385) == conv1 on the dilated pixel list."""
+    import torch
+    from paper_2308_15949_b200 import device as D
+    from paper_2308_15949_b200.network import make_params
+    R = _R()
+    bp = [b for b in make_params("resnet101", 0)["blocks"] if b["stage"] == stage and b["index"] == 0][0]
+    blk = bp["block"]
+    ep = D.Epilogue(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"], relu2=True,
+                    s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"], relu_out=True)
+    db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep, masker_w=bp["masker_w"], fold_scale=True)
+    n, h = 8, blk.input_shape.height
+    x = torch.randn(n, h, h, db.cin_p, device="cuda").relu_().bfloat16()
+    o = blk.output_shape
+    coarse = (torch.rand(n * (o.height // s) * (o.width // s), device="cuda") < 0.5).to(torch.uint8)
+    y0, *_ = db.forward(x, "spatial", s, coarse=coarse, conv1_dense=False)
+    y1, *_ = db.forward(x, "spatial", s, coarse=coarse, conv1_dense=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
