@@ -285,6 +285,7 @@ def conv_roofline(torch, net, images, pk, pk_kind):
     return {
         "kernel": f"laud::conv_gemm_kernel, dominant shape rows={rows} n_out={n_out} K={k} "
                   f"taps={taps} resid={resid} ({len(grp)} launches/step)",
+        "shape": f"rows={rows} n_out={n_out} K={k} taps={taps} resid={resid}",
         "bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
         "frac": round(ach / peak, 4), "traffic": None,
         "peak_source": f"{pk_kind} MEASURED_PEAKS.json ({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})",
@@ -462,7 +463,7 @@ def run_gpu(args):
     if prof.exists():  # ncu --set full dram bytes of the same launch shape (profiles/)
         try:
             t = json.loads(prof.read_text())
-            if t.get("shape") == roof["kernel"].split(", ", 1)[1].split(" (")[0]:
+            if t.get("shape") == roof.get("shape"):
                 roof["traffic"] = t.get("traffic_per_launch")
         except Exception:
             pass

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
-timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines > gpurun_out/bench_quick.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_step.py resnet101 spatial 256 > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "masker or block_sparse" > gpurun_out/pytest_gpu.log 2>&1
+LAUD_MASKER_V2=0 python tools/profile_step.py resnet101 spatial 256 > gpurun_out/profile_v1.log 2>&1
+python tools/profile_step.py resnet101 spatial 256 > gpurun_out/profile_v2.log 2>&1
