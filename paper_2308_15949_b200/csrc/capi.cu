@@ -348,12 +348,13 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   // CTA pairs (cta_group::2, M = 256): long-K wide tiles with contiguous A rows and
   // enough rows to fill the TPCs (measured: short K loses, gathered A gains nothing)
   static const int pair_env = [] {
-    const char* e = getenv("LAUD_PAIR");
-    return e ? atoi(e) : 1;
+    const char* e = getenv("LAUD_PAIR");  // bit 0: long-K pairs, bit 1: short-K pairs
+    return e ? atoi(e) : 1;  // short-K pairs (2) measured slower: opt-in
   }();
   const long long pair_tiles = (long long)((a->rows_max + 255) / 256) * ((a->n_out + bn - 1) / bn);
-  const int pair = pair_env && bn == 256 && p.a_tile && kw >= 1024 && !a->sample_rows &&
-                   !a->chan_count && !a->b_batched && p.groups == 1 && pair_tiles >= num_sms() / 2;
+  const bool pair_ok = pair_env && bn == 256 && p.a_tile && !a->sample_rows && !a->chan_count &&
+                       !a->b_batched && p.groups == 1 && pair_tiles >= num_sms() / 2;
+  const int pair = !pair_ok ? 0 : (kw >= 1024 ? 1 : (kw <= 512 && (pair_env & 2) ? 2 : 0));
   CUtensorMap m;
   if ((rc = tensor_map_2d(a->weight, a->n_out, kw, kw, pair ? bn / 2 : bn, &m, a->b_batched ? a->batch : 0)))
     return rc;

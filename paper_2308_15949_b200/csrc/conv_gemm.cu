@@ -123,7 +123,12 @@ struct Smem {
   static constexpr int B_STAGE_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's B rows
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
-  static constexpr int STG_ROW = BN * 2 + 16;  // padded: conflict-free row-per-lane access
+  static constexpr int EW_COLS0 = BN / (NUM_EPI_WARPS / 4);
+  // staging rows: 16-byte chunks XOR-swizzled by row when a warp's slice is 8
+  // chunks wide (conflict-free row-per-lane and row-major access, no padding);
+  // narrower slices are padded instead
+  static constexpr bool STG_SWZ = EW_COLS0 == 64;
+  static constexpr int STG_ROW = STG_SWZ ? BN * 2 : BN * 2 + 16;
   static constexpr int STG_OFF = B_OFF + STAGES * B_STAGE_BYTES;
   static constexpr int STG_BUF = BM * STG_ROW;  // one staging buffer
   static constexpr int VEC_OFF = STG_OFF + NSTG * STG_BUF;  // per-warp scale/bias slices
@@ -488,6 +493,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - FIRST_EPI;
     const int col0 = (ew >> 2) * EW_COLS;
     const int stg_off0 = L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
+    // byte offset of 16-byte chunk c of slice row r (relative to stg_off0)
+    auto soff = [](int r, int c) { return r * L::STG_ROW + ((L::STG_SWZ ? (c ^ (r & 7)) : c) << 4); };
     float* const vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + ew * 3 * EW_COLS;
     float* const vbi_w = vsc + EW_COLS;
     float* const vnw = vbi_w + EW_COLS;  // next block's masker weights (masker-conv3 fusion)
@@ -544,7 +551,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const long long dr = __shfl_sync(0xffffffffu, ri.dst, r);
         const bool ok = rv && c < vchunks;
         const __nv_bfloat16* src = resid + dr * p.resid_ld + c_base + c * 8;
-        cp_async_16(sbase + r * L::STG_ROW + c * 16, ok ? (const void*)src : (const void*)resid,
+        cp_async_16(sbase + soff(r, c), ok ? (const void*)src : (const void*)resid,
                     ok ? 16u : 0u);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -634,7 +641,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (pre) asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col0;
-      uint8_t* my_row = stg + lane * L::STG_ROW;
+      auto slot_of = [&](int cl) { return reinterpret_cast<uint4*>(stg + soff(lane, cl >> 3)); };
       // generic 8-column step: affine, masks, residual, ReLU, store
       auto finish8 = [&](const uint32_t* rv, int cl) {
         float v[8];
@@ -664,7 +671,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] *= ymul;
         }
-        uint4* slot = reinterpret_cast<uint4*>(my_row + cl * 2);
+        uint4* slot = slot_of(cl);
         if (pre) {
           const uint4 rr = *slot;
           float2 f;
@@ -701,11 +708,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       };
       // branch-free CH-column step of the plain epilogue: y = acc + bias (+ resid), ReLU
       auto plain_chunk = [&](const uint32_t* rv, int cl, bool with_resid, bool relu) {
-        uint4* slot = reinterpret_cast<uint4*>(my_row + cl * 2);
         uint4 rr[CH / 8];
         if (with_resid) {
 #pragma unroll
-          for (int g = 0; g < CH / 8; ++g) rr[g] = slot[g];
+          for (int g = 0; g < CH / 8; ++g) rr[g] = *slot_of(cl + g * 8);
         }
 #pragma unroll
         for (int g = 0; g < CH / 8; ++g) {
@@ -736,7 +742,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           w.y = pack_bf16x2(v[2], v[3]);
           w.z = pack_bf16x2(v[4], v[5]);
           w.w = pack_bf16x2(v[6], v[7]);
-          slot[g] = w;
+          *slot_of(cl + g * 8) = w;
         }
       };
       const bool full = nch == EW_COLS;
@@ -813,7 +819,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const long long dr = __shfl_sync(0xffffffffu, cur.dst, r);
           if (rv && cc < vchunks)
             *reinterpret_cast<uint4*>(outp + dr * p.out_ld + c_base + cc * 8) =
-                *reinterpret_cast<const uint4*>(stg + r * L::STG_ROW + cc * 16);
+                *reinterpret_cast<const uint4*>(stg + soff(r, cc));
         }
       }
       __syncwarp();
@@ -884,14 +890,18 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   }
 }
 
-// pair = 1: BN = 256 tiles of 256 rows on CTA pairs (cta_group::2); the B
-// tensor map's box is then BN / 2 rows (each CTA loads half).
+// pair = 1: BN = 256 tiles of 256 rows on CTA pairs (cta_group::2), 4 stages;
+// pair = 2: the same for short K with 2 stages and double-buffered epilogue
+// staging (the next tile's residual streams in during this tile's math).  The
+// B tensor map's box is then BN / 2 rows (each CTA loads half).
 cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
                              cudaStream_t stream, int pair) {
   const int n_tiles = (p.n_out + bn - 1) / bn;
   if (pair) {
     if (bn != 256) return cudaErrorInvalidValue;
     const int tiles_max = ((p.rows_max + 2 * BM - 1) / (2 * BM)) * n_tiles;
+    if (pair == 2)  // short K: 2 operand stages, double-buffered epilogue staging
+      return launch_bn<256, 2, 2, true>(tmap_a, tmap, p, tiles_max, num_sms, stream);
     return launch_bn<256, 4, 1, true>(tmap_a, tmap, p, tiles_max, num_sms, stream);
   }
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
