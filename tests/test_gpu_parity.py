@@ -344,3 +344,16 @@ def test_dense_conv1_schedule_is_bitwise_identical(stage, s):
     y1, *_ = db.forward(x, "spatial", s, coarse=coarse, conv1_dense=True)
     torch.cuda.synchronize()
     assert torch.equal(y0, y1)
+
+
+def test_verify_cli_on_gpu(tmp_path):
+    """The reference's `verify` command (cli.py:250-278) against the GPU path:
+    the shipped case file passes, the fault hook fails (exit 1)."""
+    from paper_2308_15949_b200 import verify
+    cases = tmp_path / "cases.txt"  # the golden case set in the reference's case-file format
+    cases.write_text("".join(
+        f"paradigm={m['paradigm']} channels={m['channels']} height={m['height']} width={m['width']} "
+        f"granularity={m['granularity']} seed={m['seed']} tol={m['tol']}\n" for m in _cases()))
+    assert verify.main(["--cases", str(cases)]) == 0
+    assert verify.main(["--cases", str(cases), "--precision", "fp32"]) == 0
+    assert verify.main(["--per-paradigm", "2", "--inject-fault"]) == 1
