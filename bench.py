@@ -322,6 +322,40 @@ def static_cudnn_ms(torch, batch, steps, warmup, flush, arch="resnet101"):
     return tot / steps
 
 
+def batch1_latency(torch, args, net, flush, reps=20):
+    """BASELINE config 3's latency leg: one image, whole network as one CUDA graph
+    (L2 flushed before each replay): the dynamic net (its calibrated maskers),
+    the in-house static net and the torchvision/cuDNN static net, median ms."""
+    from paper_2308_15949_b200.network import LaudNetwork, random_images
+    img = random_images(1, seed=7)
+
+    def med(g):
+        _, per = timed_graph(torch, g, reps, flush, torch.cuda.current_stream())
+        return round(float(np.median(per)), 4)
+
+    out = {}
+    g, _ = capture(torch, lambda: net.forward(img), 2)
+    out["laud"] = med(g)
+    del g
+    snet = LaudNetwork(args.arch, "static", args.plan, 1.0, seed=0)
+    g, _ = capture(torch, lambda: snet.forward(img), 2)
+    out["static_inhouse"] = med(g)
+    del g, snet
+    try:
+        import torchvision
+        m = getattr(torchvision.models, TV_MODELS[args.arch])().cuda().eval().to(
+            memory_format=torch.channels_last).bfloat16()
+        x = torch.randn(1, 3, 224, 224, device="cuda").bfloat16().to(memory_format=torch.channels_last)
+        with torch.no_grad():
+            g, _ = capture(torch, lambda: m(x), 2)
+            out["static_cudnn"] = med(g)
+        del g, m
+    except Exception:
+        out["static_cudnn"] = None
+    torch.cuda.empty_cache()
+    return out
+
+
 def block_sweep(torch, args, flush):
     """Per-block device latency vs activation ratio (exact-count masks), batch = args.batch."""
     from paper_2308_15949_b200 import device as D
@@ -481,6 +515,10 @@ def run_gpu(args):
         extra["latency_reduction_vs_static_inhouse"] = round(1 - ms_step / static_ms, 4)
         if cud:
             extra["latency_reduction_vs_static_cudnn"] = round(1 - ms_step / cud, 4)
+        try:
+            extra["batch1_latency_ms"] = batch1_latency(torch, args, net, flush)
+        except Exception as exc:
+            extra["batch1_latency_ms"] = f"failed: {exc!r}"
         try:
             extra["per_block_us_vs_ratio"] = block_sweep(torch, args, flush)
         except Exception as exc:  # never lose the headline line to the sweep
