@@ -29,6 +29,7 @@ def shape_defs():
     d["two_wave_k256"] = dict(kind="gemm", m=2 * 148 * 128, n=256, k=256)
     d["four_wave_k256"] = dict(kind="gemm", m=4 * 148 * 128, n=256, k=256)
     d["conv2_s3"] = dict(kind="conv3x3", n=256, h=14, c=256)
+    d["conv2_s3_r05"] = dict(kind="conv3x3", n=128, h=14, c=256)  # 25088 rows = stage-3 conv2 at r=0.5
     d["conv2_s2"] = dict(kind="conv3x3", n=256, h=28, c=128)
     d["conv2_s1"] = dict(kind="conv3x3", n=256, h=56, c=64)
     d["conv1_s1"] = dict(kind="gemm", m=256 * 56 * 56, n=64, k=256)
