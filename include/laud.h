@@ -211,6 +211,16 @@ typedef struct laud_block_args {
    * schedule, reference.py:385) instead of on the dilated pixel list — cheaper
    * when the dilated set covers most pixels (S <= 2 at ratio >= 0.4). */
   int conv1_dense;
+  /* EXT squeeze-excitation after conv2 (RegNetY; se_hidden = C_mid / se_reduction,
+   * reference core.py:195): per sample, gate = sigmoid(se_w2 relu(se_w1 mean(h2)
+   * + se_b1) + se_b2) over the sample's conv2 rows (its active patches under a
+   * spatial mask), h2 *= gate.  fp32 [se_hidden][c_mid], [se_hidden], [c_mid][se_hidden],
+   * [c_mid]; se_w1 NULL = no SE (the reference executor has none). */
+  const float* se_w1;
+  const float* se_b1;
+  const float* se_w2;
+  const float* se_b2;
+  int se_hidden;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

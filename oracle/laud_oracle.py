@@ -314,6 +314,21 @@ class Epilogues:
     sd: Optional[np.ndarray] = None
     bd: Optional[np.ndarray] = None
     relu_out: bool = False
+    # EXT squeeze-excitation after conv2 (RegNetY; `core.py:195` se_hidden
+    # = C_mid // se_reduction): s = sigmoid(W2 relu(W1 mean(h2) + b1) + b2),
+    # h2 *= s per channel.  Under spatial sparsity the mean runs over the
+    # sample's active patches only (the pooling `latency.py:428-430` models);
+    # the reference executor itself never reads se_reduction.
+    se_w1: Optional[np.ndarray] = None  # [se_hidden, C_mid]
+    se_b1: Optional[np.ndarray] = None
+    se_w2: Optional[np.ndarray] = None  # [C_mid, se_hidden]
+    se_b2: Optional[np.ndarray] = None
+
+
+def _se_scale(pooled, ep):
+    """EXT SE gate from pooled h2 (..., C): sigmoid(W2 relu(W1 p + b1) + b2)."""
+    hid = np.maximum(pooled @ ep.se_w1.T + ep.se_b1, 0.0)
+    return 1.0 / (1.0 + np.exp(-(hid @ ep.se_w2.T + ep.se_b2)))
 
 
 def _affine(y, s, b, relu):
@@ -421,6 +436,13 @@ def _spatial_sparse(x, bw, block, mask, ep, rnd, misplace_first):
         y = _affine(y, ep.s2, ep.b2, ep.relu2)
     if rnd:
         y = rnd(y)
+    if ep is not None and ep.se_w1 is not None:  # EXT SE over each sample's active patches
+        for ni in np.unique(idx[:, 0]):
+            sel = idx[:, 0] == ni
+            gate = _se_scale(y[sel].transpose(1, 0, 2, 3).reshape(y.shape[1], -1).mean(axis=1), ep)
+            y[sel] = y[sel] * gate.reshape(1, -1, 1, 1)
+        if rnd:
+            y = rnd(y)
     y = conv_raw(y, bw.w3)
     if ep is not None:
         y = _affine(y, ep.s3, ep.b3, False)
@@ -506,6 +528,10 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
                 y = _affine(y, ep.s2, ep.b2, ep.relu2)
             if rnd:
                 y = rnd(y)
+            if ep is not None and ep.se_w1 is not None:  # EXT SE (whole image)
+                y = y * _se_scale(y.mean(axis=(2, 3))[0], ep).reshape(1, -1, 1, 1)
+                if rnd:
+                    y = rnd(y)
             y = conv2d_direct(y, block.conv3, bw.w3)
             if ep is not None:
                 y = _affine(y, ep.s3, ep.b3, False)
@@ -768,7 +794,8 @@ def network_forward(params: dict, images_u8: np.ndarray, paradigm: str = "spatia
         # folded BN as the device executor packs it: W' = W * s (rounded once), + b
         fold = lambda w, sc: None if w is None else w * sc.reshape(-1, 1, 1, 1)  # noqa: E731
         ep = Epilogues(b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"],
-                       relu_out=True)
+                       relu_out=True, se_w1=bp.get("se_w1"), se_b1=bp.get("se_b1"),
+                       se_w2=bp.get("se_w2"), se_b2=bp.get("se_b2"))
         bw = BlockWeights(fold(bp["w1"], bp["s1"]), fold(bp["w2"], bp["s2"]),
                           fold(bp["w3"], bp["s3"]), fold(bp["wd"], bp["sd"]))
         bias = 0.0 if biases is None else biases[i]

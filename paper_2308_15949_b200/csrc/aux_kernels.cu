@@ -119,6 +119,194 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int hw, int c,
   y[(size_t)ni * c + ch] = __float2bfloat16_rn(s / (float)hw);
 }
 
+// EXT squeeze-excitation on conv2's compact output rows h2 [rows][c] (bf16,
+// in place), two launches:
+//  se_pool_kernel (one CTA per sample n): its rows [r0, r1) — its active
+//    patches (patch list sorted by cell, `cells_per_img` cells per image,
+//    `rows_per_cell` rows each; found by a block-wide k-ary search) or, with
+//    list == nullptr, its dense pixel block — averaged into means[n][c]; the
+//    row range goes to rr[n].
+//  se_fc_scale_kernel (one CTA per SE_SPB samples): gate = sigmoid(W2 relu(W1
+//    mean + b1) + b2) with each weight row read once for SE_SPB samples, then
+//    h2 *= gate over those samples' rows (bf16 RNE) — the oracle EXT
+//    (`laud_oracle._se_scale`).
+constexpr int SE_SPB = 16;
+
+__global__ void __launch_bounds__(256) se_pool_kernel(const __nv_bfloat16* __restrict__ h2, int c,
+                                                      const int* __restrict__ list,
+                                                      const int* __restrict__ count, int cells_per_img,
+                                                      int rows_per_cell, int rows_per_img,
+                                                      float* __restrict__ means, int2* __restrict__ rr) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float mean[];
+  __shared__ int s_r0, s_r1;
+  const int n = blockIdx.x, tid = threadIdx.x;
+  if (list) {
+    // first patch of sample n and of n+1 in the sorted list: block-wide
+    // (blockDim)-ary search, a few rounds of one load per thread
+    const int cnt = *count;
+    for (int which = 0; which < 2; ++which) {
+      const int key = (n + which) * cells_per_img;
+      int lo = 0, hi = cnt;
+      while (hi - lo > 0) {
+        const int step = (hi - lo + blockDim.x - 1) / blockDim.x;
+        const int pos = lo + tid * step;
+        const bool below = pos < hi && list[pos] < key;
+        const int nb = __syncthreads_count(below);
+        if (step == 1) {
+          lo = hi = lo + nb;
+          break;
+        }
+        const int new_lo = nb == 0 ? lo : min(hi, lo + (nb - 1) * step + 1);
+        hi = min(hi, lo + nb * step);
+        lo = new_lo;
+      }
+      if (tid == 0) {
+        if (which == 0) s_r0 = lo * rows_per_cell; else s_r1 = lo * rows_per_cell;
+      }
+    }
+  } else if (tid == 0) {
+    s_r0 = n * rows_per_img;
+    s_r1 = (n + 1) * rows_per_img;
+  }
+  for (int i = tid; i < c; i += blockDim.x) mean[i] = 0.f;
+  __syncthreads();
+  const int r0 = s_r0, r1 = s_r1;
+  if (tid == 0) rr[n] = make_int2(r0, r1);
+  const int cpp = c >> 3;
+  const int groups = cpp <= (int)blockDim.x ? (int)blockDim.x / cpp : 1;
+  if (r1 > r0 && (tid < groups * cpp || cpp > (int)blockDim.x)) {
+    for (int cc = tid % cpp; cc < cpp; cc += (cpp > (int)blockDim.x ? blockDim.x : cpp)) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const int ch = cc << 3;
+      for (int r = r0 + tid / cpp; r < r1; r += groups) {
+        const uint4 v = *reinterpret_cast<const uint4*>(h2 + (size_t)r * c + ch);
+        float2 f;
+        f = unpack_bf16x2(v.x); acc[0] += f.x; acc[1] += f.y;
+        f = unpack_bf16x2(v.y); acc[2] += f.x; acc[3] += f.y;
+        f = unpack_bf16x2(v.z); acc[4] += f.x; acc[5] += f.y;
+        f = unpack_bf16x2(v.w); acc[6] += f.x; acc[7] += f.y;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) atomicAdd(&mean[ch + e], acc[e]);
+      if (cpp <= (int)blockDim.x) break;
+    }
+  }
+  __syncthreads();
+  const float inv = r1 > r0 ? 1.f / (float)(r1 - r0) : 0.f;
+  for (int i = tid; i < c; i += blockDim.x) means[(size_t)n * c + i] = mean[i] * inv;
+}
+
+__global__ void __launch_bounds__(256) se_fc_kernel(int n, int c, const float* __restrict__ means,
+                                                    const float* __restrict__ w1,
+                                                    const float* __restrict__ b1, int hs,
+                                                    const float* __restrict__ w2,
+                                                    const float* __restrict__ b2, float* __restrict__ gates) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float sm[];
+  float* mean = sm;                  // [SE_SPB][c]
+  float* hid = mean + SE_SPB * c;    // [SE_SPB][hs]
+  const int s0 = blockIdx.x * SE_SPB;
+  const int ns = min(SE_SPB, n - s0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < SE_SPB * c; i += blockDim.x)
+    mean[i] = i / c < ns ? means[(size_t)s0 * c + i] : 0.f;
+  __syncthreads();
+  // thread per output unit for all SE_SPB samples of the CTA: every weight is
+  // loaded once per CTA and feeds SE_SPB FMAs (means / hidden in smem)
+  for (int jj = tid; jj < hs; jj += blockDim.x) {  // hidden = relu(W1 mean + b1)
+    float a[SE_SPB];
+#pragma unroll
+    for (int q = 0; q < SE_SPB; ++q) a[q] = 0.f;
+    const float4* wr = reinterpret_cast<const float4*>(w1 + (size_t)jj * c);
+#pragma unroll 2
+    for (int i = 0; i < c / 4; ++i) {
+      const float4 wv = __ldg(wr + i);
+#pragma unroll
+      for (int q = 0; q < SE_SPB; ++q) {
+        const float4 mv = reinterpret_cast<const float4*>(mean + q * c)[i];
+        a[q] = fmaf(wv.x, mv.x, fmaf(wv.y, mv.y, fmaf(wv.z, mv.z, fmaf(wv.w, mv.w, a[q]))));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < SE_SPB; ++q) hid[q * hs + jj] = fmaxf(a[q] + b1[jj], 0.f);
+  }
+  __syncthreads();
+  for (int ii = tid; ii < c; ii += blockDim.x) {  // gate = sigmoid(W2 hidden + b2)
+    float a[SE_SPB];
+#pragma unroll
+    for (int q = 0; q < SE_SPB; ++q) a[q] = 0.f;
+    const float* wr = w2 + (size_t)ii * hs;
+#pragma unroll 4
+    for (int jj = 0; jj < hs; ++jj) {
+      const float wv = __ldg(wr + jj);
+#pragma unroll
+      for (int q = 0; q < SE_SPB; ++q) a[q] = fmaf(wv, hid[q * hs + jj], a[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < SE_SPB; ++q)
+      if (q < ns) gates[(size_t)(s0 + q) * c + ii] = 1.f / (1.f + __expf(-(a[q] + b2[ii])));
+  }
+}
+
+// h2 *= gate[sample of the row], elementwise over all rows (16-byte chunks)
+__global__ void __launch_bounds__(256) se_scale_kernel(__nv_bfloat16* __restrict__ h2, int c,
+                                                       const int* __restrict__ list,
+                                                       const int* __restrict__ count, int cells_per_img,
+                                                       int rows_per_cell, int rows_per_img, int rows_max,
+                                                       const float* __restrict__ gates) {
+  pdl_wait();
+  pdl_trigger();
+  const int cpp = c >> 3;
+  const long long rows = list ? min((long long)*count * rows_per_cell, (long long)rows_max) : rows_max;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < rows * cpp;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long row = k / cpp;
+    const int ch = (int)(k - row * cpp) << 3;
+    const int n = list ? list[row / rows_per_cell] / cells_per_img : (int)(row / rows_per_img);
+    const float4 g0 = *reinterpret_cast<const float4*>(gates + (size_t)n * c + ch);
+    const float4 g1 = *reinterpret_cast<const float4*>(gates + (size_t)n * c + ch + 4);
+    uint4* pp = reinterpret_cast<uint4*>(h2 + row * c + ch);
+    uint4 v = *pp;
+    float2 f;
+    f = unpack_bf16x2(v.x); v.x = pack_bf16x2(f.x * g0.x, f.y * g0.y);
+    f = unpack_bf16x2(v.y); v.y = pack_bf16x2(f.x * g0.z, f.y * g0.w);
+    f = unpack_bf16x2(v.z); v.z = pack_bf16x2(f.x * g1.x, f.y * g1.y);
+    f = unpack_bf16x2(v.w); v.w = pack_bf16x2(f.x * g1.z, f.y * g1.w);
+    *pp = v;
+  }
+}
+
+// scratch: >= 2*n*c floats + n int2 (the block's h1 buffer, dead after conv2)
+cudaError_t launch_se(void* h2, int n, int c, const int* list, const int* count, int cells_per_img,
+                      int rows_per_cell, int rows_per_img, const float* w1, const float* b1, int hs,
+                      const float* w2, const float* b2, void* scratch, cudaStream_t s) {
+  float* means = reinterpret_cast<float*>(scratch);
+  float* gates = means + (size_t)n * c;
+  int2* rr = reinterpret_cast<int2*>(gates + (((size_t)n * c + 3) & ~(size_t)3));
+  launch_k(se_pool_kernel, dim3(n), dim3(256), (size_t)c * sizeof(float), s,
+           reinterpret_cast<const __nv_bfloat16*>(h2), c, list, count, cells_per_img, rows_per_cell,
+           rows_per_img, means, rr);
+  const size_t smem = (size_t)SE_SPB * (c + hs) * sizeof(float);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(se_fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  launch_k(se_fc_kernel, dim3((n + SE_SPB - 1) / SE_SPB), dim3(256), smem, s, n, c, means, w1, b1, hs, w2,
+           b2, gates);
+  const int rows_max = list ? n * cells_per_img * rows_per_cell : n * rows_per_img;
+  const long long work = (long long)rows_max * (c / 8);
+  const int blocks = (int)((work + 255) / 256 < 148 * 16 ? (work + 255) / 256 : 148 * 16);
+  launch_k(se_scale_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s,
+           reinterpret_cast<__nv_bfloat16*>(h2), c, list, count, cells_per_img, rows_per_cell, rows_per_img,
+           rows_max, gates);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride, int pad,
                                const float* mean, const float* inv_std, void* cols, int cols_ld,
                                cudaStream_t s) {

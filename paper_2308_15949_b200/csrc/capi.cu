@@ -39,6 +39,9 @@ cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, i
                                cudaStream_t s);
 cudaError_t launch_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, cudaStream_t s);
 cudaError_t launch_gap(const void* x, int n, int hw, int c, void* y, cudaStream_t s);
+cudaError_t launch_se(void* h2, int n, int c, const int* list, const int* count, int cells_per_img,
+                      int rows_per_cell, int rows_per_img, const float* w1, const float* b1, int hs,
+                      const float* w2, const float* b2, void* scratch, cudaStream_t s);
 cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c,
                                   const float* w1, int hd, const float* w2, int d, int g, int cm,
                                   int cm_p, uint8_t* coarse, float* dvals, uint8_t* expanded,
@@ -907,6 +910,17 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c2.out = a->h2;
   c2.out_ld = a->c_mid;
   if ((rc = run_conv(&c2, st))) return rc;
+  if (a->se_w1) {  // EXT squeeze-excitation over each sample's conv2 rows
+    if (a->fp32) return fail(LAUD_ERR_UNSUPPORTED, "SE in fp32 mode");
+    if (!a->se_b1 || !a->se_w2 || !a->se_b2 || a->se_hidden < 1)
+      return fail(LAUD_ERR_ARG, "SE weights incomplete");
+    ProfScope ps(3, st);
+    if ((rc = cuda_check(launch_se(a->h2, n, a->c_mid, pm == ROWS_DENSE ? nullptr : cells,
+                                   pm == ROWS_DENSE ? nullptr : cells_n, ch * cw, ph * pw, ho * wo,
+                                   a->se_w1, a->se_b1, a->se_hidden, a->se_w2, a->se_b2, a->h1, st),
+                         "se", 3)))
+      return rc;
+  }
 
   // ---------------------------------------------------------------- conv3 + scatter-add
   laud_conv_args c3 = c2;

@@ -199,6 +199,7 @@ class DeviceBlock:
         self.wdiff = None
         self.masker_bias = float(masker_bias)
         self.conv1_dense = False  # spatial conv1 on the dilated pixel list (see laud.h)
+        self.se = None            # EXT squeeze-excitation (set_se)
         if masker_w is not None:
             self.set_masker(masker_w, masker_bias)
 
@@ -209,6 +210,16 @@ class DeviceBlock:
         wd[: mw.shape[1]] = (mw[0] - mw[1]).astype(np.float32)
         self.wdiff = torch.from_numpy(wd).to(self.w1.device)
         self.masker_bias = float(bias)
+
+    def set_se(self, w1, b1, w2, b2):
+        """EXT squeeze-excitation after conv2 (include/laud.h, laud_block_args.se_*):
+        w1 [hidden, C_mid], b1 [hidden], w2 [C_mid, hidden], b2 [C_mid]."""
+        dev = self.w1.device
+        f = lambda a: torch.as_tensor(np.asarray(a, dtype=np.float32)).contiguous().to(dev)  # noqa: E731
+        w1, w2 = np.asarray(w1), np.asarray(w2)
+        if w1.shape[1] != self.c_mid or w2.shape[0] != self.c_mid or self.cmid_p != self.c_mid:
+            raise DeviceError("SE needs [hidden, C_mid] / [C_mid, hidden] weights and C_mid % 8 == 0")
+        self.se = (f(w1), f(b1), f(w2), f(b2), int(w1.shape[0]))
 
     def out_hw(self, h: int, w: int):
         return self.block.conv2.out_hw(h, w)
@@ -311,6 +322,9 @@ class DeviceBlock:
             pix_count=C.c_void_p(counts.data_ptr() + 4), h1=ptr(h1), h2=ptr(h2),
             partial=ptr(partial), scan=ptr(scan), misplace_first=int(misplace_first),
             fp32=int(self.dtype == torch.float32),
+            se_w1=ptr(self.se[0]) if self.se else None, se_b1=ptr(self.se[1]) if self.se else None,
+            se_w2=ptr(self.se[2]) if self.se else None, se_b2=ptr(self.se[3]) if self.se else None,
+            se_hidden=self.se[4] if self.se else 0,
             conv1_dense=int(self.conv1_dense if conv1_dense is None else conv1_dense))
         if paradigm == "channel":
             self._channel_args(a, n, ws, chmask)

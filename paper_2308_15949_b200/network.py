@@ -67,6 +67,12 @@ def make_params(arch: str = "resnet101", seed: int = 0) -> dict:
             s3=np.full(co, 0.5), b3=rng.standard_normal(co) * 0.05,
             sd=np.ones(co), bd=np.zeros(co),
             masker_w=rng.standard_normal((2, ci, 1, 1)) / np.sqrt(ci)))
+        if blk.se_reduction:  # RegNetY squeeze-excitation (EXT; `core.py:195` se_hidden)
+            hs = blk.se_hidden
+            blocks[-1].update(se_w1=rng.standard_normal((hs, cm)) / np.sqrt(cm),
+                              se_b1=rng.standard_normal(hs) * 0.05,
+                              se_w2=rng.standard_normal((cm, hs)) / np.sqrt(hs),
+                              se_b2=rng.standard_normal(cm) * 0.05 + 1.0)
     p["blocks"] = blocks
     fc_in = net.classifier_features
     p["fc_w"] = rng.standard_normal((net.num_classes, fc_in)) / np.sqrt(fc_in)
@@ -132,6 +138,8 @@ class LaudNetwork:
             if para is Paradigm.CHANNEL:
                 g = self.plan[bp["stage"] - 1]
                 db.set_channel_masker(bp["ch_w1"], bp["ch_w2"], g)
+            if "se_w1" in bp:  # RegNetY squeeze-excitation (EXT)
+                db.set_se(bp["se_w1"], bp["se_b1"], bp["se_w2"], bp["se_b2"])
             # conv1 schedule: the dilated pixel set covers most of the input for
             # S <= 2 at ratio >= 0.4 (r_dil ~0.9 at r = 0.5), where the dense
             # conv1 (contiguous TMA rows, no dilation pass) is cheaper

@@ -357,3 +357,49 @@ def test_verify_cli_on_gpu(tmp_path):
     assert verify.main(["--cases", str(cases)]) == 0
     assert verify.main(["--cases", str(cases), "--precision", "fp32"]) == 0
     assert verify.main(["--per-paradigm", "2", "--inject-fault"]) == 1
+
+
+@pytest.mark.parametrize("stage,index,paradigm", [(2, 1, "spatial"), (3, 0, "spatial"), (4, 1, "spatial"),
+                                                   (3, 1, "layer"), (2, 0, "static")])
+def test_regnet_se_block_matches_oracle_ext(stage, index, paradigm):
+    """EXT squeeze-excitation (pool over the sample's active patches) on the device
+    vs the oracle EXT, bf16 rounding points emulated."""
+    import torch
+    from paper_2308_15949_b200 import device as D
+    from paper_2308_15949_b200.network import make_params
+    _R()
+    bp = [b for b in make_params("regnety-1.6gf", 0)["blocks"] if b["stage"] == stage and b["index"] == index][0]
+    blk = bp["block"]
+    assert "se_w1" in bp
+    ep = D.Epilogue(b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"], relu_out=True)
+    db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep)
+    db.set_se(bp["se_w1"], bp["se_b1"], bp["se_w2"], bp["se_b2"])
+    rng = np.random.default_rng(stage)
+    n = 3
+    ci = blk.input_shape
+    x = np.maximum(rng.standard_normal((n, ci.channels, ci.height, ci.width)), 0)
+    o = blk.output_shape
+    s = (4, 4, 2, 1)[stage - 1]
+    oep = O.Epilogues(b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"],
+                      relu_out=True, se_w1=bp["se_w1"], se_b1=bp["se_b1"], se_w2=bp["se_w2"], se_b2=bp["se_b2"])
+    obw = O.BlockWeights(bp["w1"], bp["w2"], bp["w3"], bp["wd"])
+    xd = D.to_device_nhwc(x)
+    if paradigm == "spatial":
+        coarse = rng.random((n, o.height // s, o.width // s)) < 0.5
+        coarse[1] = False  # a sample with no active patch
+        y, *_ = db.forward(xd, "spatial", s, coarse=torch.from_numpy(coarse.astype(np.uint8).reshape(-1)).cuda())
+        cfg, om = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=s), O.SpatialMask(coarse, O.upsample_coarse(coarse, s), s)
+    elif paradigm == "layer":
+        d = np.array([True, False, True])
+        y, *_ = db.forward(xd, "layer", coarse=torch.from_numpy(d.astype(np.uint8)).cuda())
+        cfg, om = DynamicConfig(Paradigm.LAYER), O.LayerMask(d)
+    else:
+        y, *_ = db.forward(xd, "static")
+        cfg, om = DynamicConfig(Paradigm.STATIC), None
+    torch.cuda.synchronize()
+    yg = D.from_device_nhwc(y, o.channels)
+    emu = O.block_forward_sparse(x, obw, blk, cfg, om, epilogues=oep, emulate_bf16=True)
+    assert _rel(yg, emu) <= 2e-3, _rel(yg, emu)
+    no_se = O.block_forward_sparse(x, obw, blk, cfg, om, epilogues=O.Epilogues(
+        b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"], relu_out=True), emulate_bf16=True)
+    assert _rel(yg, no_se) > 1e-2  # the gate is really applied

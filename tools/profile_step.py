@@ -8,7 +8,7 @@ from paper_2308_15949_b200.network import LaudNetwork, random_images
 arch = sys.argv[1] if len(sys.argv) > 1 else "resnet101"
 para = sys.argv[2] if len(sys.argv) > 2 else "spatial"
 batch = int(sys.argv[3]) if len(sys.argv) > 3 else 256
-net = LaudNetwork(arch, para, "4-2-2-1", 0.5)
+net = LaudNetwork(arch, para, sys.argv[4] if len(sys.argv) > 4 else ("4-4-2-1" if arch.startswith("regnet") else "4-2-2-1"), 0.5)
 img = random_images(batch)
 net.calibrate(img)
 for _ in range(3):

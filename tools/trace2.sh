@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-python tools/engine_probe.py stem gemm_k256_n1024 conv3_s3 conv2_s3 > gpurun_out/probe_stem.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_rg.csv python tools/profile_step.py regnety-1.6gf spatial 1024 > /dev/null 2>&1
