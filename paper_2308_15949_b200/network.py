@@ -354,6 +354,63 @@ class LaudNetwork:
         return out
 
 
+class PipelinedRunner:
+    """Streams host image batches through a LaudNetwork end to end.
+
+    Two device input buffers, one captured CUDA graph per buffer: the pinned
+    host->device upload of batch i+1 runs on a copy stream while batch i's
+    forward runs; each batch's fp32 logits come back to pinned host memory on
+    the compute stream right after its graph.  ``run`` returns the device-timed
+    milliseconds of the whole sequence (CUDA events on the compute stream).
+    """
+
+    def __init__(self, net: "LaudNetwork", batch: int, h: int = 224, w: int = 224, warmup: int = 2):
+        self.net = net
+        self.bufs = [torch.empty((batch, h, w, 3), dtype=torch.uint8, device=net.device) for _ in range(2)]
+        self.copy = torch.cuda.Stream(device=net.device)
+        self.comp = torch.cuda.Stream(device=net.device)
+        self.graphs = []
+        self.logits = None
+        for buf in self.bufs:
+            with torch.cuda.stream(self.comp):
+                for _ in range(max(1, warmup)):
+                    net.forward(buf)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.comp):
+                self.logits = net.forward(buf)
+            self.graphs.append(g)
+        torch.cuda.synchronize()
+
+    def run(self, host_batches, host_out, before_step=None) -> float:
+        """host_batches: pinned uint8 (N, H, W, 3) tensors; host_out: pinned fp32
+        (len, N, classes) tensor receiving the logits."""
+        up = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.copy.wait_stream(torch.cuda.current_stream())
+        self.comp.wait_stream(torch.cuda.current_stream())
+        e0.record(self.comp)
+        self.copy.wait_event(e0)
+        for i, hb in enumerate(host_batches):
+            k = i & 1
+            with torch.cuda.stream(self.copy):
+                if i >= 2:
+                    self.copy.wait_event(done[k])  # graph i-2 finished reading this buffer
+                self.bufs[k].copy_(hb, non_blocking=True)
+                up[k].record(self.copy)
+            with torch.cuda.stream(self.comp):
+                if before_step is not None:
+                    before_step()
+                self.comp.wait_event(up[k])
+                self.graphs[k].replay()
+                done[k].record(self.comp)
+                host_out[i].copy_(self.logits, non_blocking=True)
+        e1.record(self.comp)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+
 def add_channel_maskers(params: dict, gplan, seed: int = 0) -> dict:
     """Channel-masker MLP weights per block (`reference.py:189-223`): G from the
     stage's plan entry, D = C_mid / G, hidden h = max(D // 16, 16); w1 [h, C_in]

@@ -74,3 +74,21 @@ def test_masker_conv3_fusion_matches_unfused():
     assert agree > 0.999, agree
     rel = np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[0])
     assert rel < 2e-2, rel
+
+
+def test_pipelined_runner_matches_forward():
+    """Streaming e2e path (upload overlapping the previous forward) returns, per
+    batch, the same logits as a plain forward of that batch."""
+    import torch
+    from paper_2308_15949_b200.network import LaudNetwork, PipelinedRunner, random_images
+    net = LaudNetwork("resnet50", "spatial", "4-4-2-1", 0.5, seed=0)
+    imgs = [random_images(4, seed=s) for s in (11, 12, 13)]
+    net.calibrate(imgs[0])
+    ref = [net.forward(b)[:, :1000].float().cpu() for b in imgs]
+    runner = PipelinedRunner(net, 4)
+    host = [b.cpu().pin_memory() for b in imgs]
+    out = torch.empty((3, 4, net.n_cls), dtype=torch.float32, pin_memory=True)
+    ms = runner.run(host, out)
+    assert ms > 0
+    for i in range(3):
+        assert torch.equal(out[i, :, :1000], ref[i])
