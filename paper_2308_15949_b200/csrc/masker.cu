@@ -554,7 +554,11 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
           reinterpret_cast<ScanState*>(scan), tiles);
     return cudaGetLastError();
   }
-  if (splits == 1 && total > 0 && total <= 4096 && !dn) {  // small grids: one launch wins
+  static const int fused_max = [] {
+    const char* e = getenv("LAUD_MASKER_FUSED_MAX");
+    return e ? atoi(e) : 4096;
+  }();
+  if (splits == 1 && total > 0 && total <= fused_max && !dn) {  // small grids: one launch wins
     // one pass: dots + decisions + compaction; ~2 waves of CTAs over the SMs
     // one cell per warp: as many resident warps (bytes in flight) as the SMs hold
     const int tc = 8;
