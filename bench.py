@@ -151,13 +151,14 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host time, csv line)
+        self.window = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -167,7 +168,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def wait_ready(self, timeout=10.0):
+        """Block until nvidia-smi streams samples (it takes ~0.1-1 s to start)."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self, t0, t1):
+        """Keep only the samples taken inside [t0, t1] (the timed region)."""
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -180,7 +191,9 @@ class ClockSampler:
     def summary(self):
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for ts, ln in self.lines
+                 if self.window is None or self.window[0] <= ts <= self.window[1] + 0.03]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -449,7 +462,10 @@ def run_gpu(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.wait_ready()
+        t_start = time.time()
         tot_ms, per = timed_graph(torch, graph, args.steps, flush, stream)
+        clk.mark(t_start, time.time())
     torch.cuda.synchronize()
     if ws > 1:
         t = torch.tensor([tot_ms], device="cuda")
