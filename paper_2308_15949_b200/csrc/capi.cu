@@ -207,6 +207,45 @@ int tensor_map_2d(const void* w, int rows, int k, int ld, int bn, CUtensorMap* o
   return LAUD_OK;
 }
 
+// Activation as a 4D tensor [batch][h][w][c] (c contiguous, row stride ld) with a
+// {64 ch, S, S, 1} box traversed at the conv stride: one TMA op loads one S x S
+// patch's tap window (OOB -> zeros, negative coordinates included).
+int tensor_map_patch(const void* act, int batch, int h, int w, int c, int ld, int s, int stride,
+                     CUtensorMap* out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  MapKey key{act, -(batch * 4096 + h), -(w * 65536 + c), -(ld * 64 + s * 8 + stride), dev};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return LAUD_OK;
+    }
+  }
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                               CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                               CUtensorMapFloatOOBfill);
+  EncodeFn fn = reinterpret_cast<EncodeFn>(encode_fn());
+  if (!fn) return fail(LAUD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap m;
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)ld * 2, (cuuint64_t)w * ld * 2, (cuuint64_t)h * w * ld * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)(s * stride), (cuuint32_t)(s * stride), 1};
+  cuuint32_t estr[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(act), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LAUD_ERR_CUDA, "cuTensorMapEncodeTiled (patch box) failed (%d)", (int)r);
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    g_maps[key] = m;
+  }
+  *out = m;
+  return LAUD_OK;
+}
+
 // Tile width: BN=128 (double-buffered epilogue staging) for epilogue-heavy
 // small-K convs and for grids too small to fill the SMs at BN=256.
 int pick_bn(int n_out, int k, long long rows) {
@@ -339,7 +378,21 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
                  (a->a_compact || (a->row_mode == ROWS_DENSE && a->sample_rows == 0 &&
                                    a->stride == 1 && a->pad == 0 && a->in_h == a->out_h &&
                                    a->in_w == a->out_w));
-      if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, p.a_tile ? 128 : 1, &ma))) return rc;
+      // S x S patches of a 3x3 conv: one 4D box per patch and tap instead of S*S/4 gathers
+      static const int a_box_env = [] {
+        const char* e = getenv("LAUD_A_BOX");  // bit 0: S = 4, bit 1: S = 2
+        return e ? atoi(e) : 1;
+      }();
+      const int s_box = a->patch_h;
+      p.a_box = a->row_mode == ROWS_PATCH && a->ksize == 3 && !a->a_compact && a->patch_h == a->patch_w &&
+                ((s_box == 4 && (a_box_env & 1)) || (s_box == 2 && (a_box_env & 2))) &&
+                a->in_ld % 8 == 0 && !a->sample_rows && a->stride * s_box <= 256;
+      if (p.a_box) {
+        if ((rc = tensor_map_patch(a->act, a->batch, a->in_h, a->in_w, a->in_c, a->in_ld, s_box, a->stride, &ma)))
+          return rc;
+      } else if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, p.a_tile ? 128 : 1, &ma))) {
+        return rc;
+      }
     }
   }
   // gathered (non-contiguous, non-compact) A rows: split across TMA gather4 and cp.async

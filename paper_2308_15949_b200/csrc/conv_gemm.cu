@@ -307,6 +307,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+    } else if (p.a_box) {
+      // S x S patches: thread i < 128 / S^2 owns patch i of the tile and loads its
+      // tap window as one 4D box (S^2 rows x 64 channels, OOB -> zero halo)
+      const int s2 = p.patch_h * p.patch_w;
+      const int ppt = BM / s2;  // patches per tile
+      const int cpi = p.cells_h * p.cells_w;
+      for (int t = t_begin; t < tiles; t += t_step) {
+        const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
+        if (ti.skip) continue;
+        int bn_ = p.batch, by = 0, bx = 0;  // invalid patch -> image index past the end (zeros)
+        const int pi = ti.m0 / s2 + tid;
+        if (tid < ppt && pi * s2 < nvalid) {
+          const int cell = __ldg(p.list + pi);
+          bn_ = cell / cpi;
+          const int cr = cell - bn_ * cpi;
+          const int ci = cr / p.cells_w, cj = cr - (cr / p.cells_w) * p.cells_w;
+          by = ci * p.patch_h * p.stride - p.pad;
+          bx = cj * p.patch_w * p.stride - p.pad;
+        }
+        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (trc && tid == 0 && it < 4096) trc[TRACE_A + it] = global_ns();
+          const int tap = kb / ti.kpt;
+          const int c0 = ti.c_lo + (kb - tap * ti.kpt) * BK;
+          const int ky = tap / p.ksize;
+          const int kx = tap - ky * p.ksize;
+          const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
+          if (tid == 0) mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES);
+          if (tid < ppt) tma_load_4d(sA + tid * s2 * 128, &tmap_a, &full[stage], c0, bx + kx, by + ky, bn_);
+        }
+      }
     } else if (p.a_tma) {
       // One output row per thread; per (tap, channel block) every 4th lane issues
       // a TMA tile::gather4 of its 4 rows' source pixels (OOB index -> zeros).

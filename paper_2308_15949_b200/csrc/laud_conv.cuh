@@ -36,6 +36,7 @@ struct ConvParams {
   int a_tma;             // 1: A rows gathered with TMA tile::gather4 (else cp.async)
   int a_tile;            // 1: the 128 A rows of a tile are contiguous: one 2D TMA box
   int a_hybrid;          // 1: gathered rows split between TMA gather4 and cp.async
+  int a_box;             // 1: S x S patch rows loaded as one 4D TMA box per patch and tap
   int a_rows;            // rows of the A tensor map (also the out-of-bounds marker)
   int ksize, stride, pad;
   int kpad;              // in_c rounded up to 64 (+64 for grouped convs)

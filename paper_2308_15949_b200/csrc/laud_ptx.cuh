@@ -82,6 +82,13 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* desc, uint
       " [%0], [%1, {%2, %3, %4}], [%5];"
       ::"r"(dst), "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* desc, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(dst), "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
+}
 // Row gather: 4 arbitrary rows (r0..r3) x box-width columns starting at column c0,
 // landing as 4 consecutive box rows at dst.  Rows outside the tensor read as zero.
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const void* desc, uint64_t* bar, int c0,

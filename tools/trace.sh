@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-for m in 4096 20000 1000000; do LAUD_MASKER_FUSED_MAX=$m timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines > gpurun_out/bench_m$m.log 2>&1; done
-LAUD_MASKER_FUSED_MAX=1000000 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "masker" > gpurun_out/pytest_m.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+LAUD_A_BOX=3 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_box3.log 2>&1
+for b in 0 1 3; do LAUD_A_BOX=$b timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines > gpurun_out/bench_box$b.log 2>&1; done
+LAUD_A_BOX=0 python tools/profile_step.py resnet101 spatial 256 > gpurun_out/prof_box0.log 2>&1
+LAUD_A_BOX=3 python tools/profile_step.py resnet101 spatial 256 > gpurun_out/prof_box3.log 2>&1
