@@ -31,6 +31,8 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
                                   float* dn);
 cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,
                                   void* scan, cudaStream_t stream);
+cudaError_t launch_masker_decide(const float* cell_sums, int total, int win, float bias, uint8_t* coarse,
+                                 int* list, int* count, void* scan, cudaStream_t stream);
 cudaError_t launch_dilate_pixels(const uint8_t* coarse, int n, int h, int w, int s, int stride,
                                  int cells_h, int cells_w, int radius, int* list, int* count,
                                  void* scan, cudaStream_t stream);
@@ -259,7 +261,15 @@ int pick_bn(int n_out, int k, long long rows) {
   return 256;  // measured best for every R101 conv shape (tools/sweep_cfg.sh)
 }
 
-int run_conv(const laud_conv_args* a, cudaStream_t st) {
+// fused masker dots riding on a dense 1x1 conv (ConvParams::adot_*)
+struct AdotArgs {
+  const float* w;
+  float* out;
+  int win, cells_h, cells_w;
+};
+constexpr int LAUD_ADOT_UNAVAILABLE = 99;  // internal: conv shape cannot host the masker
+
+int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = nullptr) {
   if (!a || !a->act || !a->weight || !a->out) return fail(LAUD_ERR_ARG, "null pointer in conv args");
   if (a->in_c % 8 || a->in_ld % 8 || a->in_ld < a->in_c)
     return fail(LAUD_ERR_SHAPE, "in_c (%d) and in_ld (%d) must be multiples of 8, ld >= c", a->in_c,
@@ -410,7 +420,15 @@ int run_conv(const laud_conv_args* a, cudaStream_t st) {
   const long long pair_tiles = (long long)((a->rows_max + 255) / 256) * ((a->n_out + bn - 1) / bn);
   const bool pair_ok = pair_env && bn == 256 && p.a_tile && !a->sample_rows && !a->chan_count &&
                        !a->b_batched && p.groups == 1 && pair_tiles >= num_sms() / 2;
-  const int pair = !pair_ok ? 0 : (kw >= 1024 ? 1 : (kw <= 512 && (pair_env & 2) ? 2 : 0));
+  const int pair = (!pair_ok || ad) ? 0 : (kw >= 1024 ? 1 : (kw <= 512 && (pair_env & 2) ? 2 : 0));
+  if (ad) {  // fused masker readers need single-CTA tiles with contiguous (TMA box) A rows
+    if (!p.a_tile) return LAUD_ADOT_UNAVAILABLE;
+    p.adot_w = ad->w;
+    p.adot_out = ad->out;
+    p.adot_win = ad->win;
+    p.adot_cells_h = ad->cells_h;
+    p.adot_cells_w = ad->cells_w;
+  }
   CUtensorMap m;
   if ((rc = tensor_map_2d(a->weight, a->n_out, kw, kw, pair ? bn / 2 : bn, &m, a->b_batched ? a->batch : 0)))
     return rc;
@@ -787,6 +805,15 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   if (a->paradigm == LAUD_PARADIGM_CHANNEL) return channel_forward(a, st);
   const int n = a->n;
   int rc;
+  // masker fused into a dense conv1: its A stages feed the window dots, so x is
+  // read once for both (the masker's own pass over x disappears)
+  static const int fuse_env = [] {
+    const char* e = getenv("LAUD_MASKER_IN_CONV1");
+    return e ? atoi(e) : 1;
+  }();
+  const bool fuse_masker = fuse_env && a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense &&
+                           !a->given_coarse && !a->dn && !a->fp32 && a->masker_wdiff && a->partial &&
+                           a->x_ld == a->c_in && a->c_in % 64 == 0;
 
   // ---------------------------------------------------------------- rows
   int pm;  // row mode for conv2/conv3
@@ -810,6 +837,11 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     if (a->given_coarse) {
       coarse = a->given_coarse;
       rc = laud_cells_from_mask(coarse, n * ch * cw, a->cell_list, a->cell_count, a->scan, stream);
+    } else if (fuse_masker) {
+      // decisions come from conv1's fused dots (below, before the skip path)
+      if (!a->coarse_out) return fail(LAUD_ERR_ARG, "coarse output missing");
+      coarse = a->coarse_out;
+      rc = LAUD_OK;
     } else {
       if (!a->masker_wdiff || !a->coarse_out || !a->partial)
         return fail(LAUD_ERR_ARG, "masker weights / coarse output / partials missing");
@@ -839,6 +871,57 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     pm = ROWS_DENSE;
   } else {
     return fail(LAUD_ERR_ARG, "unknown paradigm %d", a->paradigm);
+  }
+
+  // ---------------------------------------------------------------- conv1
+  laud_conv_args c1;
+  memset(&c1, 0, sizeof(c1));
+  c1.fp32 = a->fp32;
+  c1.batch = n;
+  c1.out_h = a->h_in;
+  c1.out_w = a->w_in;
+  c1.act = a->x;
+  c1.in_h = a->h_in;
+  c1.in_w = a->w_in;
+  c1.in_c = a->c_in;
+  c1.in_ld = a->x_ld;
+  c1.ksize = 1;
+  c1.stride = 1;
+  c1.weight = a->w1;
+  c1.n_out = a->c_mid;
+  c1.scale = a->s1;
+  c1.bias = a->b1;
+  c1.relu = a->relu1;
+  c1.out_mode = OUT_PIXEL;
+  c1.out = a->h1;
+  c1.out_ld = a->c_mid;
+  c1.rows_max = n * a->h_in * a->w_in;
+  bool conv1_done = false;
+  if (fuse_masker) {
+    // masker window sums accumulate in `partial` during the dense conv1, then
+    // decisions + the active-cell list (reference.py:173-183, 133-135)
+    const int win = a->s * a->stride;
+    const int total = n * ch * cw;
+    c1.row_mode = ROWS_DENSE;
+    AdotArgs ad{a->masker_wdiff, a->partial, win, ch, cw};
+    if ((rc = cuda_check(cudaMemsetAsync(a->partial, 0, (size_t)total * sizeof(float), st), "masker sums", 0)))
+      return rc;
+    rc = run_conv(&c1, st, &ad);
+    if (rc == LAUD_OK) {
+      conv1_done = true;
+      ProfScope ps(1, st);
+      if ((rc = cuda_check(launch_masker_decide(a->partial, total, win, a->masker_bias, a->coarse_out,
+                                                a->cell_list, a->cell_count, a->scan, st),
+                           "masker decide", 1)))
+        return rc;
+    } else if (rc == LAUD_ADOT_UNAVAILABLE) {  // this geometry cannot host it: standalone masker
+      if ((rc = laud_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in, a->s, a->stride,
+                                    a->masker_wdiff, a->masker_bias, a->coarse_out, a->cell_list,
+                                    a->cell_count, a->partial, a->scan, stream)))
+        return rc;
+    } else {
+      return rc;
+    }
   }
 
   // ---------------------------------------------------------------- skip path
@@ -886,30 +969,9 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
       return rc;
   }
 
-  // ---------------------------------------------------------------- conv1
-  laud_conv_args c1;
-  memset(&c1, 0, sizeof(c1));
-  c1.fp32 = a->fp32;
-  c1.batch = n;
-  c1.out_h = a->h_in;
-  c1.out_w = a->w_in;
-  c1.act = a->x;
-  c1.in_h = a->h_in;
-  c1.in_w = a->w_in;
-  c1.in_c = a->c_in;
-  c1.in_ld = a->x_ld;
-  c1.ksize = 1;
-  c1.stride = 1;
-  c1.weight = a->w1;
-  c1.n_out = a->c_mid;
-  c1.scale = a->s1;
-  c1.bias = a->b1;
-  c1.relu = a->relu1;
-  c1.out_mode = OUT_PIXEL;
-  c1.out = a->h1;
-  c1.out_ld = a->c_mid;
-  c1.rows_max = n * a->h_in * a->w_in;
-  if (pm == ROWS_DENSE || (a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense)) {
+  // ---------------------------------------------------------------- conv1 (unfused)
+  if (conv1_done) {
+  } else if (pm == ROWS_DENSE || (a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense)) {
     c1.row_mode = ROWS_DENSE;
   } else if (a->paradigm == LAUD_PARADIGM_LAYER) {
     c1.row_mode = ROWS_PATCH;  // whole images of the active samples
@@ -928,7 +990,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     c1.list = a->pix_list;
     c1.count = a->pix_count;
   }
-  if ((rc = run_conv(&c1, st))) return rc;
+  if (!conv1_done && (rc = run_conv(&c1, st))) return rc;
 
   // ---------------------------------------------------------------- conv2 (3x3 over patches)
   laud_conv_args c2;

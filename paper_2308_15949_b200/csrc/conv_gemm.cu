@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       // arrivals: A expect_tx (TMA) or 128 cp.async threads, hybrid both halves, + B
       mbar_init(&full[s], p.a_hybrid ? 1 + 64 + 1 : (p.a_tma ? 2 : 128 + 1));
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], p.adot_out ? 2 : 1);  // + the fused masker readers
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
@@ -217,7 +217,61 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ A producers
     const int tid = threadIdx.x;
     uint32_t it = 0;
-    if (p.a_tile) {
+    if (p.a_tile && p.adot_out && warp >= 1) {
+      // fused masker readers (warps 1-3): every A stage, once landed, is also
+      // read here — dot of each row with the masker weights W0 - W1
+      // (`reference.py:244-253`) — and released with a second arrive
+      const int mt = tid - 32;  // 0 .. 95: rows mt and mt + 96 (< 128)
+      const int ra = mt, rb = mt + 96;
+      for (int t = t_begin; t < tiles; t += t_step) {
+        const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
+        if (ti.skip) continue;
+        float acc_a = 0.f, acc_b = 0.f;
+        const bool dots = ti.n0 == 0;  // every N tile re-reads the rows: dot them once
+        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&full[stage], phase);
+          const uint8_t* sA = base + L::A_OFF + stage * A_STAGE_BYTES;
+          if (dots) {
+          const float* wv = p.adot_w + kb * BK;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(wv + c * 8));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(wv + c * 8 + 4));
+            const uint4 va = *reinterpret_cast<const uint4*>(sA + ra * 128 + ((c ^ (ra & 7)) << 4));
+            float2 f;
+            f = unpack_bf16x2(va.x); acc_a = fmaf(f.x, w0.x, acc_a); acc_a = fmaf(f.y, w0.y, acc_a);
+            f = unpack_bf16x2(va.y); acc_a = fmaf(f.x, w0.z, acc_a); acc_a = fmaf(f.y, w0.w, acc_a);
+            f = unpack_bf16x2(va.z); acc_a = fmaf(f.x, w1.x, acc_a); acc_a = fmaf(f.y, w1.y, acc_a);
+            f = unpack_bf16x2(va.w); acc_a = fmaf(f.x, w1.z, acc_a); acc_a = fmaf(f.y, w1.w, acc_a);
+            if (rb < BM) {
+              const uint4 vb = *reinterpret_cast<const uint4*>(sA + rb * 128 + ((c ^ (rb & 7)) << 4));
+              f = unpack_bf16x2(vb.x); acc_b = fmaf(f.x, w0.x, acc_b); acc_b = fmaf(f.y, w0.y, acc_b);
+              f = unpack_bf16x2(vb.y); acc_b = fmaf(f.x, w0.z, acc_b); acc_b = fmaf(f.y, w0.w, acc_b);
+              f = unpack_bf16x2(vb.z); acc_b = fmaf(f.x, w1.x, acc_b); acc_b = fmaf(f.y, w1.y, acc_b);
+              f = unpack_bf16x2(vb.w); acc_b = fmaf(f.x, w1.z, acc_b); acc_b = fmaf(f.y, w1.w, acc_b);
+            }
+          }
+          }
+          asm volatile("bar.sync 3, 96;" ::: "memory");
+          if (mt == 0) mbar_arrive(&empty[stage]);
+        }
+        // rows -> pixels of the dense input grid -> masker cells
+        const int hw = p.out_h * p.out_w;
+        auto add = [&](int r, float v) {
+          const int m = ti.m0 + r;
+          if (m >= nvalid) return;
+          const int n = m / hw, rem = m - n * hw;
+          const int y = rem / p.out_w, x = rem - (rem / p.out_w) * p.out_w;
+          atomicAdd(p.adot_out + (n * p.adot_cells_h + y / p.adot_win) * p.adot_cells_w + x / p.adot_win, v);
+        };
+        if (dots) {
+          add(ra, acc_a);
+          if (rb < BM) add(rb, acc_b);
+        }
+      }
+    } else if (p.a_tile) {
       // Contiguous rows (compact / dense 1x1): one 128 x 64 TMA box per stage.
       if (tid == 0) {
         for (int t = t_begin; t < tiles; t += t_step) {

@@ -603,6 +603,14 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
   return launch_compact(f, total, list, count, scan, stream);
 }
 
+// Decisions + active-cell list from per-cell window sums accumulated elsewhere
+// (conv1's fused masker dots): d = sum / win^2 + bias >= 0.
+cudaError_t launch_masker_decide(const float* cell_sums, int total, int win, float bias, uint8_t* coarse,
+                                 int* list, int* count, void* scan, cudaStream_t stream) {
+  MaskerFlag f{cell_sums, 1, 1.0f / (float)(win * win), bias, coarse};
+  return launch_compact(f, total, list, count, scan, stream);
+}
+
 cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,
                                   void* scan, cudaStream_t stream) {
   GivenFlag f{coarse};

@@ -206,7 +206,7 @@ class DeviceBlock:
     def set_masker(self, masker_w, bias: float = 0.0):
         """Store W0 - W1 (fused-masker identity, `reference.py:244-253`)."""
         mw = np.asarray(masker_w, dtype=np.float64).reshape(2, -1)
-        wd = np.zeros(self.cin_p, dtype=np.float32)
+        wd = np.zeros(kpad(self.cin_p), dtype=np.float32)  # zero tail: read per 64-channel block
         wd[: mw.shape[1]] = (mw[0] - mw[1]).astype(np.float32)
         self.wdiff = torch.from_numpy(wd).to(self.w1.device)
         self.masker_bias = float(bias)

@@ -403,3 +403,31 @@ def test_regnet_se_block_matches_oracle_ext(stage, index, paradigm):
     no_se = O.block_forward_sparse(x, obw, blk, cfg, om, epilogues=O.Epilogues(
         b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"], relu_out=True), emulate_bf16=True)
     assert _rel(yg, no_se) > 1e-2  # the gate is really applied
+
+
+@pytest.mark.parametrize("stage,index,s", [(3, 1, 2), (2, 0, 2), (4, 1, 1), (4, 0, 1)])
+def test_masker_fused_into_conv1_decides_like_standalone(stage, index, s):
+    """The masker dots accumulated from conv1's A stages (dense conv1, incl. blocks
+    whose conv1 has several N tiles) decide exactly like the standalone masker,
+    with a non-zero calibration bias."""
+    import torch
+    from paper_2308_15949_b200 import device as D
+    from paper_2308_15949_b200.network import make_params
+    _R()
+    bp = [b for b in make_params("resnet101", 0)["blocks"] if b["stage"] == stage and b["index"] == index][0]
+    blk = bp["block"]
+    ep = D.Epilogue(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"], relu2=True,
+                    s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"], relu_out=True)
+    db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep, masker_w=bp["masker_w"],
+                       masker_bias=0.37, fold_scale=True)
+    n, h = 16, blk.input_shape.height
+    x = torch.randn(n, h, h, db.cin_p, device="cuda").relu_().bfloat16()
+    o = blk.output_shape
+    nc = n * (o.height // s) * (o.width // s)
+    got = []
+    for dense in (False, True):
+        _, coarse, _, _ = db.forward(x.clone(), "spatial", s, ws=D.Workspace(), conv1_dense=dense)
+        torch.cuda.synchronize()
+        got.append(coarse[:nc].cpu().numpy().copy())
+    assert 0.0 < got[0].mean() < 1.0
+    assert np.mean(got[0] == got[1]) > 0.999
