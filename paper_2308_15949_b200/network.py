@@ -17,6 +17,7 @@ the role a trained masker's FLOPs loss plays in the paper.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -143,7 +144,8 @@ class LaudNetwork:
             # conv1 schedule: the dilated pixel set covers most of the input for
             # S <= 2 at ratio >= 0.4 (r_dil ~0.9 at r = 0.5), where the dense
             # conv1 (contiguous TMA rows, no dilation pass) is cheaper
-            db.conv1_dense = para is Paradigm.SPATIAL and s <= 2 and target_ratio >= 0.4
+            db.conv1_dense = para is Paradigm.SPATIAL and (
+                s <= 2 and target_ratio >= 0.4 or os.environ.get("LAUD_CONV1_DENSE_ALL", "1") == "1")
             self.slots.append(BlockSlot(bp["stage"], bp["index"], db, s))
         fc_in = net.classifier_features
         self.fc_w = D.pack_weight(params["fc_w"][:, :, None, None], D.pad8(fc_in), device)
