@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = t_begin; t < tiles; t += t_step) {
         const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
         if (ti.skip) continue;
-        float acc_a = 0.f, acc_b = 0.f;
+        float aa[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};  // 4-way ILP per row
         const bool dots = ti.n0 == 0;  // every N tile re-reads the rows: dot them once
         for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
           const int stage = it % STAGES;
@@ -234,29 +234,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&full[stage], phase);
           const uint8_t* sA = base + L::A_OFF + stage * A_STAGE_BYTES;
           if (dots) {
-          const float* wv = p.adot_w + kb * BK;
+            const float* wv = p.adot_w + kb * BK;
+            uint4 va[8], vb[8];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 w0 = __ldg(reinterpret_cast<const float4*>(wv + c * 8));
-            const float4 w1 = __ldg(reinterpret_cast<const float4*>(wv + c * 8 + 4));
-            const uint4 va = *reinterpret_cast<const uint4*>(sA + ra * 128 + ((c ^ (ra & 7)) << 4));
-            float2 f;
-            f = unpack_bf16x2(va.x); acc_a = fmaf(f.x, w0.x, acc_a); acc_a = fmaf(f.y, w0.y, acc_a);
-            f = unpack_bf16x2(va.y); acc_a = fmaf(f.x, w0.z, acc_a); acc_a = fmaf(f.y, w0.w, acc_a);
-            f = unpack_bf16x2(va.z); acc_a = fmaf(f.x, w1.x, acc_a); acc_a = fmaf(f.y, w1.y, acc_a);
-            f = unpack_bf16x2(va.w); acc_a = fmaf(f.x, w1.z, acc_a); acc_a = fmaf(f.y, w1.w, acc_a);
-            if (rb < BM) {
-              const uint4 vb = *reinterpret_cast<const uint4*>(sA + rb * 128 + ((c ^ (rb & 7)) << 4));
-              f = unpack_bf16x2(vb.x); acc_b = fmaf(f.x, w0.x, acc_b); acc_b = fmaf(f.y, w0.y, acc_b);
-              f = unpack_bf16x2(vb.y); acc_b = fmaf(f.x, w0.z, acc_b); acc_b = fmaf(f.y, w0.w, acc_b);
-              f = unpack_bf16x2(vb.z); acc_b = fmaf(f.x, w1.x, acc_b); acc_b = fmaf(f.y, w1.y, acc_b);
-              f = unpack_bf16x2(vb.w); acc_b = fmaf(f.x, w1.z, acc_b); acc_b = fmaf(f.y, w1.w, acc_b);
+            for (int c = 0; c < 8; ++c) {
+              va[c] = *reinterpret_cast<const uint4*>(sA + ra * 128 + ((c ^ (ra & 7)) << 4));
+              vb[c] = rb < BM ? *reinterpret_cast<const uint4*>(sA + rb * 128 + ((c ^ (rb & 7)) << 4))
+                              : make_uint4(0u, 0u, 0u, 0u);
             }
-          }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 w0 = __ldg(reinterpret_cast<const float4*>(wv + c * 8));
+              const float4 w1 = __ldg(reinterpret_cast<const float4*>(wv + c * 8 + 4));
+              const int k = c & 3;
+              float2 f;
+              f = unpack_bf16x2(va[c].x); aa[k] = fmaf(f.x, w0.x, aa[k]); aa[k] = fmaf(f.y, w0.y, aa[k]);
+              f = unpack_bf16x2(va[c].y); aa[k] = fmaf(f.x, w0.z, aa[k]); aa[k] = fmaf(f.y, w0.w, aa[k]);
+              f = unpack_bf16x2(va[c].z); aa[k] = fmaf(f.x, w1.x, aa[k]); aa[k] = fmaf(f.y, w1.y, aa[k]);
+              f = unpack_bf16x2(va[c].w); aa[k] = fmaf(f.x, w1.z, aa[k]); aa[k] = fmaf(f.y, w1.w, aa[k]);
+              f = unpack_bf16x2(vb[c].x); ab[k] = fmaf(f.x, w0.x, ab[k]); ab[k] = fmaf(f.y, w0.y, ab[k]);
+              f = unpack_bf16x2(vb[c].y); ab[k] = fmaf(f.x, w0.z, ab[k]); ab[k] = fmaf(f.y, w0.w, ab[k]);
+              f = unpack_bf16x2(vb[c].z); ab[k] = fmaf(f.x, w1.x, ab[k]); ab[k] = fmaf(f.y, w1.y, ab[k]);
+              f = unpack_bf16x2(vb[c].w); ab[k] = fmaf(f.x, w1.z, ab[k]); ab[k] = fmaf(f.y, w1.w, ab[k]);
+            }
           }
           asm volatile("bar.sync 3, 96;" ::: "memory");
           if (mt == 0) mbar_arrive(&empty[stage]);
         }
+        const float acc_a = (aa[0] + aa[1]) + (aa[2] + aa[3]);
+        const float acc_b = (ab[0] + ab[1]) + (ab[2] + ab[3]);
         // rows -> pixels of the dense input grid -> masker cells
         const int hw = p.out_h * p.out_w;
         auto add = [&](int r, float v) {

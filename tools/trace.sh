@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-LAUD_CONV1_DENSE_ALL=0 timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines > gpurun_out/bench_d0.log 2>&1
-LAUD_CONV1_DENSE_ALL=1 timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines > gpurun_out/bench_d1.log 2>&1
-LAUD_CONV1_DENSE_ALL=1 timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines --arch resnet50 --plan 4-4-2-1 --batch 128 > gpurun_out/bench_r50_d1.log 2>&1
-LAUD_CONV1_DENSE_ALL=0 timeout 600 python bench.py --steps 20 --warmup 5 --no-baselines --arch resnet50 --plan 4-4-2-1 --batch 128 > gpurun_out/bench_r50_d0.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_network.py -x -q > gpurun_out/pytest_gpu.log 2>&1
+for cfg in "LAUD_MASKER_IN_CONV1=0" "LAUD_MASKER_IN_CONV1=0 LAUD_PAIR=0" "LAUD_MASKER_IN_CONV1=1"; do echo "== $cfg"; env $cfg python tools/profile_step.py resnet101 spatial 256 | python -c "
+import sys, json
+rows=[json.loads(l) for l in sys.stdin if l.startswith('{')]
+print('conv1s3', round(sum(r['us'] for r in rows if r['tag']==0 and r['n_out']==256 and r['k']==1024)), 'masker', round(sum(r['us'] for r in rows if r['tag']==1)), 'total', round(sum(r['us'] for r in rows)))
+"; done > gpurun_out/iso.log 2>&1
