@@ -1,0 +1,38 @@
+"""Small spatial / channel / layer / static block forwards for compute-sanitizer
+(memcheck, racecheck, synccheck): python tools/sanitize_block.py"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2308_15949_b200 import device as D
+from paper_2308_15949_b200.network import make_params
+
+
+def main():
+    torch.cuda.set_device(0)
+    for arch, stage, index, s in (("resnet50", 3, 1, 2), ("resnet50", 2, 0, 2), ("resnet50", 1, 1, 4),
+                                  ("regnety-1.6gf", 3, 1, 2)):
+        bp = [b for b in make_params(arch, 0)["blocks"] if b["stage"] == stage and b["index"] == index][0]
+        blk = bp["block"]
+        ep = D.Epilogue(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"], relu2=True,
+                        s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"], relu_out=True)
+        db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep, masker_w=bp["masker_w"],
+                           fold_scale=True)
+        if "se_w1" in bp:
+            db.set_se(bp["se_w1"], bp["se_b1"], bp["se_w2"], bp["se_b2"])
+        n, h = 2, blk.input_shape.height
+        x = torch.randn(n, h, h, db.cin_p, device="cuda").relu_().bfloat16()
+        for dense in (False, True):
+            db.forward(x.clone(), "spatial", s, conv1_dense=dense)
+        db.forward(x.clone(), "static")
+        db.forward(x.clone(), "layer", coarse=torch.tensor([1, 0], dtype=torch.uint8, device="cuda"))
+        if blk.conv2.groups == 1:
+            cm = torch.zeros(n * db.cmid_p, dtype=torch.uint8, device="cuda")
+            cm[: blk.conv2.out_channels // 2] = 1
+            db.forward(x.clone(), "channel", chmask=cm)
+        torch.cuda.synchronize()
+        print("ok", arch, stage, index, flush=True)
+
+
+if __name__ == "__main__":
+    main()
