@@ -221,6 +221,10 @@ typedef struct laud_block_args {
   const float* se_w2;
   const float* se_b2;
   int se_hidden;
+  /* spatial masker fused into a dense conv1 (conv1_dense, masker computed):
+   * per-cell window sums [n * cells], zero on entry and left zero (the decision
+   * pass clears what it reads); NULL = standalone masker pass. */
+  float* cell_sums;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

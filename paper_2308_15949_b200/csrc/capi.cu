@@ -812,7 +812,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     return e ? atoi(e) : 1;
   }();
   const bool fuse_masker = fuse_env && a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense &&
-                           !a->given_coarse && !a->dn && !a->fp32 && a->masker_wdiff && a->partial &&
+                           !a->given_coarse && !a->dn && !a->fp32 && a->masker_wdiff && a->cell_sums &&
                            a->x_ld == a->c_in && a->c_in % 64 == 0;
 
   // ---------------------------------------------------------------- rows
@@ -903,14 +903,14 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     const int win = a->s * a->stride;
     const int total = n * ch * cw;
     c1.row_mode = ROWS_DENSE;
-    AdotArgs ad{a->masker_wdiff, a->partial, win, ch, cw};
-    if ((rc = cuda_check(cudaMemsetAsync(a->partial, 0, (size_t)total * sizeof(float), st), "masker sums", 0)))
-      return rc;
+    AdotArgs ad{a->masker_wdiff, a->cell_sums, win, ch, cw};
+    // `cell_sums` is zero here: allocated zeroed, and the decision pass below
+    // clears every sum it reads (MaskerFlag)
     rc = run_conv(&c1, st, &ad);
     if (rc == LAUD_OK) {
       conv1_done = true;
       ProfScope ps(1, st);
-      if ((rc = cuda_check(launch_masker_decide(a->partial, total, win, a->masker_bias, a->coarse_out,
+      if ((rc = cuda_check(launch_masker_decide(a->cell_sums, total, win, a->masker_bias, a->coarse_out,
                                                 a->cell_list, a->cell_count, a->scan, st),
                            "masker decide", 1)))
         return rc;

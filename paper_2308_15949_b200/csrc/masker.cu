@@ -173,9 +173,16 @@ struct MaskerFlag {  // decision from split partials; also materialises coarse
   int splits;
   float inv_area, bias;
   uint8_t* coarse;
+  bool clear;  // zero the sums after reading (conv1-fused cell_sums only)
   __device__ bool operator()(int i) const {
     float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += partial[(size_t)i * splits + k];
+    for (int k = 0; k < splits; ++k) {
+      s += partial[(size_t)i * splits + k];
+      // leave cell_sums zeroed: the next block's conv1-fused masker accumulates
+      // into it without a memset (each item is read exactly once).  Standalone
+      // masker partials stay intact (calibration reads them back).
+      if (clear) const_cast<float*>(partial)[(size_t)i * splits + k] = 0.f;
+    }
     const bool f = s * inv_area + bias >= 0.f;
     if (coarse) coarse[i] = f ? 1 : 0;
     return f;
@@ -599,7 +606,7 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
         splits, cps, partial, prev_coarse, dn);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse};
+  MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse, false};
   return launch_compact(f, total, list, count, scan, stream);
 }
 
@@ -607,7 +614,7 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
 // (conv1's fused masker dots): d = sum / win^2 + bias >= 0.
 cudaError_t launch_masker_decide(const float* cell_sums, int total, int win, float bias, uint8_t* coarse,
                                  int* list, int* count, void* scan, cudaStream_t stream) {
-  MaskerFlag f{cell_sums, 1, 1.0f / (float)(win * win), bias, coarse};
+  MaskerFlag f{cell_sums, 1, 1.0f / (float)(win * win), bias, coarse, true};
   return launch_compact(f, total, list, count, scan, stream);
 }
 

@@ -306,6 +306,7 @@ class DeviceBlock:
             ss = s if paradigm == "spatial" else ho
             partial_n = max(1, lib.laud_masker_partial_floats(n, h, w, self.cin_p, ss, blk.stride))
         partial = ws.get("partial", partial_n * 4)
+        cell_sums = ws.get("cell_sums", cells * 4, zero=True)  # zero-invariant (laud.h)
         scan = ws.get("scan", lib.laud_scan_workspace_bytes(max(pix, cells)), zero=True)
         v = self.vec
         a = _lib.BlockArgs(
@@ -325,7 +326,8 @@ class DeviceBlock:
             se_w1=ptr(self.se[0]) if self.se else None, se_b1=ptr(self.se[1]) if self.se else None,
             se_w2=ptr(self.se[2]) if self.se else None, se_b2=ptr(self.se[3]) if self.se else None,
             se_hidden=self.se[4] if self.se else 0,
-            conv1_dense=int(self.conv1_dense if conv1_dense is None else conv1_dense))
+            conv1_dense=int(self.conv1_dense if conv1_dense is None else conv1_dense),
+            cell_sums=ptr(cell_sums))
         if paradigm == "channel":
             self._channel_args(a, n, ws, chmask)
         if dn is not None and paradigm == "spatial":
