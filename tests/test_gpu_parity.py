@@ -405,11 +405,14 @@ def test_regnet_se_block_matches_oracle_ext(stage, index, paradigm):
     assert _rel(yg, no_se) > 1e-2  # the gate is really applied
 
 
-@pytest.mark.parametrize("stage,index,s", [(3, 1, 2), (2, 0, 2), (4, 1, 1), (4, 0, 1)])
-def test_masker_fused_into_conv1_decides_like_standalone(stage, index, s):
+@pytest.mark.parametrize("stage,index,s,n", [(3, 1, 2, 16), (2, 0, 2, 16), (4, 1, 1, 16), (4, 0, 1, 16),
+                                             (3, 1, 2, 128)])
+def test_masker_fused_into_conv1_decides_like_standalone(stage, index, s, n):
     """The masker dots accumulated from conv1's A stages (dense conv1, incl. blocks
-    whose conv1 has several N tiles) decide exactly like the standalone masker,
-    with a non-zero calibration bias."""
+    whose conv1 has several N tiles; n = 128 at stage 3 runs conv1 on CTA pairs,
+    whose readers relay A completion to the leader) decide exactly like the
+    standalone masker, with a non-zero calibration bias, and the block outputs
+    agree bit for bit where the decisions do."""
     import torch
     from paper_2308_15949_b200 import device as D
     from paper_2308_15949_b200.network import make_params
@@ -420,14 +423,17 @@ def test_masker_fused_into_conv1_decides_like_standalone(stage, index, s):
                     s3=bp["s3"], b3=bp["b3"], sd=bp["sd"], bd=bp["bd"], relu_out=True)
     db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], bp["wd"], ep, masker_w=bp["masker_w"],
                        masker_bias=0.37, fold_scale=True)
-    n, h = 16, blk.input_shape.height
+    h = blk.input_shape.height
     x = torch.randn(n, h, h, db.cin_p, device="cuda").relu_().bfloat16()
     o = blk.output_shape
     nc = n * (o.height // s) * (o.width // s)
-    got = []
+    got, ys = [], []
     for dense in (False, True):
-        _, coarse, _, _ = db.forward(x.clone(), "spatial", s, ws=D.Workspace(), conv1_dense=dense)
+        y, coarse, _, _ = db.forward(x.clone(), "spatial", s, ws=D.Workspace(), conv1_dense=dense)
         torch.cuda.synchronize()
         got.append(coarse[:nc].cpu().numpy().copy())
+        ys.append(y.float().cpu())
     assert 0.0 < got[0].mean() < 1.0
     assert np.mean(got[0] == got[1]) > 0.999
+    if (got[0] == got[1]).all():
+        assert torch.equal(ys[0], ys[1])
