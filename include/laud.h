@@ -225,6 +225,13 @@ typedef struct laud_block_args {
    * per-cell window sums [n * cells], zero on entry and left zero (the decision
    * pass clears what it reads); NULL = standalone masker pass. */
   float* cell_sums;
+  /* EXT channel skipping over a grouped conv2 (RegNet; the reference's sparse
+   * executor rejects groups != 1, reference.py:405-406): w2 holds the grouped
+   * kernel expanded block-diagonally to a dense [c_mid][9][kpad] kernel, so
+   * W2[sel][:, sel] keeps each group's kept links — the sparse form of the
+   * reference's dense-masked channel forward (reference.py:331-339).  0 = the
+   * reference behaviour (LAUD_ERR_UNSUPPORTED). */
+  int ch_dense_w2;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

@@ -18,7 +18,9 @@ Layout follows the reference: NCHW float64, masks as bool arrays.  Every
 function cites the reference lines it restates.  Extensions the reference
 lacks (flagged EXT) are compositions the GPU path needs a checker for:
 bf16 rounding emulation, folded-BN/ReLU epilogues (default off = reference
-semantics), masker->block wiring on the output grid, and a network composer.
+semantics), masker->block wiring on the output grid, a network composer, and
+sparse channel skipping over grouped conv2 (pinned to the reference's own
+dense-masked outputs, tests/golden/grouped_channel.npz).
 """
 
 from __future__ import annotations
@@ -456,10 +458,22 @@ def _spatial_sparse(x, bw, block, mask, ep, rnd, misplace_first):
     return result
 
 
+def grouped_to_dense(w: np.ndarray, groups: int) -> np.ndarray:
+    """EXT: [C_out, C_in/g, k, k] grouped kernel -> [C_out, C_in, k, k] block-diagonal
+    dense kernel (zeros between groups; group layout of `reference.py:43-49`)."""
+    co, cig, kh, kw = w.shape
+    cog = co // groups
+    out = np.zeros((co, cig * groups, kh, kw), dtype=w.dtype)
+    for g in range(groups):
+        out[g * cog:(g + 1) * cog, g * cig:(g + 1) * cig] = w[g * cog:(g + 1) * cog]
+    return out
+
+
 def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConfig, mask,
                          _misplace_first_patch: bool = False,
                          epilogues: Optional[Epilogues] = None,
-                         emulate_bf16: bool = False) -> np.ndarray:
+                         emulate_bf16: bool = False,
+                         grouped_channel_ext: bool = False) -> np.ndarray:
     """Inference-style forward computing only what the mask selects.
 
     Restates `reference.py:356-436`.  ``epilogues`` (EXT) adds folded
@@ -479,8 +493,15 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
         r = _spatial_sparse(x, bw, block, mask, epilogues, rnd, _misplace_first_patch)
         return rnd(r) if rnd else r
     if p is Paradigm.CHANNEL:
+        w2 = bw.w2
         if block.conv2.groups != 1:
-            raise ShapeMismatch("sparse channel execution requires groups == 1")
+            if not grouped_channel_ext:
+                raise ShapeMismatch("sparse channel execution requires groups == 1")
+            # EXT: the grouped conv2 as its block-diagonal dense kernel; W2[sel][:, sel]
+            # then keeps exactly the kept-input x kept-output links of each group, the
+            # sparse form of the reference's dense-masked channel forward
+            # (`reference.py:331-339`, which masks conv2's input and output)
+            w2 = grouped_to_dense(w2, block.conv2.groups)
         m = mask.expanded
         if m.shape != (n, block.conv2.out_channels):
             raise MaskShapeMismatch(f"channel mask {m.shape} != {(n, block.conv2.out_channels)}")
@@ -489,6 +510,11 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
         for ni in range(n):
             sel = np.flatnonzero(m[ni])
             if sel.size == 0:
+                # `reference.py:415-416` skips the sample; with the EXT epilogue the
+                # dense-masked conv path still contributes conv3's bias (conv3 of
+                # an all-zero input is 0, + b3), which is what the device computes
+                if ep is not None and ep.b3 is not None:
+                    result[ni] += ep.b3.reshape(-1, 1, 1)
                 continue
             xi = x[ni:ni + 1]
             h1 = conv_raw(xi, bw.w1[sel])
@@ -497,13 +523,22 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
                              None if ep.b1 is None else ep.b1[sel], ep.relu1)
             if rnd:
                 h1 = rnd(h1)
-            h2 = conv_raw(h1, bw.w2[np.ix_(sel, sel)], stride=block.conv2.stride,
+            h2 = conv_raw(h1, w2[np.ix_(sel, sel)], stride=block.conv2.stride,
                           pad=block.conv2.kernel // 2)
             if ep is not None:
                 h2 = _affine(h2, None if ep.s2 is None else ep.s2[sel],
                              None if ep.b2 is None else ep.b2[sel], ep.relu2)
             if rnd:
                 h2 = rnd(h2)
+            if ep is not None and ep.se_w1 is not None:
+                # EXT SE under channel skipping: the dense-masked h2 is zero on the
+                # dropped channels, so the pooled vector is the kept channels' means
+                # scattered into C_m zeros; the gate multiplies the kept channels
+                pooled = np.zeros(block.conv2.out_channels)
+                pooled[sel] = h2[0].mean(axis=(1, 2))
+                h2 = h2 * _se_scale(pooled, ep)[sel].reshape(1, -1, 1, 1)
+                if rnd:
+                    h2 = rnd(h2)
             h3 = conv_raw(h2, bw.w3[:, sel])
             if ep is not None:
                 h3 = _affine(h3, ep.s3, ep.b3, False)
@@ -827,6 +862,7 @@ def network_forward(params: dict, images_u8: np.ndarray, paradigm: str = "spatia
                 mask = block_spatial_mask(x, bp["masker_w"], blk, s, bias)
         if record is not None:
             record.append(mask)
-        x = block_forward_sparse(x, bw, blk, cfg, mask, epilogues=ep, emulate_bf16=emulate_bf16)
+        x = block_forward_sparse(x, bw, blk, cfg, mask, epilogues=ep, emulate_bf16=emulate_bf16,
+                                 grouped_channel_ext=True)
     feat = rnd(x.mean(axis=(2, 3)))
     return feat @ rnd(params["fc_w"]).T + params["fc_b"]

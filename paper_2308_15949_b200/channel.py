@@ -126,18 +126,24 @@ def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None):
     return R.ChannelMask(cz, np.repeat(cz, g, axis=1), g, soft)
 
 
-def channel_block_sparse(x, bw, block, mask):
-    """Channel-skipping block forward on the device (`reference.py:404-423`)."""
+def channel_block_sparse(x, bw, block, mask, grouped_channel_ext: bool = False):
+    """Channel-skipping block forward on the device (`reference.py:404-423`).
+
+    ``grouped_channel_ext`` (EXT) lifts the reference's groups == 1 requirement
+    (`reference.py:405-406`): a grouped conv2 runs as its block-diagonal dense
+    kernel, the sparse form of the reference's dense-masked channel forward."""
     import numpy as np
     from .errors import MaskShapeMismatch, ShapeMismatch
     R = _rm()
-    if block.conv2.groups != 1:
+    if block.conv2.groups != 1 and not grouped_channel_ext:
         raise ShapeMismatch("sparse channel execution requires groups == 1")
     n = x.shape[0]
     m = np.asarray(mask.expanded)
     if m.shape != (n, block.conv2.out_channels):
         raise MaskShapeMismatch(f"channel mask {m.shape} != {(n, block.conv2.out_channels)}")
     db = R.device_block(bw, block)
+    if block.conv2.groups != 1:
+        db.enable_grouped_channel()
     mm = np.zeros((n, db.cmid_p), np.uint8)
     mm[:, : m.shape[1]] = m
     xd = D.to_device_nhwc(x, dtype=db.dtype)

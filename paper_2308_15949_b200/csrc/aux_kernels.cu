@@ -307,6 +307,96 @@ cudaError_t launch_se(void* h2, int n, int c, const int* list, const int* count,
   return cudaGetLastError();
 }
 
+// SE under channel skipping (EXT): sample n's conv2 rows are [n*sr, n*sr + hw) (sr = hw: compact),
+// column j < count[n] holds kept channel sel[n*c + j] (the dynamic-width
+// layout of the channel executor); dropped channels pool to zero, the gate
+// multiplies the kept columns.
+__global__ void __launch_bounds__(256) se_pool_ch_kernel(const __nv_bfloat16* __restrict__ h2, int c, int hw,
+                                                         int sr, const int* __restrict__ sel,
+                                                         const int* __restrict__ count,
+                                                         float* __restrict__ means) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float acc[];  // c floats
+  const int n = blockIdx.x, tid = threadIdx.x;
+  const int kc = min(__ldg(count + n), c);
+  for (int i = tid; i < c; i += blockDim.x) {
+    acc[i] = 0.f;
+    means[(size_t)n * c + i] = 0.f;
+  }
+  __syncthreads();
+  const int cpr = (kc + 7) >> 3;
+  const __nv_bfloat16* base = h2 + (size_t)n * sr * c;
+  for (int k = tid; k < hw * cpr; k += blockDim.x) {
+    const int r = k / cpr, ch = (k - r * cpr) << 3;
+    const uint4 v = *reinterpret_cast<const uint4*>(base + (size_t)r * c + ch);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = unpack_bf16x2(w[e]);
+      if (ch + 2 * e < kc) atomicAdd(&acc[ch + 2 * e], f.x);
+      if (ch + 2 * e + 1 < kc) atomicAdd(&acc[ch + 2 * e + 1], f.y);
+    }
+  }
+  __syncthreads();
+  const float inv = 1.f / (float)hw;
+  for (int j = tid; j < kc; j += blockDim.x) means[(size_t)n * c + __ldg(sel + (size_t)n * c + j)] = acc[j] * inv;
+}
+
+__global__ void __launch_bounds__(256) se_scale_ch_kernel(__nv_bfloat16* __restrict__ h2, int n, int c, int hw,
+                                                          int sr, const int* __restrict__ sel,
+                                                          const int* __restrict__ count,
+                                                          const float* __restrict__ gates) {
+  pdl_wait();
+  pdl_trigger();
+  const int c8 = c >> 3;
+  const long long per = (long long)hw * c8;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < (long long)n * per;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int ni = (int)(k / per);
+    const long long rem = k - ni * per;
+    const int r = (int)(rem / c8), ch = (int)(rem - (long long)r * c8) << 3;
+    const int kc = __ldg(count + ni);
+    if (ch >= kc) continue;
+    const int* sl = sel + (size_t)ni * c;
+    const float* g = gates + (size_t)ni * c;
+    uint4* pp = reinterpret_cast<uint4*>(h2 + ((size_t)ni * sr + r) * c + ch);
+    uint4 v = *pp;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = unpack_bf16x2(w[e]);
+      const int j = ch + 2 * e;
+      if (j < kc) f.x *= __ldg(g + __ldg(sl + j));
+      if (j + 1 < kc) f.y *= __ldg(g + __ldg(sl + j + 1));
+      w[e] = pack_bf16x2(f.x, f.y);
+    }
+    *pp = v;
+  }
+}
+
+// scratch: >= 2*n*c floats (the block's h1 buffer, dead after conv2)
+cudaError_t launch_se_channel(void* h2, int n, int c, int hw, int sr, const int* sel, const int* count,
+                              const float* w1, const float* b1, int hs, const float* w2, const float* b2,
+                              void* scratch, cudaStream_t s) {
+  float* means = reinterpret_cast<float*>(scratch);
+  float* gates = means + (size_t)n * c;
+  launch_k(se_pool_ch_kernel, dim3(n), dim3(256), (size_t)c * sizeof(float), s,
+           reinterpret_cast<const __nv_bfloat16*>(h2), c, hw, sr, sel, count, means);
+  const size_t smem = (size_t)SE_SPB * (c + hs) * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(se_fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  launch_k(se_fc_kernel, dim3((n + SE_SPB - 1) / SE_SPB), dim3(256), smem, s, n, c, means, w1, b1, hs, w2,
+           b2, gates);
+  const long long work = (long long)n * hw * (c / 8);
+  const int blocks = (int)((work + 255) / 256 < 148 * 16 ? (work + 255) / 256 : 148 * 16);
+  launch_k(se_scale_ch_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s,
+           reinterpret_cast<__nv_bfloat16*>(h2), n, c, hw, sr, sel, count, gates);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride, int pad,
                                const float* mean, const float* inv_std, void* cols, int cols_ld,
                                cudaStream_t s) {

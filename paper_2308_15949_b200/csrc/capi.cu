@@ -36,6 +36,9 @@ cudaError_t launch_masker_decide(const float* cell_sums, int total, int win, flo
 cudaError_t launch_dilate_pixels(const uint8_t* coarse, int n, int h, int w, int s, int stride,
                                  int cells_h, int cells_w, int radius, int* list, int* count,
                                  void* scan, cudaStream_t stream);
+cudaError_t launch_se_channel(void* h2, int n, int c, int hw, int sr, const int* sel, const int* count,
+                              const float* w1, const float* b1, int hs, const float* w2, const float* b2,
+                              void* scratch, cudaStream_t s);
 cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride, int pad,
                                const float* mean, const float* inv_std, void* cols, int cols_ld,
                                cudaStream_t s);
@@ -765,6 +768,15 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
   c2.relu = a->relu2;
   c2.out = a->h2;
   if ((rc = run_conv(&c2, st))) return rc;
+  if (a->se_w1) {  // EXT squeeze-excitation over each sample's kept channels
+    // (conv2 wrote sample n's rows compactly at [n*ho*wo, (n+1)*ho*wo))
+    if (a->c_mid % 8 || (size_t)n * sr1 * cmp * 2 < (size_t)2 * n * cmp * 4)
+      return fail(LAUD_ERR_SHAPE, "SE needs c_mid % 8 == 0");
+    if ((rc = cuda_check(launch_se_channel(a->h2, n, cmp, ho * wo, ho * wo, a->ch_sel, a->ch_count, a->se_w1,
+                                           a->se_b1, a->se_hidden, a->se_w2, a->se_b2, a->h1, st),
+                         "squeeze-excitation (channel)", 1)))
+      return rc;
+  }
   laud_conv_args c3 = c2;
   c3.act = a->h2;
   c3.in_h = ho;
@@ -793,8 +805,10 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   if (!a || !a->x || !a->out || !a->w1 || !a->w2 || !a->w3)
     return fail(LAUD_ERR_ARG, "null pointer in block args");
   if (a->groups < 1) return fail(LAUD_ERR_ARG, "groups must be >= 1");
-  if (a->groups != 1 && a->paradigm == LAUD_PARADIGM_CHANNEL)  // reference.py:405-406
+  if (a->groups != 1 && a->paradigm == LAUD_PARADIGM_CHANNEL && !a->ch_dense_w2)  // reference.py:405-406
     return fail(LAUD_ERR_UNSUPPORTED, "sparse channel execution requires groups == 1");
+  if (a->se_w1 && a->paradigm == LAUD_PARADIGM_CHANNEL && a->fp32)
+    return fail(LAUD_ERR_UNSUPPORTED, "squeeze-excitation under channel skipping needs bf16 mode");
   if (a->stride != 1 && a->stride != 2) return fail(LAUD_ERR_ARG, "stride must be 1 or 2");
   if (a->stride > 1 && !a->has_down)
     return fail(LAUD_ERR_SHAPE, "a strided block needs a downsample path");

@@ -88,6 +88,17 @@ def pack_weight(w, c_in_pad: int, device="cuda", groups: int = 1, dtype=torch.bf
     return out.to(device=device, dtype=dtype).contiguous()
 
 
+def grouped_to_dense(w, groups: int) -> np.ndarray:
+    """[c_out, c_in / groups, k, k] -> [c_out, c_in, k, k] block-diagonal dense kernel."""
+    w = np.asarray(w if isinstance(w, np.ndarray) else torch.as_tensor(w).cpu().numpy(), dtype=np.float64)
+    co, cig, kh, kw = w.shape
+    cog = co // groups
+    out = np.zeros((co, cig * groups, kh, kw))
+    for g in range(groups):
+        out[g * cog:(g + 1) * cog, g * cig:(g + 1) * cig] = w[g * cog:(g + 1) * cog]
+    return out
+
+
 def fvec(v, n: int, fill: float, device="cuda") -> torch.Tensor:
     """Per-channel fp32 vector padded to pad8(n) (padding channels get `fill`)."""
     out = torch.full((pad8(n),), fill, dtype=torch.float32)
@@ -166,7 +177,7 @@ class DeviceBlock:
 
     def __init__(self, block: BlockSpec, w1, w2, w3, w_down=None, epilogue: Optional[Epilogue] = None,
                  masker_w=None, masker_bias: float = 0.0, device="cuda", fold_scale: bool = False,
-                 dtype=torch.bfloat16):
+                 dtype=torch.bfloat16, grouped_channel_ext: bool = False):
         require_cuda()
         if dtype not in (torch.bfloat16, torch.float32):
             raise DeviceError("compute dtype must be bf16 (tcgen05) or fp32 (FFMA numerics mode)")
@@ -187,6 +198,13 @@ class DeviceBlock:
         if self.groups > 1 and self.cmid_p != self.c_mid:
             raise DeviceError("grouped conv2 needs a mid width that is a multiple of 8")
         self.w2 = pack_weight(w2, self.cmid_p, device, groups=self.groups, dtype=dtype)
+        # EXT (laud.h ch_dense_w2): channel skipping over a grouped conv2 runs on the
+        # block-diagonal dense kernel; without it channel mode keeps the reference's
+        # groups == 1 requirement
+        self.w2_dense = None
+        self._w2_grouped = (w2, device) if self.groups > 1 else None
+        if grouped_channel_ext:
+            self.enable_grouped_channel()
         self.w3 = pack_weight(w3, self.cmid_p, device, dtype=dtype)
         self.wd = pack_weight(w_down, self.cin_p, device, dtype=dtype) if w_down is not None else None
         self.ep = ep
@@ -265,6 +283,14 @@ class DeviceBlock:
             a.ch_bias = ptr(getattr(self, "ch_bias", None))
             a.ch_hidden, a.ch_d, a.ch_groups = self.ch_hidden, self.ch_d, self.ch_g
 
+    def enable_grouped_channel(self):
+        """EXT: allow channel skipping over this block's grouped conv2 (packs the
+        block-diagonal dense kernel once; laud.h ch_dense_w2)."""
+        if self._w2_grouped is not None and self.w2_dense is None:
+            w2, device = self._w2_grouped
+            self.w2_dense = pack_weight(grouped_to_dense(w2, self.groups), self.cmid_p, device, dtype=self.dtype)
+        return self
+
     def forward(self, x: torch.Tensor, paradigm: str = "spatial", s: int = 1,
                 coarse: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
                 misplace_first: bool = False, stream=None, ws: Optional[Workspace] = None,
@@ -330,6 +356,8 @@ class DeviceBlock:
             cell_sums=ptr(cell_sums))
         if paradigm == "channel":
             self._channel_args(a, n, ws, chmask)
+            if self.w2_dense is not None:
+                a.w2, a.ch_dense_w2 = ptr(self.w2_dense), 1
         if dn is not None and paradigm == "spatial":
             a.dn, a.prev_coarse, a.next_wdiff = ptr(dn), ptr(prev_coarse), ptr(next_wdiff)
         _lib.check(lib.laud_block_forward(C.byref(a), stream_handle(stream)))

@@ -336,7 +336,7 @@ def _u8(a) -> torch.Tensor:
 
 
 def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConfig, mask,
-                         _misplace_first_patch: bool = False):
+                         _misplace_first_patch: bool = False, grouped_channel_ext: bool = False):
     """Inference forward computing only what the mask selects (`reference.py:356-436`).
 
     SPATIAL: gather-conv1 on the halo-dilated pixel set, 3x3 conv over the
@@ -344,6 +344,8 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
     CHANNEL: dynamic-width convs over the kept channels; LAYER: per-sample
     compaction; STATIC: the dense block.  ``_misplace_first_patch`` is the
     reference's fault hook (`reference.py:362, 400-401`), honoured on device.
+    ``grouped_channel_ext`` (EXT, default off = the reference's ShapeMismatch)
+    runs channel skipping over a grouped conv2 (`channel.channel_block_sparse`).
     """
     D.require_cuda()
     x = np.asarray(x)
@@ -352,7 +354,7 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
     p = cfg.paradigm
     if p is Paradigm.CHANNEL:
         from . import channel as CH
-        return CH.channel_block_sparse(x, bw, block, mask)
+        return CH.channel_block_sparse(x, bw, block, mask, grouped_channel_ext=grouped_channel_ext)
     db = device_block(bw, block)
     xd = D.to_device_nhwc(x, dtype=db.dtype)
     out = block.output_shape

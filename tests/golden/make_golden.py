@@ -148,6 +148,44 @@ def config1():
                         coarse_exact=coarse, y_exact=y2.astype(np.float32))
 
 
+def grouped_channel():
+    """Channel skipping over a GROUPED conv2 (RegNet-style): the reference's sparse
+    executor rejects it (`reference.py:405-406`), its dense-masked executor defines
+    it (`reference.py:331-339`: conv2 input and output masked, groups kept).  The
+    oracle's EXT sparse path is pinned to these dense-masked outputs."""
+    a = {}
+    rng = np.random.default_rng(21)
+    for tag, (cin, cm, g, cout, hw, stride, gran) in {
+            "a": (16, 24, 3, 32, 8, 1, 1), "b": (24, 48, 6, 48, 10, 2, 2), "c": (32, 32, 4, 32, 6, 1, 4)}.items():
+        blk = rcore.BlockSpec(conv1=rcore.ConvLayerSpec(cin, cm, 1),
+                              conv2=rcore.ConvLayerSpec(cm, cm, 3, stride, g),
+                              conv3=rcore.ConvLayerSpec(cm, cout, 1),
+                              input_shape=rcore.TensorShape(cin, hw, hw),
+                              has_downsample=stride > 1 or cin != cout)
+        bw = R.make_block_weights(blk, rng)
+        n = 3
+        x = rng.standard_normal((n, cin, hw, hw))
+        d = cm // gran
+        coarse = np.zeros((n, d), bool)
+        for i in range(n):
+            coarse[i, rng.permutation(d)[: max(1, d // 2 + i - 1)]] = True
+        expanded = np.repeat(coarse, gran, axis=1)
+        m = R.ChannelMask(coarse, expanded, gran)
+        cfg = rcore.DynamicConfig(rcore.Paradigm.CHANNEL, channel_granularity=gran)
+        a[f"{tag}_x"], a[f"{tag}_w1"], a[f"{tag}_w2"], a[f"{tag}_w3"] = x, bw.w1, bw.w2, bw.w3
+        if bw.w_down is not None:
+            a[f"{tag}_wd"] = bw.w_down
+        a[f"{tag}_geom"] = np.array([cin, cm, g, cout, hw, stride, gran])
+        a[f"{tag}_coarse"] = coarse
+        a[f"{tag}_y_dense"] = R.block_forward_dense_masked(x, bw, blk, cfg, m)
+        try:
+            R.block_forward_sparse(x, bw, blk, cfg, m)
+            a[f"{tag}_sparse_rejected"] = np.array(False)
+        except Exception as exc:  # the reference's sparse executor refuses groups != 1
+            a[f"{tag}_sparse_rejected"] = np.array(type(exc).__name__ == "ShapeMismatch")
+    np.savez_compressed(OUT / "grouped_channel.npz", **a)
+
+
 def zoo_shapes():
     out = {}
     for name in ("resnet50", "resnet101", "regnety-400mf", "regnety-800mf"):
@@ -166,5 +204,6 @@ if __name__ == "__main__":
     maskers()
     block_weights_and_convs()
     config1()
+    grouped_channel()
     zoo_shapes()
     print("golden fixtures written to", OUT)

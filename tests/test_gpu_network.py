@@ -32,7 +32,8 @@ def _net(arch, paradigm, plan="4-2-2-1", ratio=0.5):
     ("resnet50", "layer", "4-2-2-1"), ("resnet50", "static", "4-2-2-1"),
     ("resnet50", "channel", "1-1-1-1"), ("resnet50", "channel", "2-2-2-2"),
     ("regnety-1.6gf", "spatial", "4-4-2-1"), ("regnety-1.6gf", "layer", "4-4-2-1"),
-    ("regnety-1.6gf", "static", "4-4-2-1"), ("regnety-400mf", "spatial", "4-4-2-1")])
+    ("regnety-1.6gf", "static", "4-4-2-1"), ("regnety-400mf", "spatial", "4-4-2-1"),
+    ("regnety-1.6gf", "channel", "1-1-1-1"), ("regnety-400mf", "channel", "2-2-2-2")])
 def test_network_matches_oracle(arch, paradigm, plan):
     net, img, logits, masks = _net(arch, paradigm, plan)
     plan = tuple(net.plan)

@@ -360,7 +360,8 @@ def test_verify_cli_on_gpu(tmp_path):
 
 
 @pytest.mark.parametrize("stage,index,paradigm", [(2, 1, "spatial"), (3, 0, "spatial"), (4, 1, "spatial"),
-                                                   (3, 1, "layer"), (2, 0, "static")])
+                                                   (3, 1, "layer"), (2, 0, "static"), (3, 1, "channel"),
+                                                   (2, 0, "channel"), (1, 1, "channel")])
 def test_regnet_se_block_matches_oracle_ext(stage, index, paradigm):
     """EXT squeeze-excitation (pool over the sample's active patches) on the device
     vs the oracle EXT, bf16 rounding points emulated."""
@@ -393,15 +394,25 @@ def test_regnet_se_block_matches_oracle_ext(stage, index, paradigm):
         d = np.array([True, False, True])
         y, *_ = db.forward(xd, "layer", coarse=torch.from_numpy(d.astype(np.uint8)).cuda())
         cfg, om = DynamicConfig(Paradigm.LAYER), O.LayerMask(d)
+    elif paradigm == "channel":  # EXT: grouped conv2 + SE under channel skipping
+        db.enable_grouped_channel()
+        cm = blk.conv2.out_channels
+        cmask = rng.random((n, cm)) < 0.5
+        cmask[1] = False  # a sample that keeps no channel
+        mm = np.zeros((n, db.cmid_p), np.uint8)
+        mm[:, :cm] = cmask
+        y, *_ = db.forward(xd, "channel", chmask=torch.from_numpy(mm.reshape(-1)).cuda())
+        cfg, om = DynamicConfig(Paradigm.CHANNEL, channel_granularity=1), O.ChannelMask(cmask, cmask, 1)
     else:
         y, *_ = db.forward(xd, "static")
         cfg, om = DynamicConfig(Paradigm.STATIC), None
     torch.cuda.synchronize()
     yg = D.from_device_nhwc(y, o.channels)
-    emu = O.block_forward_sparse(x, obw, blk, cfg, om, epilogues=oep, emulate_bf16=True)
+    emu = O.block_forward_sparse(x, obw, blk, cfg, om, epilogues=oep, emulate_bf16=True, grouped_channel_ext=True)
     assert _rel(yg, emu) <= 2e-3, _rel(yg, emu)
     no_se = O.block_forward_sparse(x, obw, blk, cfg, om, epilogues=O.Epilogues(
-        b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"], relu_out=True), emulate_bf16=True)
+        b1=bp["b1"], relu1=True, b2=bp["b2"], relu2=True, b3=bp["b3"], bd=bp["bd"], relu_out=True), emulate_bf16=True,
+        grouped_channel_ext=True)
     assert _rel(yg, no_se) > 1e-2  # the gate is really applied
 
 
@@ -437,3 +448,70 @@ def test_masker_fused_into_conv1_decides_like_standalone(stage, index, s, n):
     assert np.mean(got[0] == got[1]) > 0.999
     if (got[0] == got[1]).all():
         assert torch.equal(ys[0], ys[1])
+
+
+def _grouped_golden(tag):
+    d = np.load(G / "grouped_channel.npz")
+    cin, cm, g, cout, hw, stride, gran = (int(v) for v in d[f"{tag}_geom"])
+    blk = BlockSpec(ConvLayerSpec(cin, cm, 1), ConvLayerSpec(cm, cm, 3, stride, g), ConvLayerSpec(cm, cout, 1),
+                    TensorShape(cin, hw, hw), has_downsample=stride > 1 or cin != cout)
+    wd = d[f"{tag}_wd"] if f"{tag}_wd" in d else None
+    coarse = d[f"{tag}_coarse"]
+    return d, blk, (d[f"{tag}_w1"], d[f"{tag}_w2"], d[f"{tag}_w3"], wd), coarse, gran, d[f"{tag}_x"]
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_grouped_channel_ext_matches_reference_dense_masked(tag):
+    """EXT channel skipping over a grouped conv2 on the GPU (dynamic-width GEMMs over
+    the block-diagonal dense kernel) vs the REFERENCE's dense-masked output
+    (golden) and the bf16-emulating oracle EXT; off by default like the reference."""
+    R = _R()
+    from paper_2308_15949_b200.errors import ShapeMismatch
+    d, blk, ws, coarse, gran, x = _grouped_golden(tag)
+    bw = R.BlockWeights(*ws)
+    m = R.ChannelMask(coarse, np.repeat(coarse, gran, axis=1), gran)
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=gran)
+    with pytest.raises(ShapeMismatch):
+        R.block_forward_sparse(x, bw, blk, cfg, m)
+    y = R.block_forward_sparse(x, bw, blk, cfg, m, grouped_channel_ext=True)
+    emu = O.block_forward_sparse(x, O.BlockWeights(*ws), blk, cfg, O.ChannelMask(coarse, m.expanded, gran),
+                                 emulate_bf16=True, grouped_channel_ext=True)
+    assert _rel(y, emu) <= BF16_TOL, _rel(y, emu)
+    assert _rel(y, d[f"{tag}_y_dense"]) <= 1e-2
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_grouped_channel_ext_fp32_mode(tag, fp32_mode):
+    """fp32 mode: <= 1e-5 vs the reference's fp64 dense-masked output."""
+    R = fp32_mode
+    d, blk, ws, coarse, gran, x = _grouped_golden(tag)
+    m = R.ChannelMask(coarse, np.repeat(coarse, gran, axis=1), gran)
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=gran)
+    y = R.block_forward_sparse(x, R.BlockWeights(*ws), blk, cfg, m, grouped_channel_ext=True)
+    assert _rel(y, d[f"{tag}_y_dense"]) <= 1e-5
+
+
+@pytest.mark.parametrize("stage,r", [(2, 0.5), (3, 0.3), (4, 0.75)])
+def test_regnet_grouped_channel_ext_block(stage, r):
+    """RegNetY-1.6GF template blocks (group width 24) with exact-count channel masks."""
+    R = _R()
+    from paper_2308_15949_b200.zoo import build_network
+    net = build_network("regnety-1.6gf")
+    block = [b.block for b in net.blocks if b.stage == stage and b.index == 1][0]
+    rng = np.random.default_rng(40 + stage)
+    bw = R.make_block_weights(block, rng)
+    n, cm = 2, block.conv2.out_channels
+    ci = block.input_shape
+    x = rng.standard_normal((n, ci.channels, ci.height, ci.width))
+    coarse = np.zeros((n, cm), bool)
+    for i in range(n):
+        coarse[i, rng.permutation(cm)[: int(round(r * cm))]] = True
+    m = R.ChannelMask(coarse, coarse, 1)
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=1)
+    y = R.block_forward_sparse(x, bw, block, cfg, m, grouped_channel_ext=True)
+    emu = O.block_forward_sparse(x, O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down), block, cfg,
+                                 O.ChannelMask(coarse, coarse, 1), emulate_bf16=True, grouped_channel_ext=True)
+    assert _rel(y, emu) <= BF16_TOL, _rel(y, emu)
+    yd = O.block_forward_dense_masked(x, O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down), block, cfg,
+                                      O.ChannelMask(coarse, coarse, 1))
+    assert _rel(y, yd) <= 1e-2

@@ -176,3 +176,42 @@ def test_zoo_matches_reference():
     assert [s.depth for s in net.stages] == [2, 6, 17, 2]
     assert [s.block_template.conv3.out_channels for s in net.stages] == [48, 120, 336, 888]
     assert net.blocks[0].block.conv2.groups == 2
+
+
+def _grouped_case(d, tag):
+    cin, cm, g, cout, hw, stride, gran = (int(v) for v in d[f"{tag}_geom"])
+    blk = BlockSpec(conv1=ConvLayerSpec(cin, cm, 1), conv2=ConvLayerSpec(cm, cm, 3, stride, g),
+                    conv3=ConvLayerSpec(cm, cout, 1), input_shape=TensorShape(cin, hw, hw),
+                    has_downsample=stride > 1 or cin != cout)
+    wd = d[f"{tag}_wd"] if f"{tag}_wd" in d else None
+    bw = O.BlockWeights(d[f"{tag}_w1"], d[f"{tag}_w2"], d[f"{tag}_w3"], wd)
+    coarse = d[f"{tag}_coarse"]
+    mask = O.ChannelMask(coarse, np.repeat(coarse, gran, axis=1), gran)
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=gran)
+    return blk, bw, mask, cfg, d[f"{tag}_x"]
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_grouped_channel_ext_matches_reference_dense_masked(tag):
+    """EXT sparse channel skipping over a grouped conv2 reproduces the REFERENCE's
+    dense-masked channel forward (fixture from dynlat) to 1e-9; without the EXT
+    flag the oracle rejects it exactly like the reference's sparse executor."""
+    d = np.load(G / "grouped_channel.npz")
+    blk, bw, mask, cfg, x = _grouped_case(d, tag)
+    assert bool(d[f"{tag}_sparse_rejected"])
+    with pytest.raises(ShapeMismatch):
+        O.block_forward_sparse(x, bw, blk, cfg, mask)
+    y = O.block_forward_sparse(x, bw, blk, cfg, mask, grouped_channel_ext=True)
+    np.testing.assert_allclose(y, d[f"{tag}_y_dense"], rtol=0, atol=1e-9)
+    np.testing.assert_allclose(O.block_forward_dense_masked(x, bw, blk, cfg, mask), d[f"{tag}_y_dense"],
+                               rtol=0, atol=1e-11)
+
+
+def test_grouped_to_dense_is_block_diagonal():
+    w = np.arange(6 * 2 * 3 * 3, dtype=float).reshape(6, 2, 3, 3) + 1
+    dense = O.grouped_to_dense(w, 3)
+    assert dense.shape == (6, 6, 3, 3)
+    for o in range(6):
+        g = o // 2
+        np.testing.assert_array_equal(dense[o, 2 * g:2 * g + 2], w[o])
+        assert not dense[o, :2 * g].any() and not dense[o, 2 * g + 2:].any()
