@@ -226,12 +226,14 @@ typedef struct laud_block_args {
    * pass clears what it reads); NULL = standalone masker pass. */
   float* cell_sums;
   /* EXT channel skipping over a grouped conv2 (RegNet; the reference's sparse
-   * executor rejects groups != 1, reference.py:405-406): w2 holds the grouped
-   * kernel expanded block-diagonally to a dense [c_mid][9][kpad] kernel, so
-   * W2[sel][:, sel] keeps each group's kept links — the sparse form of the
-   * reference's dense-masked channel forward (reference.py:331-339).  0 = the
-   * reference behaviour (LAUD_ERR_UNSUPPORTED). */
-  int ch_dense_w2;
+   * executor rejects groups != 1, reference.py:405-406): the grouped kernel
+   * expanded block-diagonally to a dense [c_mid][9][kpad] kernel, so the
+   * per-sample schedule's W2[sel][:, sel] keeps each group's kept links — the
+   * sparse form of the reference's dense-masked channel forward
+   * (reference.py:331-339); w2 keeps the grouped layout, which the
+   * dense-masked schedule uses.  NULL = the reference behaviour
+   * (LAUD_ERR_UNSUPPORTED for groups != 1). */
+  const void* w2_dense;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

@@ -635,12 +635,21 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
                          "skip copy", 0)))
       return rc;
   }
-  if (a->fp32) {
-    // fp32 mode: the dense-masked schedule of the same algebra (reference.py:336-339):
-    // h1 and h2 are zero on the dropped channels, so conv3 sums only the kept ones.
+  // Schedule.  Per-sample dynamic width (below) computes exactly the kept
+  // channels but packs W1[sel], W2[sel][:, sel], W3[:, sel] for every sample —
+  // at large batch that weight traffic (n * r|W|) dwarfs the activations, so
+  // from LAUD_CH_DENSE_MIN samples on (and in fp32 mode) the block runs the
+  // dense-masked schedule of the same algebra (reference.py:336-339): dense
+  // convs, h1 and h2 zeroed on the dropped channels in the epilogues, so conv3
+  // sums only the kept ones.
+  static const int dense_min = [] {
+    const char* e = getenv("LAUD_CH_DENSE_MIN");
+    return e ? atoi(e) : 8;
+  }();
+  if (a->fp32 || (dense_min > 0 && n >= dense_min)) {
     laud_conv_args c1;
     memset(&c1, 0, sizeof(c1));
-    c1.fp32 = 1;
+    c1.fp32 = a->fp32;
     c1.row_mode = ROWS_DENSE;
     c1.rows_max = n * a->h_in * a->w_in;
     c1.batch = n;
@@ -674,14 +683,22 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
     c2.ksize = 3;
     c2.stride = a->stride;
     c2.pad = 1;
-    c2.weight = a->w2;
+    c2.weight = a->w2;  // the grouped kernel itself: masking is multiplicative
+    c2.groups = a->groups;
     c2.scale = a->s2;
     c2.bias = a->b2;
     c2.relu = a->relu2;
     c2.out_mode = OUT_ROW;
     c2.out = a->h2;
     if ((rc = run_conv(&c2, st))) return rc;
+    if (a->se_w1) {  // EXT SE on the dense-masked h2 (dropped channels pool to zero)
+      if ((rc = cuda_check(launch_se(a->h2, n, cmp, nullptr, nullptr, 1, 1, ho * wo, a->se_w1, a->se_b1,
+                                     a->se_hidden, a->se_w2, a->se_b2, a->h1, st),
+                           "squeeze-excitation (channel)", 1)))
+        return rc;
+    }
     laud_conv_args c3 = c2;
+    c3.groups = 1;
     c3.act = a->h2;
     c3.in_h = ho;
     c3.in_w = wo;
@@ -712,7 +729,7 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
     ProfScope ps(3, st);
     if ((rc = cuda_check(launch_pack_weights(a->w1, cmp, 1, k1, w1s, cmp, k1, a->ch_sel, a->ch_count,
                                              cmp, 1, 0, n, st), "pack w1", 1)) ||
-        (rc = cuda_check(launch_pack_weights(a->w2, cmp, 9, k2, w2s, cmp, k2, a->ch_sel, a->ch_count,
+        (rc = cuda_check(launch_pack_weights(a->groups > 1 ? a->w2_dense : a->w2, cmp, 9, k2, w2s, cmp, k2, a->ch_sel, a->ch_count,
                                              cmp, 1, 1, n, st), "pack w2", 1)) ||
         (rc = cuda_check(launch_pack_weights(a->w3, a->c_out, 1, k2, w3s, a->c_out, k2, a->ch_sel,
                                              a->ch_count, cmp, 0, 1, n, st), "pack w3", 1)))
@@ -805,7 +822,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   if (!a || !a->x || !a->out || !a->w1 || !a->w2 || !a->w3)
     return fail(LAUD_ERR_ARG, "null pointer in block args");
   if (a->groups < 1) return fail(LAUD_ERR_ARG, "groups must be >= 1");
-  if (a->groups != 1 && a->paradigm == LAUD_PARADIGM_CHANNEL && !a->ch_dense_w2)  // reference.py:405-406
+  if (a->groups != 1 && a->paradigm == LAUD_PARADIGM_CHANNEL && !a->w2_dense)  // reference.py:405-406
     return fail(LAUD_ERR_UNSUPPORTED, "sparse channel execution requires groups == 1");
   if (a->se_w1 && a->paradigm == LAUD_PARADIGM_CHANNEL && a->fp32)
     return fail(LAUD_ERR_UNSUPPORTED, "squeeze-excitation under channel skipping needs bf16 mode");

@@ -1,7 +1,7 @@
 // Channel skipping (sm_100a): channel masker and per-sample weight packing.
 //
-// K5 channel_masker_kernel  one CTA per sample: global average pool (128-bit
-//    NHWC loads) -> relu(W1 gap) -> W2 hidden -> D interleaved logit pairs,
+// K5 channel_masker_kernel  one CTA (1024 threads) per sample: global average pool (128-bit
+//    NHWC loads, four in flight per thread) -> relu(W1 gap) -> W2 hidden -> D interleaved logit pairs,
 //    keep = l0 >= l1 (`reference.py:189-218`), G-fold expansion, and the
 //    ordered list of kept channels (`np.flatnonzero`, `reference.py:414`)
 //    with its count k_n — the indices the dynamic-width GEMMs run over.
@@ -35,8 +35,10 @@ __device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
 }
 
 // smem: gap[c] + hid[hd] + dl[d]; c, hd, d given at launch.
+constexpr int CM_THREADS = 1024;  // one CTA per sample; two resident per SM
+
 template <typename T>
-__global__ void __launch_bounds__(256) channel_masker_kernel(
+__global__ void __launch_bounds__(CM_THREADS) channel_masker_kernel(
     const T* __restrict__ x, int ld, int hw, int c, const float* __restrict__ w1, int hd,
     const float* __restrict__ w2, int d, int g, int cm, int cm_p, uint8_t* __restrict__ coarse,
     float* __restrict__ dvals, uint8_t* __restrict__ expanded, int* __restrict__ sel,
@@ -58,7 +60,18 @@ __global__ void __launch_bounds__(256) channel_masker_kernel(
     const int groups = blockDim.x / cpp;
     const int chunk = tid % cpp, grp = tid / cpp;
     float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int px = grp; px < hw; px += groups) {
+    int px = grp;
+    // four independent 16-byte loads in flight per thread (the pass is HBM-bound)
+    for (; px + 3 * groups < hw; px += 4 * groups) {
+      float v0[8], v1[8], v2[8], v3[8];
+      load8<T>(xs + (size_t)px * ld + chunk * 8, v0);
+      load8<T>(xs + (size_t)(px + groups) * ld + chunk * 8, v1);
+      load8<T>(xs + (size_t)(px + 2 * groups) * ld + chunk * 8, v2);
+      load8<T>(xs + (size_t)(px + 3 * groups) * ld + chunk * 8, v3);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] += (v0[e] + v1[e]) + (v2[e] + v3[e]);
+    }
+    for (; px < hw; px += groups) {
       float v[8];
       load8<T>(xs + (size_t)px * ld + chunk * 8, v);
 #pragma unroll
@@ -110,7 +123,7 @@ __global__ void __launch_bounds__(256) channel_masker_kernel(
     const bool keep = ch < cm && dl[ch / g] >= 0.f;
     if (ch < cm_p) expanded[(size_t)n * cm_p + ch] = keep ? 1 : 0;
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    __shared__ int s_wc[8];
+    __shared__ int s_wc[CM_THREADS / 32];
     if (lane == 0) s_wc[warp] = __popc(bal);
     __syncthreads();
     int off = s_base;
@@ -202,11 +215,11 @@ cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int h
                                   int* sel, int* count, const float* bias, cudaStream_t s) {
   const size_t smem = (size_t)(c + hd + d) * sizeof(float);
   if (x_f32)
-    launch_k(channel_masker_kernel<float>, dim3(n), dim3(256), smem, s, reinterpret_cast<const float*>(x), ld, hw, c,
+    launch_k(channel_masker_kernel<float>, dim3(n), dim3(CM_THREADS), smem, s, reinterpret_cast<const float*>(x), ld, hw, c,
                                                       w1, hd, w2, d, g, cm, cm_p, coarse, dvals,
                                                       expanded, sel, count, bias);
   else
-    launch_k(channel_masker_kernel<__nv_bfloat16>, dim3(n), dim3(256), smem, s, 
+    launch_k(channel_masker_kernel<__nv_bfloat16>, dim3(n), dim3(CM_THREADS), smem, s, 
         reinterpret_cast<const __nv_bfloat16*>(x), ld, hw, c, w1, hd, w2, d, g, cm, cm_p, coarse,
         dvals, expanded, sel, count, bias);
   return cudaGetLastError();

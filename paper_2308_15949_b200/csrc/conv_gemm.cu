@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool pre = staged && resid != nullptr;
     const bool has_scale = p.scale != nullptr || p.col_index != nullptr;
     // the common epilogues (bias [+ residual] [+ ReLU]) take a branch-free path
-    const bool plain = staged && !has_scale && !p.ymask_channel && !p.ymask_coarse && !p.mdot_w;
+    const bool plain = staged && !has_scale && !p.ymask_coarse && !p.mdot_w;
     // the whole bias vector lives in smem for the kernel when it fits (the
     // per-warp vector slices are the fallback for scale / masker-dot / lists)
     const bool cached = !has_scale && !p.mdot_w && p.n_out <= L::VEC_BYTES / 4;
@@ -819,6 +819,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           v[5] = __uint_as_float(rv[g * 8 + 5]) + b1.y;
           v[6] = __uint_as_float(rv[g * 8 + 6]) + b1.z;
           v[7] = __uint_as_float(rv[g * 8 + 7]) + b1.w;
+          if (p.ymask_channel) {  // per-sample channel mask (dense-masked channel schedule)
+            const uint2 mk = __ldg(reinterpret_cast<const uint2*>(
+                p.ymask_channel + (size_t)cur.rp.n * p.n_out + c_base + cl + g * 8));
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (!(((e < 4 ? (mk.x >> (8 * e)) : (mk.y >> (8 * (e - 4)))) & 0xff))) v[e] = 0.f;
+          }
           if (with_resid) {
             float2 f;
             f = unpack_bf16x2(rr[g].x); v[0] += f.x; v[1] += f.y;

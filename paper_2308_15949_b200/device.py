@@ -198,7 +198,7 @@ class DeviceBlock:
         if self.groups > 1 and self.cmid_p != self.c_mid:
             raise DeviceError("grouped conv2 needs a mid width that is a multiple of 8")
         self.w2 = pack_weight(w2, self.cmid_p, device, groups=self.groups, dtype=dtype)
-        # EXT (laud.h ch_dense_w2): channel skipping over a grouped conv2 runs on the
+        # EXT (laud.h w2_dense): channel skipping over a grouped conv2 runs on the
         # block-diagonal dense kernel; without it channel mode keeps the reference's
         # groups == 1 requirement
         self.w2_dense = None
@@ -285,7 +285,7 @@ class DeviceBlock:
 
     def enable_grouped_channel(self):
         """EXT: allow channel skipping over this block's grouped conv2 (packs the
-        block-diagonal dense kernel once; laud.h ch_dense_w2)."""
+        block-diagonal dense kernel once; laud.h w2_dense)."""
         if self._w2_grouped is not None and self.w2_dense is None:
             w2, device = self._w2_grouped
             self.w2_dense = pack_weight(grouped_to_dense(w2, self.groups), self.cmid_p, device, dtype=self.dtype)
@@ -357,7 +357,7 @@ class DeviceBlock:
         if paradigm == "channel":
             self._channel_args(a, n, ws, chmask)
             if self.w2_dense is not None:
-                a.w2, a.ch_dense_w2 = ptr(self.w2_dense), 1
+                a.w2_dense = ptr(self.w2_dense)
         if dn is not None and paradigm == "spatial":
             a.dn, a.prev_coarse, a.next_wdiff = ptr(dn), ptr(prev_coarse), ptr(next_wdiff)
         _lib.check(lib.laud_block_forward(C.byref(a), stream_handle(stream)))

@@ -140,7 +140,7 @@ class LaudNetwork:
                 g = self.plan[bp["stage"] - 1]
                 db.set_channel_masker(bp["ch_w1"], bp["ch_w2"], g)
                 # grouped conv2 (RegNet): the EXT block-diagonal dense kernel
-                # (laud.h ch_dense_w2; the network executor is EXT territory anyway)
+                # (laud.h w2_dense; the network executor is EXT territory anyway)
                 db.enable_grouped_channel()
             if "se_w1" in bp:  # RegNetY squeeze-excitation (EXT)
                 db.set_se(bp["se_w1"], bp["se_b1"], bp["se_w2"], bp["se_b2"])
