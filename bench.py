@@ -369,6 +369,62 @@ def batch1_latency(torch, args, net, flush, reps=20):
     return out
 
 
+def block_sweep_b1_vs_cpu(torch, args, flush, reps_cpu=3):
+    """Per-block latency vs activation ratio at batch 1 (SURVEY §8d CPU baseline):
+    the device (CUDA graph, L2 flushed) next to the numpy fp64 oracle's
+    ``block_forward_sparse`` (the reference's algorithm) on this box's host
+    cores, same block geometry, exact-count masks, median of ``reps_cpu``."""
+    from oracle import laud_oracle as O
+    from paper_2308_15949_b200 import device as D
+    from paper_2308_15949_b200.core import DynamicConfig, Paradigm
+    from paper_2308_15949_b200.network import make_params
+    params = make_params(args.arch, 0)
+    plan = tuple(int(v) for v in args.plan.split("-"))
+    out = {}
+    rng = np.random.default_rng(0)
+    seen = set()
+    for bp in params["blocks"]:
+        if bp["stage"] in seen or bp["index"] != 1:
+            continue
+        seen.add(bp["stage"])
+        blk = bp["block"]
+        s = plan[bp["stage"] - 1]
+        db = D.DeviceBlock(blk, bp["w1"], bp["w2"], bp["w3"], None)
+        wsp = D.Workspace()
+        ci, o = blk.input_shape, blk.output_shape
+        xh = rng.standard_normal((1, ci.channels, ci.height, ci.width))
+        x = D.to_device_nhwc(xh)
+        cells = (o.height // s) * (o.width // s)
+        bw = O.BlockWeights(bp["w1"], bp["w2"], bp["w3"], None)
+        row = {}
+        for r in (0.2, 0.5, 0.8, 1.0, "static"):
+            if r == "static":
+                fn = lambda: db.forward(xx, "static", out=xx, ws=wsp)  # noqa: E731
+                cfg, om = DynamicConfig(Paradigm.STATIC), None
+            else:
+                cz = np.zeros(cells, np.uint8)
+                cz[rng.permutation(cells)[:int(round(r * cells))]] = 1
+                coarse = torch.from_numpy(cz).cuda()
+                fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp)  # noqa: E731
+                c3 = cz.reshape(1, o.height // s, o.width // s).astype(bool)
+                cfg = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=s)
+                om = O.SpatialMask(c3, O.upsample_coarse(c3, s), s)
+            xx = x.clone()
+            g, _ = capture(torch, fn, 2)
+            tot, _ = timed_graph(torch, g, 20, flush, torch.cuda.current_stream())
+            del g
+            ts = []
+            for _ in range(reps_cpu):
+                t0 = time.perf_counter()
+                O.block_forward_sparse(xh, bw, blk, cfg, om)
+                ts.append(time.perf_counter() - t0)
+            row[str(r)] = {"gpu_us": round(1e3 * tot / 20, 1),
+                           "cpu_oracle_us": round(1e6 * statistics.median(ts), 1)}
+        out[f"s{bp['stage']}b1_S{s}"] = row
+    return {"blocks": out, "cpu_cores": blas_threads(), "cpu_kind": "port (numpy fp64 oracle)",
+            "batch": 1}
+
+
 def block_sweep(torch, args, flush):
     """Per-block device latency vs activation ratio (exact-count masks), batch = args.batch."""
     from paper_2308_15949_b200 import device as D
@@ -530,6 +586,11 @@ def run_gpu(args):
             extra["per_block_us_vs_ratio"] = block_sweep(torch, args, flush)
         except Exception as exc:  # never lose the headline line to the sweep
             extra["per_block_us_vs_ratio"] = f"failed: {exc!r}"
+        if args.paradigm == "spatial" and ws == 1:
+            try:
+                extra["per_block_b1_vs_cpu"] = block_sweep_b1_vs_cpu(torch, args, flush)
+            except Exception as exc:
+                extra["per_block_b1_vs_cpu"] = f"failed: {exc!r}"
     cpu = None
     if rank == 0 and ws == 1 and not args.no_baselines:
         v, ts = cpu_oracle_images_per_s(args, args.cpu_images, params=net.params,

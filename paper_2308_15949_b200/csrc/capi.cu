@@ -260,8 +260,17 @@ int pick_bn(int n_out, int k, long long rows) {
   }();
   if (forced == 64 || forced == 128 || forced == 256) return n_out <= 64 ? 64 : forced;
   if (n_out <= 64) return 64;
+  // grids under one wave (small batch): narrower N tiles give more CTAs, each
+  // with a shorter B stream — the single-CTA K loop is the latency there
+  static const int small_env = [] {
+    const char* e = getenv("LAUD_SMALL_GRID_BN");
+    return e ? atoi(e) : 1;
+  }();
+  const long long mt = (rows + 127) / 128;
+  if (small_env && mt * ((n_out + 63) / 64) <= num_sms()) return 64;
+  if (small_env && mt * ((n_out + 127) / 128) <= num_sms()) return 128;
   if (n_out <= 128) return 128;
-  return 256;  // measured best for every R101 conv shape (tools/sweep_cfg.sh)
+  return 256;  // measured best for every R101 conv shape at batch 256 (tools/sweep_cfg.sh)
 }
 
 // fused masker dots riding on a dense 1x1 conv (ConvParams::adot_*)
