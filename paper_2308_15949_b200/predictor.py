@@ -28,6 +28,7 @@ from .core import BlockSpec, DynamicConfig, Paradigm
 DATA = Path(__file__).resolve().parent / "data"
 _PEAKS_FALLBACK = {"hbm_gbs": 6551.7, "bf16_tflops_sustained": 1384.1}
 CLASSES = ("conv_gather", "conv_dense", "masker", "small")
+CHANNEL_DENSE_MIN = 8  # LAUD_CH_DENSE_MIN default: batch from which channel blocks run dense-masked
 
 
 @dataclass(frozen=True)
@@ -70,6 +71,11 @@ def block_kernels(block: BlockSpec, cfg: DynamicConfig, rate: float, batch: int,
         pass  # in-place residual: no skip copy
     if p is Paradigm.CHANNEL:
         ks.append(KernelWork("masker", 0.0, 2.0 * pin * cin))
+        if n >= CHANNEL_DENSE_MIN:  # dense-masked schedule (capi.cu channel_forward)
+            conv(pin, pin, cin, cm)
+            conv(pin, pout, cm, cm, taps=9, cls="conv_gather", gdiv=g)
+            conv(pout, pout, cm, co, resid=True)
+            return ks
         ks.append(KernelWork("small", 0.0, wbytes * n * r * r))  # per-sample packed weights
         conv(pin, pin, cin, cm * r, cls="conv_dense")
         conv(pin * r, pout, cm * r, cm * r, taps=9, cls="conv_gather")

@@ -29,6 +29,8 @@ def shape_defs():
     d["two_wave_k256"] = dict(kind="gemm", m=2 * 148 * 128, n=256, k=256)
     d["four_wave_k256"] = dict(kind="gemm", m=4 * 148 * 128, n=256, k=256)
     d["conv2_s3"] = dict(kind="conv3x3", n=256, h=14, c=256)
+    d["conv2_s3_b1"] = dict(kind="conv3x3", n=1, h=14, c=256)   # batch-1 latency shapes
+    d["conv1_s3_b1"] = dict(kind="gemm", m=196, n=256, k=1024)
     d["conv2_s3_r05"] = dict(kind="conv3x3", n=128, h=14, c=256)  # 25088 rows = stage-3 conv2 at r=0.5
     d["conv2_s2"] = dict(kind="conv3x3", n=256, h=28, c=128)
     d["conv2_s1"] = dict(kind="conv3x3", n=256, h=56, c=64)
