@@ -15,6 +15,8 @@ from pathlib import Path
 from .errors import DeviceError, GranularityMismatch, MaskShapeMismatch, ShapeMismatch
 
 _SO = Path(__file__).resolve().parent / "_laud.so"
+if os.environ.get("LAUD_SO_VARIANT"):  # tools/ab.sh: A/B two in-tree builds in one run
+    _SO = _SO.with_name(f"_laud_{os.environ['LAUD_SO_VARIANT']}.so")
 
 OK, ERR_GRANULARITY, ERR_MASK_SHAPE, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CUDA, ERR_ARG = range(7)
 PARADIGM = {"spatial": 0, "channel": 1, "layer": 2, "static": 3}

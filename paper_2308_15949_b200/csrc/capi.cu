@@ -417,12 +417,6 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
       }
     }
   }
-  // gathered (non-contiguous, non-compact) A rows: split across TMA gather4 and cp.async
-  static const int hybrid_env = [] {  // opt-in: measured slower on B200 (conv2 85 -> 93 us)
-    const char* e = getenv("LAUD_A_HYBRID");
-    return e ? atoi(e) : 0;
-  }();
-  p.a_hybrid = hybrid_env && p.a_tma && !p.a_tile && !a->a_compact;
   // CTA pairs (cta_group::2, M = 256): long-K wide tiles with contiguous A rows and
   // enough rows to fill the TPCs (measured: short K loses, gathered A gains nothing)
   static const int pair_env = [] {

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // arrivals: A expect_tx (TMA) or 128 cp.async threads, hybrid both halves, + B
-      mbar_init(&full[s], p.a_hybrid ? 1 + 64 + 1 : (p.a_tma ? 2 : 128 + 1));
+      mbar_init(&full[s], p.a_tma ? 2 : 128 + 1);
       mbar_init(&empty[s], p.adot_out ? 2 : 1);  // + the fused masker readers
     }
     for (int a = 0; a < 2; ++a) {
@@ -301,69 +301,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES);
               tma_load_2d(sA, &tmap_a, &full[stage], ti.c_lo + kb * BK, row0);
             }
-          }
-        }
-      }
-    } else if (p.a_hybrid) {
-      // Gathered rows split across two copy engines: rows 0-63 by TMA
-      // tile::gather4 (warps 0-1), rows 64-127 by cp.async through the LSU
-      // (warps 2-3, each thread one 16-byte chunk of 8 rows): the TMA unit's
-      // per-instruction rate no longer bounds the A stream alone.
-      const __nv_bfloat16* act = reinterpret_cast<const __nv_bfloat16*>(p.act);
-      const bool tma_half = tid < 64;
-      const int chunk = tid & 7, rsub = (tid - 64) >> 3;  // cp.async half: rows 64 + rsub + 8 i
-      for (int t = t_begin; t < tiles; t += t_step) {
-        const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
-        if (ti.skip) continue;
-        const int m0 = ti.m0;
-        RowPos rp[8];
-        bool rv[8];
-        if (tma_half) {
-          bool fp;
-          rv[0] = map_row(p, m0 + tid, nvalid, rp[0], fp);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            bool fp;
-            rv[i] = map_row(p, m0 + 64 + rsub + 8 * i, nvalid, rp[i], fp);
-          }
-        }
-        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
-          const int stage = it % STAGES;
-          const uint32_t phase = (it / STAGES) & 1;
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (trc && tid == 0 && it < 4096) trc[TRACE_A + it] = global_ns();
-          const int tap = kb / ti.kpt;
-          const int c0 = ti.c_lo + (kb - tap * ti.kpt) * BK;
-          const int ky = tap / p.ksize;
-          const int kx = tap - ky * p.ksize;
-          const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
-          if (tma_half) {
-            int row = p.a_rows;  // out of bounds -> zero fill
-            if (rv[0]) {
-              const int iy = rp[0].y * p.stride + ky - p.pad;
-              const int ix = rp[0].x * p.stride + kx - p.pad;
-              if (iy >= 0 && iy < p.in_h && ix >= 0 && ix < p.in_w) row = (rp[0].n * p.in_h + iy) * p.in_w + ix;
-            }
-            const int r1 = __shfl_down_sync(0xffffffffu, row, 1);
-            const int r2 = __shfl_down_sync(0xffffffffu, row, 2);
-            const int r3 = __shfl_down_sync(0xffffffffu, row, 3);
-            if (tid == 0) mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES / 2);
-            if ((lane & 3) == 0) tma_gather4(sA + tid * 128, &tmap_a, &full[stage], c0, row, r1, r2, r3);
-          } else {
-            const int ch = c0 + chunk * 8;
-            const bool chv = ch < p.in_c;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = 64 + rsub + 8 * i;
-              const uint32_t dst = sA + r * 128 + ((chunk ^ (r & 7)) << 4);
-              const int iy = rp[i].y * p.stride + ky - p.pad;
-              const int ix = rp[i].x * p.stride + kx - p.pad;
-              const bool v = rv[i] && chv && iy >= 0 && iy < p.in_h && ix >= 0 && ix < p.in_w;
-              const __nv_bfloat16* src = act + ((size_t)(rp[i].n * p.in_h + iy) * p.in_w + ix) * p.in_ld + ch;
-              cp_async_16(dst, v ? (const void*)src : (const void*)act, v ? 16u : 0u);
-            }
-            cp_async_mbar_arrive_noinc(&full[stage]);
           }
         }
       }

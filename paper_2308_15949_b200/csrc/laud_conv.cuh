@@ -35,7 +35,6 @@ struct ConvParams {
   int a_compact;         // 1: A row = m directly (1x1, taps must be 1)
   int a_tma;             // 1: A rows gathered with TMA tile::gather4 (else cp.async)
   int a_tile;            // 1: the 128 A rows of a tile are contiguous: one 2D TMA box
-  int a_hybrid;          // 1: gathered rows split between TMA gather4 and cp.async
   int a_box;             // 1: S x S patch rows loaded as one 4D TMA box per patch and tap
   // fused masker (dense 1x1 conv1 with contiguous A rows, a_tile): idle producer
   // warps read each A stage from smem and accumulate dot(x_row, adot_w) per row;
