@@ -142,7 +142,11 @@ struct Smem {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 
-template <int BN, int STAGES, int NSTG, bool PAIR>
+// A-operand producer compiled into an instantiation (the kernel carries every
+// role; keeping only the launch's A path shrinks the code the warps fetch)
+enum AMode { AM_TILE = 0, AM_BOX = 1, AM_G4 = 2, AM_ANY = 3 };
+
+template <int BN, int STAGES, int NSTG, bool PAIR, int AM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      const ConvParams p) {
@@ -217,7 +221,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ A producers
     const int tid = threadIdx.x;
     uint32_t it = 0;
-    if (p.a_tile && p.adot_out && warp >= 1) {
+    constexpr bool kTile = AM == AM_TILE || AM == AM_ANY;
+    constexpr bool kBox = AM == AM_BOX || AM == AM_ANY;
+    constexpr bool kG4 = AM == AM_G4 || AM == AM_ANY;
+    if (kTile && p.a_tile && p.adot_out && warp >= 1) {
       // fused masker readers (warps 1-3): every A stage, once landed, is also
       // read here — dot of each row with the masker weights W0 - W1
       // (`reference.py:244-253`) — and released with a second arrive
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (rb < BM) add(rb, acc_b);
         }
       }
-    } else if (p.a_tile) {
+    } else if (kTile && p.a_tile) {
       // Contiguous rows (compact / dense 1x1): one 128 x 64 TMA box per stage.
       if (tid == 0) {
         for (int t = t_begin; t < tiles; t += t_step) {
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-    } else if (p.a_box) {
+    } else if (kBox && p.a_box) {
       // S x S patches: thread i < 128 / S^2 owns patch i of the tile and loads its
       // tap window as one 4D box (S^2 rows x 64 channels, OOB -> zero halo)
       const int s2 = p.patch_h * p.patch_w;
@@ -337,7 +344,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (tid < ppt) tma_load_4d(sA + tid * s2 * 128, &tmap_a, &full[stage], c0, bx + kx, by + ky, bn_);
         }
       }
-    } else if (p.a_tma) {
+    } else if (kG4 && p.a_tma) {
       // One output row per thread; per (tap, channel block) every 4th lane issues
       // a TMA tile::gather4 of its 4 rows' source pixels (OOB index -> zeros).
       for (int t = t_begin; t < tiles; t += t_step) {
@@ -380,7 +387,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-    } else {
+    } else if (AM == AM_ANY) {
     const int chunk = tid & 7;
     const int rsub = tid >> 3;
     const __nv_bfloat16* act = reinterpret_cast<const __nv_bfloat16*>(p.act);
@@ -885,12 +892,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // host side
 // ---------------------------------------------------------------------------
 
-template <int BN, int STAGES, int NSTG, bool PAIR = false>
+template <int BN, int STAGES, int NSTG, bool PAIR = false, int AM = AM_ANY>
 static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const ConvParams& p, int tiles_max,
                              int num_sms, cudaStream_t stream) {
   using L = Smem<BN, STAGES, NSTG, PAIR>;
   static_assert(L::ALLOC <= 227 * 1024, "shared memory budget");
-  auto kern = conv_gemm_kernel<BN, STAGES, NSTG, PAIR>;
+  auto kern = conv_gemm_kernel<BN, STAGES, NSTG, PAIR, AM>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
@@ -937,17 +944,28 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   if (pair) {
     if (bn != 256) return cudaErrorInvalidValue;
     const int tiles_max = ((p.rows_max + 2 * BM - 1) / (2 * BM)) * n_tiles;
+    if (!p.a_tile) return cudaErrorInvalidValue;  // pairs run contiguous (TMA box) A rows only
     if (pair == 2)  // short K: 2 operand stages, double-buffered epilogue staging
-      return launch_bn<256, 2, 2, true>(tmap_a, tmap, p, tiles_max, num_sms, stream);
-    return launch_bn<256, 4, 1, true>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+      return launch_bn<256, 2, 2, true, AM_TILE>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+    return launch_bn<256, 4, 1, true, AM_TILE>(tmap_a, tmap, p, tiles_max, num_sms, stream);
   }
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
+  const int am = p.a_tile ? AM_TILE : p.a_box ? AM_BOX : p.a_tma ? AM_G4 : AM_ANY;
+#define LAUD_BN_CASE(B, S, N)                                                            \
+  case B:                                                                                \
+    switch (am) {                                                                        \
+      case AM_TILE: return launch_bn<B, S, N, false, AM_TILE>(tmap_a, tmap, p, tiles_max, num_sms, stream); \
+      case AM_BOX: return launch_bn<B, S, N, false, AM_BOX>(tmap_a, tmap, p, tiles_max, num_sms, stream);   \
+      case AM_G4: return launch_bn<B, S, N, false, AM_G4>(tmap_a, tmap, p, tiles_max, num_sms, stream);     \
+      default: return launch_bn<B, S, N, false, AM_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream);       \
+    }
   switch (bn) {
-    case 64: return launch_bn<64, 6, 2>(tmap_a, tmap, p, tiles_max, num_sms, stream);
-    case 128: return launch_bn<128, 4, 2>(tmap_a, tmap, p, tiles_max, num_sms, stream);
-    case 256: return launch_bn<256, 3, 1>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+    LAUD_BN_CASE(64, 6, 2)
+    LAUD_BN_CASE(128, 4, 2)
+    LAUD_BN_CASE(256, 3, 1)
     default: return cudaErrorInvalidValue;
   }
+#undef LAUD_BN_CASE
 }
 
 }  // namespace laud
