@@ -144,9 +144,12 @@ struct Smem {
 
 // A-operand producer compiled into an instantiation (the kernel carries every
 // role; keeping only the launch's A path shrinks the code the warps fetch)
-enum AMode { AM_TILE = 0, AM_BOX = 1, AM_G4 = 2, AM_ANY = 3 };
+enum AMode { AM_TILE = 0, AM_BOX = 1, AM_G4 = 2, AM_ANY = 3, AM_TILE_DOT = 4 };
+// epilogue compiled in: EP_PLAIN = bf16 out, bias from the smem cache, optional
+// residual / ReLU / per-sample channel mask, every warp slice full; EP_ANY = all
+enum EpMode { EP_PLAIN = 0, EP_ANY = 1 };
 
-template <int BN, int STAGES, int NSTG, bool PAIR, int AM>
+template <int BN, int STAGES, int NSTG, bool PAIR, int AM, int EP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      const ConvParams p) {
@@ -221,10 +224,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ A producers
     const int tid = threadIdx.x;
     uint32_t it = 0;
-    constexpr bool kTile = AM == AM_TILE || AM == AM_ANY;
+    constexpr bool kTile = AM == AM_TILE || AM == AM_TILE_DOT || AM == AM_ANY;
+    constexpr bool kDot = AM == AM_TILE_DOT || AM == AM_ANY;
     constexpr bool kBox = AM == AM_BOX || AM == AM_ANY;
     constexpr bool kG4 = AM == AM_G4 || AM == AM_ANY;
-    if (kTile && p.a_tile && p.adot_out && warp >= 1) {
+    if (kDot && p.a_tile && p.adot_out && warp >= 1) {
       // fused masker readers (warps 1-3): every A stage, once landed, is also
       // read here — dot of each row with the masker weights W0 - W1
       // (`reference.py:244-253`) — and released with a second arrive
@@ -541,10 +545,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool pre = staged && resid != nullptr;
     const bool has_scale = p.scale != nullptr || p.col_index != nullptr;
     // the common epilogues (bias [+ residual] [+ ReLU]) take a branch-free path
-    const bool plain = staged && !has_scale && !p.ymask_coarse && !p.mdot_w;
+    constexpr bool kPlain = EP == EP_PLAIN;  // host guarantees plain && cached && full slices
+    const bool plain = kPlain || (staged && !has_scale && !p.ymask_coarse && !p.mdot_w);
     // the whole bias vector lives in smem for the kernel when it fits (the
     // per-warp vector slices are the fallback for scale / masker-dot / lists)
-    const bool cached = !has_scale && !p.mdot_w && p.n_out <= L::VEC_BYTES / 4;
+    const bool cached = kPlain || (!has_scale && !p.mdot_w && p.n_out <= L::VEC_BYTES / 4);
     float* const bias_cache = reinterpret_cast<float*>(base + L::VEC_OFF);
     if (cached) {
       for (int i = threadIdx.x - FIRST_EPI * 32; i < p.n_out; i += NUM_EPI_WARPS * 32)
@@ -732,7 +737,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           w.z = pack_bf16x2(v[4], v[5]);
           w.w = pack_bf16x2(v[6], v[7]);
           *slot = w;
-          if (p.mdot_w) {  // the stored (bf16) values are what the next masker sees
+          if (!kPlain && p.mdot_w) {  // the stored (bf16) values are what the next masker sees
             const float4 n0 = *reinterpret_cast<const float4*>(vnw + cl);
             const float4 n1 = *reinterpret_cast<const float4*>(vnw + cl + 4);
             float2 f;
@@ -801,7 +806,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int e = 0; e < CH; ++e) r[e] = 0u;
         }
         if (!cur.valid || (p.dbg & 1)) continue;
-        if (plain && full) {
+        if (kPlain || (plain && full)) {
           if (pre) {
             if (do_relu) plain_chunk(r, j * CH, true, true);
             else plain_chunk(r, j * CH, true, false);
@@ -809,7 +814,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (do_relu) plain_chunk(r, j * CH, false, true);
             else plain_chunk(r, j * CH, false, false);
           }
-        } else {
+        } else if constexpr (!kPlain) {
 #pragma unroll
           for (int g = 0; g < CH / 8; ++g) {
             if (j * CH + g * 8 >= nch) break;
@@ -817,7 +822,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-      if (p.mdot_w) {
+      if (!kPlain && p.mdot_w) {
         // rows of one patch are consecutive lanes: reduce per patch, one atomic each
         const int seg = p.patch_h * p.patch_w;
         if (seg <= 32 && (32 % seg) == 0) {
@@ -892,12 +897,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // host side
 // ---------------------------------------------------------------------------
 
-template <int BN, int STAGES, int NSTG, bool PAIR = false, int AM = AM_ANY>
+template <int BN, int STAGES, int NSTG, bool PAIR = false, int AM = AM_ANY, int EP = EP_ANY>
 static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const ConvParams& p, int tiles_max,
                              int num_sms, cudaStream_t stream) {
   using L = Smem<BN, STAGES, NSTG, PAIR>;
   static_assert(L::ALLOC <= 227 * 1024, "shared memory budget");
-  auto kern = conv_gemm_kernel<BN, STAGES, NSTG, PAIR, AM>;
+  auto kern = conv_gemm_kernel<BN, STAGES, NSTG, PAIR, AM, EP>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
@@ -941,23 +946,33 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
 cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
                              cudaStream_t stream, int pair) {
   const int n_tiles = (p.n_out + bn - 1) / bn;
+  // EP_PLAIN: bf16 out, no per-channel scale / coarse mask / masker-dot, bias
+  // vector fits the smem cache (12 * BN floats), every warp slice full
+  const bool ep_plain = !p.out_f32 && !p.scale && !p.col_index && !p.ymask_coarse && !p.mdot_w &&
+                        p.n_out <= 12 * bn && p.n_out % bn == 0;
   if (pair) {
     if (bn != 256) return cudaErrorInvalidValue;
     const int tiles_max = ((p.rows_max + 2 * BM - 1) / (2 * BM)) * n_tiles;
-    if (!p.a_tile) return cudaErrorInvalidValue;  // pairs run contiguous (TMA box) A rows only
+    if (!p.a_tile || p.adot_out) return cudaErrorInvalidValue;  // pairs: TMA-box A rows, no masker readers
     if (pair == 2)  // short K: 2 operand stages, double-buffered epilogue staging
-      return launch_bn<256, 2, 2, true, AM_TILE>(tmap_a, tmap, p, tiles_max, num_sms, stream);
-    return launch_bn<256, 4, 1, true, AM_TILE>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+      return ep_plain ? launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream)
+                      : launch_bn<256, 2, 2, true, AM_TILE, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+    return ep_plain ? launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream)
+                    : launch_bn<256, 4, 1, true, AM_TILE, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream);
   }
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
-  const int am = p.a_tile ? AM_TILE : p.a_box ? AM_BOX : p.a_tma ? AM_G4 : AM_ANY;
-#define LAUD_BN_CASE(B, S, N)                                                            \
-  case B:                                                                                \
-    switch (am) {                                                                        \
-      case AM_TILE: return launch_bn<B, S, N, false, AM_TILE>(tmap_a, tmap, p, tiles_max, num_sms, stream); \
-      case AM_BOX: return launch_bn<B, S, N, false, AM_BOX>(tmap_a, tmap, p, tiles_max, num_sms, stream);   \
-      case AM_G4: return launch_bn<B, S, N, false, AM_G4>(tmap_a, tmap, p, tiles_max, num_sms, stream);     \
-      default: return launch_bn<B, S, N, false, AM_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream);       \
+  const int am = p.a_tile ? (p.adot_out ? AM_TILE_DOT : AM_TILE) : p.a_box ? AM_BOX : p.a_tma ? AM_G4 : AM_ANY;
+#define LAUD_LB(B, S, N, A)                                                                          \
+  (ep_plain ? launch_bn<B, S, N, false, A, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream)    \
+            : launch_bn<B, S, N, false, A, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream))
+#define LAUD_BN_CASE(B, S, N)                                     \
+  case B:                                                         \
+    switch (am) {                                                 \
+      case AM_TILE: return LAUD_LB(B, S, N, AM_TILE);             \
+      case AM_TILE_DOT: return LAUD_LB(B, S, N, AM_TILE_DOT);     \
+      case AM_BOX: return LAUD_LB(B, S, N, AM_BOX);               \
+      case AM_G4: return LAUD_LB(B, S, N, AM_G4);                 \
+      default: return LAUD_LB(B, S, N, AM_ANY);                   \
     }
   switch (bn) {
     LAUD_BN_CASE(64, 6, 2)
@@ -966,6 +981,7 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
     default: return cudaErrorInvalidValue;
   }
 #undef LAUD_BN_CASE
+#undef LAUD_LB
 }
 
 }  // namespace laud
