@@ -147,7 +147,7 @@ struct Smem {
 enum AMode { AM_TILE = 0, AM_BOX = 1, AM_G4 = 2, AM_ANY = 3, AM_TILE_DOT = 4 };
 // epilogue compiled in: EP_PLAIN = bf16 out, bias from the smem cache, optional
 // residual / ReLU / per-sample channel mask, every warp slice full; EP_ANY = all
-enum EpMode { EP_PLAIN = 0, EP_ANY = 1 };
+enum EpMode { EP_PLAIN = 0, EP_ANY = 1, EP_PLAIN_RES = 2 };  // _RES: with the residual add
 
 template <int BN, int STAGES, int NSTG, bool PAIR, int AM, int EP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -542,10 +542,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const __nv_bfloat16* resid = reinterpret_cast<const __nv_bfloat16*>(p.resid);
     __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
     const bool staged = !p.out_f32;
-    const bool pre = staged && resid != nullptr;
+    const bool pre = EP == EP_PLAIN_RES ? true : EP == EP_PLAIN ? false : (staged && resid != nullptr);
     const bool has_scale = p.scale != nullptr || p.col_index != nullptr;
     // the common epilogues (bias [+ residual] [+ ReLU]) take a branch-free path
-    constexpr bool kPlain = EP == EP_PLAIN;  // host guarantees plain && cached && full slices
+    constexpr bool kPlain = EP == EP_PLAIN || EP == EP_PLAIN_RES;  // host: plain && cached && full slices
     const bool plain = kPlain || (staged && !has_scale && !p.ymask_coarse && !p.mdot_w);
     // the whole bias vector lives in smem for the kernel when it fits (the
     // per-warp vector slices are the fallback for scale / masker-dot / lists)
@@ -955,16 +955,19 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
     const int tiles_max = ((p.rows_max + 2 * BM - 1) / (2 * BM)) * n_tiles;
     if (!p.a_tile || p.adot_out) return cudaErrorInvalidValue;  // pairs: TMA-box A rows, no masker readers
     if (pair == 2)  // short K: 2 operand stages, double-buffered epilogue staging
-      return ep_plain ? launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream)
-                      : launch_bn<256, 2, 2, true, AM_TILE, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream);
-    return ep_plain ? launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream)
-                    : launch_bn<256, 4, 1, true, AM_TILE, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+      return !ep_plain ? launch_bn<256, 2, 2, true, AM_TILE, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream)
+             : p.resid ? launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN_RES>(tmap_a, tmap, p, tiles_max, num_sms, stream)
+                       : launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream);
+    return !ep_plain ? launch_bn<256, 4, 1, true, AM_TILE, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream)
+           : p.resid ? launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN_RES>(tmap_a, tmap, p, tiles_max, num_sms, stream)
+                     : launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream);
   }
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
   const int am = p.a_tile ? (p.adot_out ? AM_TILE_DOT : AM_TILE) : p.a_box ? AM_BOX : p.a_tma ? AM_G4 : AM_ANY;
-#define LAUD_LB(B, S, N, A)                                                                          \
-  (ep_plain ? launch_bn<B, S, N, false, A, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream)    \
-            : launch_bn<B, S, N, false, A, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream))
+#define LAUD_LB(B, S, N, A)                                                                                \
+  (!ep_plain ? launch_bn<B, S, N, false, A, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream)            \
+   : p.resid ? launch_bn<B, S, N, false, A, EP_PLAIN_RES>(tmap_a, tmap, p, tiles_max, num_sms, stream)      \
+             : launch_bn<B, S, N, false, A, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream))
 #define LAUD_BN_CASE(B, S, N)                                     \
   case B:                                                         \
     switch (am) {                                                 \
