@@ -234,6 +234,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // (`reference.py:244-253`) — and released with a second arrive
       const int mt = tid - 32;  // 0 .. 95: rows mt and mt + 96 (< 128)
       const int ra = mt, rb = mt + 96;
+      // plain-epilogue kernels only use the bias part of the vector region: the
+      // masker weights live at its top for the whole kernel (host checks the fit)
+      float* const wsm = reinterpret_cast<float*>(base + L::VEC_OFF + L::VEC_BYTES) - p.kpad;
+      if constexpr (EP != EP_ANY) {
+        for (int i = mt; i < p.kpad; i += 96) wsm[i] = __ldg(p.adot_w + i);
+        asm volatile("bar.sync 3, 96;" ::: "memory");
+      }
       for (int t = t_begin; t < tiles; t += t_step) {
         const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
         if (ti.skip) continue;
@@ -245,7 +252,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&full[stage], phase);
           const uint8_t* sA = base + L::A_OFF + stage * A_STAGE_BYTES;
           if (dots) {
-            const float* wv = p.adot_w + kb * BK;
             uint4 va[8], vb[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -255,8 +261,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              const float4 w0 = __ldg(reinterpret_cast<const float4*>(wv + c * 8));
-              const float4 w1 = __ldg(reinterpret_cast<const float4*>(wv + c * 8 + 4));
+              float4 w0, w1;
+              if constexpr (EP != EP_ANY) {
+                w0 = *reinterpret_cast<const float4*>(wsm + kb * BK + c * 8);
+                w1 = *reinterpret_cast<const float4*>(wsm + kb * BK + c * 8 + 4);
+              } else {
+                w0 = __ldg(reinterpret_cast<const float4*>(p.adot_w + kb * BK + c * 8));
+                w1 = __ldg(reinterpret_cast<const float4*>(p.adot_w + kb * BK + c * 8 + 4));
+              }
               const int k = c & 3;
               float2 f;
               f = unpack_bf16x2(va[c].x); aa[k] = fmaf(f.x, w0.x, aa[k]); aa[k] = fmaf(f.y, w0.y, aa[k]);
@@ -949,7 +961,8 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   // EP_PLAIN: bf16 out, no per-channel scale / coarse mask / masker-dot, bias
   // vector fits the smem cache (12 * BN floats), every warp slice full
   const bool ep_plain = !p.out_f32 && !p.scale && !p.col_index && !p.ymask_coarse && !p.mdot_w &&
-                        p.n_out <= 12 * bn && p.n_out % bn == 0;
+                        p.n_out <= 12 * bn && p.n_out % bn == 0 &&
+                        (!p.adot_out || p.n_out + p.kpad <= 12 * bn);  // + masker weights in smem
   if (pair) {
     if (bn != 256) return cudaErrorInvalidValue;
     const int tiles_max = ((p.rows_max + 2 * BM - 1) / (2 * BM)) * n_tiles;
