@@ -123,7 +123,12 @@ struct Smem {
   static constexpr int B_STAGE_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's B rows
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
-  static constexpr int EW_COLS0 = BN / (NUM_EPI_WARPS / 4);
+  // narrow tiles (BN <= 128, two staging buffers): the epilogue warps form two
+  // groups that finish alternate tiles concurrently (each group its own
+  // staging buffer and TMEM accumulators), so per-tile epilogue latency overlaps
+  static constexpr int EG = (BN <= 128 && NSTG == 2 && !PAIR) ? 2 : 1;
+  static constexpr int NACC = 2 * EG;  // TMEM accumulators in flight
+  static constexpr int EW_COLS0 = BN / (NUM_EPI_WARPS / EG / 4);
   // staging rows: 16-byte chunks XOR-swizzled by row when a warp's slice is 8
   // chunks wide (conflict-free row-per-lane and row-major access, no padding);
   // narrower slices are padded instead
@@ -132,14 +137,14 @@ struct Smem {
   static constexpr int STG_OFF = B_OFF + STAGES * B_STAGE_BYTES;
   static constexpr int STG_BUF = BM * STG_ROW;  // one staging buffer
   static constexpr int VEC_OFF = STG_OFF + NSTG * STG_BUF;  // per-warp scale/bias slices
-  static constexpr int EW_COLS = BN / (NUM_EPI_WARPS / 4);  // columns per epilogue warp
+  static constexpr int EW_COLS = EW_COLS0;  // columns per epilogue warp
   static constexpr int VEC_BYTES = NUM_EPI_WARPS * 3 * EW_COLS * 4;  // scale, bias, next wdiff
   static constexpr int BAR_OFF = VEC_OFF + VEC_BYTES;
-  static constexpr int NUM_BARS = 2 * STAGES + 4;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NACC;
   static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
   static constexpr int BYTES = TMEM_SLOT_OFF + 16;
   static constexpr int ALLOC = BYTES + 1024;  // manual 1 KiB alignment
-  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr uint32_t TMEM_COLS = NACC * BN;
 };
 
 // A-operand producer compiled into an instantiation (the kernel carries every
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* acc_full = bars + 2 * STAGES;
-  uint64_t* acc_empty = bars + 2 * STAGES + 2;
+  uint64_t* acc_empty = bars + 2 * STAGES + L::NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::TMEM_SLOT_OFF);
 
   const int warp = threadIdx.x >> 5;
@@ -180,9 +185,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&full[s], p.a_tma ? 2 : 128 + 1);
       mbar_init(&empty[s], p.adot_out ? 2 : 1);  // + the fused masker readers
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < L::NACC; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], (PAIR ? 2 : 1) * NUM_EPI_WARPS);  // one arrive per epilogue warp
+      mbar_init(&acc_empty[a], (PAIR ? 2 : 1) * NUM_EPI_WARPS / L::EG);  // one arrive per group warp
     }
     fence_barrier_init();
   }
@@ -486,8 +491,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int t = t_begin; t < tiles && leader; t += t_step) {
       const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
       if (ti.skip) continue;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = local % L::NACC;
+      const uint32_t acc_phase = (local / L::NACC) & 1;
       ++local;
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -544,8 +549,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr int CH = EW_COLS < 32 ? EW_COLS : 32;  // columns per TMEM load
     const int q = warp & 3;
     const int ew = warp - FIRST_EPI;
-    const int col0 = (ew >> 2) * EW_COLS;
-    const int stg_off0 = L::STG_OFF + q * 32 * L::STG_ROW + col0 * 2;
+    constexpr int GW = NUM_EPI_WARPS / L::EG;  // warps per epilogue group
+    const int grp = ew / GW;                     // group: tiles with local % EG == grp
+    const int col0 = ((ew % GW) >> 2) * EW_COLS;
+    // one staging buffer per group; with one group and two buffers the next
+    // tile's residual is prefetched into the other buffer
+    constexpr bool kDoubleStage = NSTG == 2 && L::EG == 1;
+    const int stg_off0 = L::STG_OFF + grp * L::STG_BUF + q * 32 * L::STG_ROW + col0 * 2;
     // byte offset of 16-byte chunk c of slice row r (relative to stg_off0)
     auto soff = [](int r, int c) { return r * L::STG_ROW + ((L::STG_SWZ ? (c ^ (r & 7)) : c) << 4); };
     float* const vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + ew * 3 * EW_COLS;
@@ -654,6 +664,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     uint32_t local = 0;
     int t = next_valid(t_begin);
+    if (grp > 0 && t < tiles) {  // group g starts at the CTA's g-th tile
+      t = next_valid(t + t_step);
+      local = 1;
+    }
     RowInfo cur;
     if (t < tiles) {
       cur = row_info(t, row_raw(t));
@@ -661,11 +675,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (!cached) vec_store(vec_load(t));
       __syncwarp();
     }
-    for (; t < tiles; ++local) {
+    for (; t < tiles; local += L::EG) {
       const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      const int buf = NSTG == 2 ? (local & 1) : 0;
+      const int acc = local % L::NACC;
+      const uint32_t acc_phase = (local / L::NACC) & 1;
+      const int buf = kDoubleStage ? (local & 1) : 0;
       uint8_t* stg = base + stg_off0 + buf * L::STG_BUF;
       const int c_base = ti.n0 + col0;                        // first output channel of this warp
       const int nch = max(0, min(EW_COLS, p.n_out - c_base));  // valid channels (multiple of 8)
@@ -679,7 +693,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.ymask_coarse) ymul = p.ymask_coarse[cell] ? 1.f : 0.f;
       }
       // next tile's rows and vectors: issue the global loads now, use them later
-      const int tn = next_valid(t + t_step);
+      int tn = next_valid(t + t_step);  // this group's next tile: EG tiles on
+      if (L::EG > 1 && tn < tiles) tn = next_valid(tn + t_step);
       RowInfo nxt = cur;
       VecPre vpn;
       int raw_n = 0;
@@ -865,7 +880,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         nxt = row_info(tn, raw_n);
         if (!cached) vec_store(vpn);  // this tile's vector reads are done (syncwarp above)
         // with two staging buffers the next residual streams in now
-        if (pre && NSTG == 2) prefetch(tn, nxt, (local + 1) & 1);
+        if (pre && kDoubleStage) prefetch(tn, nxt, (local + 1) & 1);
       }
       if (staged && vchunks > 0 && !(p.dbg & 2)) {
         // row-major sweep of the staged 32 x EW_COLS slice: each instruction
@@ -885,7 +900,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       __syncwarp();
       if (trc && ew == 0 && lane == 0 && local < 1024) trc[TRACE_EPI + 4 * local + 2] = global_ns();
-      if (tn < tiles && pre && NSTG == 1) prefetch(tn, nxt, 0);
+      if (tn < tiles && pre && !kDoubleStage) prefetch(tn, nxt, 0);
       cur = nxt;
       t = tn;
     }
