@@ -152,7 +152,8 @@ struct Smem {
 enum AMode { AM_TILE = 0, AM_BOX = 1, AM_G4 = 2, AM_ANY = 3, AM_TILE_DOT = 4 };
 // epilogue compiled in: EP_PLAIN = bf16 out, bias from the smem cache, optional
 // residual / ReLU / per-sample channel mask, every warp slice full; EP_ANY = all
-enum EpMode { EP_PLAIN = 0, EP_ANY = 1, EP_PLAIN_RES = 2 };  // _RES: with the residual add
+// _RES: with the residual add; _RELU: ReLU on every row (no per-cell ReLU mask)
+enum EpMode { EP_PLAIN = 0, EP_ANY = 1, EP_PLAIN_RES = 2, EP_PLAIN_RELU = 4, EP_PLAIN_RES_RELU = 6 };
 
 template <int BN, int STAGES, int NSTG, bool PAIR, int AM, int EP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -564,10 +565,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const __nv_bfloat16* resid = reinterpret_cast<const __nv_bfloat16*>(p.resid);
     __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
     const bool staged = !p.out_f32;
-    const bool pre = EP == EP_PLAIN_RES ? true : EP == EP_PLAIN ? false : (staged && resid != nullptr);
+    constexpr bool kRes = EP == EP_PLAIN_RES || EP == EP_PLAIN_RES_RELU;
+    constexpr bool kReluAll = EP == EP_PLAIN_RELU || EP == EP_PLAIN_RES_RELU;
+    const bool pre = EP != EP_ANY ? kRes : (staged && resid != nullptr);
     const bool has_scale = p.scale != nullptr || p.col_index != nullptr;
     // the common epilogues (bias [+ residual] [+ ReLU]) take a branch-free path
-    constexpr bool kPlain = EP == EP_PLAIN || EP == EP_PLAIN_RES;  // host: plain && cached && full slices
+    constexpr bool kPlain = EP != EP_ANY;  // host: plain && cached && full slices
     const bool plain = kPlain || (staged && !has_scale && !p.ymask_coarse && !p.mdot_w);
     // the whole bias vector lives in smem for the kernel when it fits (the
     // per-warp vector slices are the fallback for scale / masker-dot / lists)
@@ -684,12 +687,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int c_base = ti.n0 + col0;                        // first output channel of this warp
       const int nch = max(0, min(EW_COLS, p.n_out - c_base));  // valid channels (multiple of 8)
       const int vchunks = nch >> 3;
-      bool do_relu = p.relu != 0;
+      bool do_relu = kReluAll || p.relu != 0;
       float ymul = 1.f;
       if (cur.valid && (p.relu_inactive_coarse || p.ymask_coarse)) {
         const RowPos& rp = cur.rp;
         const int cell = (rp.n * p.cells_h + rp.y / p.patch_h) * p.cells_w + rp.x / p.patch_w;
-        if (p.relu_inactive_coarse) do_relu = p.relu_inactive_coarse[cell] == 0;
+        if (!kReluAll && p.relu_inactive_coarse) do_relu = p.relu_inactive_coarse[cell] == 0;
         if (p.ymask_coarse) ymul = p.ymask_coarse[cell] ? 1.f : 0.f;
       }
       // next tile's rows and vectors: issue the global loads now, use them later
@@ -992,10 +995,13 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   }
   const int tiles_max = ((p.rows_max + BM - 1) / BM) * n_tiles;
   const int am = p.a_tile ? (p.adot_out ? AM_TILE_DOT : AM_TILE) : p.a_box ? AM_BOX : p.a_tma ? AM_G4 : AM_ANY;
-#define LAUD_LB(B, S, N, A)                                                                                \
-  (!ep_plain ? launch_bn<B, S, N, false, A, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream)            \
-   : p.resid ? launch_bn<B, S, N, false, A, EP_PLAIN_RES>(tmap_a, tmap, p, tiles_max, num_sms, stream)      \
-             : launch_bn<B, S, N, false, A, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream))
+  const bool relu_all = p.relu && !p.relu_inactive_coarse;
+#define LAUD_LB(B, S, N, A)                                                                                     \
+  (!ep_plain ? launch_bn<B, S, N, false, A, EP_ANY>(tmap_a, tmap, p, tiles_max, num_sms, stream)                 \
+   : p.resid ? (relu_all ? launch_bn<B, S, N, false, A, EP_PLAIN_RES_RELU>(tmap_a, tmap, p, tiles_max, num_sms, stream) \
+                         : launch_bn<B, S, N, false, A, EP_PLAIN_RES>(tmap_a, tmap, p, tiles_max, num_sms, stream))     \
+   : (relu_all ? launch_bn<B, S, N, false, A, EP_PLAIN_RELU>(tmap_a, tmap, p, tiles_max, num_sms, stream)             \
+               : launch_bn<B, S, N, false, A, EP_PLAIN>(tmap_a, tmap, p, tiles_max, num_sms, stream)))
 #define LAUD_BN_CASE(B, S, N)                                     \
   case B:                                                         \
     switch (am) {                                                 \
