@@ -26,10 +26,15 @@ def main():
             db.forward(x.clone(), "spatial", s, conv1_dense=dense)
         db.forward(x.clone(), "static")
         db.forward(x.clone(), "layer", coarse=torch.tensor([1, 0], dtype=torch.uint8, device="cuda"))
-        if blk.conv2.groups == 1:
-            cm = torch.zeros(n * db.cmid_p, dtype=torch.uint8, device="cuda")
-            cm[: blk.conv2.out_channels // 2] = 1
-            db.forward(x.clone(), "channel", chmask=cm)
+        db.enable_grouped_channel()  # EXT for grouped conv2 (no-op otherwise)
+        cm = torch.zeros(n * db.cmid_p, dtype=torch.uint8, device="cuda")
+        cm[: blk.conv2.out_channels // 2] = 1
+        db.forward(x.clone(), "channel", chmask=cm)  # per-sample dynamic width (n < 8)
+        n8 = 8  # dense-masked channel schedule (n >= 8)
+        x8 = torch.randn(n8, h, h, db.cin_p, device="cuda").relu_().bfloat16()
+        cm8 = torch.zeros(n8 * db.cmid_p, dtype=torch.uint8, device="cuda")
+        cm8[::3] = 1
+        db.forward(x8, "channel", chmask=cm8)
         torch.cuda.synchronize()
         print("ok", arch, stage, index, flush=True)
 
