@@ -23,8 +23,8 @@
 namespace laud {
 
 constexpr int CT_THREADS = 256;
-constexpr int CT_ITEMS = 4;
-constexpr int CT_TILE = CT_THREADS * CT_ITEMS;  // 1024 items per CTA
+constexpr int CT_ITEMS = 1;
+constexpr int CT_TILE = CT_THREADS * CT_ITEMS;  // 256 items per CTA: wide grids beat short look-back chains (measured)
 
 // Look-back scratch; zero at allocation, restored to zero by the last CTA.
 struct ScanState {
