@@ -77,30 +77,29 @@ __global__ void maxpool3s2_kernel(const __nv_bfloat16* __restrict__ x, int n, in
     const long long t = pix / wo;
     const int oy = (int)(t % ho);
     const int ni = (int)(t / ho);
-    float m[8];
+    // the 9 window loads are issued together (predicated, fully unrolled); bf16
+    // max is exact, so the packed __hmax2 equals the fp32 max of the same values
+    const __nv_bfloat162 ninf = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    __nv_bfloat162 m[4] = {ninf, ninf, ninf, ninf};
 #pragma unroll
-    for (int q = 0; q < 8; ++q) m[q] = -INFINITY;
     for (int dy = 0; dy < 3; ++dy) {
       const int iy = oy * 2 - 1 + dy;
-      if (iy < 0 || iy >= h) continue;
+#pragma unroll
       for (int dx = 0; dx < 3; ++dx) {
         const int ix = ox * 2 - 1 + dx;
-        if (ix < 0 || ix >= w) continue;
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((size_t)(ni * h + iy) * w + ix) * c + cc));
-        const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+        if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((size_t)(ni * h + iy) * w + ix) * c + cc));
+          const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 f = unpack_bf16x2(u[q]);
-          m[2 * q] = fmaxf(m[2 * q], f.x);
-          m[2 * q + 1] = fmaxf(m[2 * q + 1], f.y);
+          for (int q = 0; q < 4; ++q) m[q] = __hmax2(m[q], *reinterpret_cast<const __nv_bfloat162*>(&u[q]));
         }
       }
     }
     uint4 o;
-    o.x = pack_bf16x2(m[0], m[1]);
-    o.y = pack_bf16x2(m[2], m[3]);
-    o.z = pack_bf16x2(m[4], m[5]);
-    o.w = pack_bf16x2(m[6], m[7]);
+    o.x = *reinterpret_cast<const uint32_t*>(&m[0]);
+    o.y = *reinterpret_cast<const uint32_t*>(&m[1]);
+    o.z = *reinterpret_cast<const uint32_t*>(&m[2]);
+    o.w = *reinterpret_cast<const uint32_t*>(&m[3]);
     *reinterpret_cast<uint4*>(y + (size_t)pix * c + cc) = o;
   }
 }

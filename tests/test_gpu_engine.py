@@ -167,3 +167,18 @@ def test_cta_pair_patch_rows_scatter():
     assert err < 6e-3, float(err)
     untouched = ~torch.from_numpy(np.repeat(np.repeat(cz.reshape(n, h // s, h // s), s, 1), s, 2)).cuda()
     assert torch.equal(out[untouched], base[untouched])
+
+
+@pytest.mark.parametrize("n,h,c", [(2, 112, 64), (3, 15, 24), (1, 7, 8)])
+def test_maxpool3s2_matches_torch(n, h, c):
+    """Network glue: 3x3 / stride 2 / pad 1 max-pool (packed bf16 max) bit-exact vs torch."""
+    from paper_2308_15949_b200 import _lib
+    from paper_2308_15949_b200 import device as D
+    D.require_cuda()
+    x = torch.randn(n, h, h, c, device="cuda").bfloat16()
+    ho = (h - 1) // 2 + 1
+    y = torch.empty(n, ho, ho, c, device="cuda", dtype=torch.bfloat16)
+    _lib.call("laud_maxpool3s2", D.ptr(x), n, h, h, c, D.ptr(y), None)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.max_pool2d(x.permute(0, 3, 1, 2).float(), 3, 2, 1).permute(0, 2, 3, 1)
+    assert torch.equal(y.float(), ref)
