@@ -39,13 +39,37 @@ __global__ void stem_im2col_kernel(const uint8_t* __restrict__ img, int n, int h
     if (iy >= 0 && iy < h) {
       const uint8_t* row = img + (size_t)(ni * h + iy) * w * 3;
       const int x0 = ox * stride - pad;
+      constexpr int NA = (3 * K + 3) / 4;  // aligned words covering the window's 3K bytes
+      if (x0 >= 0 && ((w * 3) & 3) == 0 && ((x0 * 3) & ~3) + 4 * (NA + 1) <= w * 3) {
+        // interior: the window's 3K bytes from aligned 32-bit loads (rows start
+        // 4-byte aligned), realigned with funnel shifts, instead of 3K byte loads
+        const int b0 = x0 * 3;
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(row + (b0 & ~3));
+        uint32_t wd[NA + 1];
 #pragma unroll
-      for (int kx = 0; kx < K; ++kx) {
-        const int ix = x0 + kx;
-        if (ix >= 0 && ix < w) {
-          v[kx * 3 + 0] = ((float)row[ix * 3 + 0] - m0) * s0;
-          v[kx * 3 + 1] = ((float)row[ix * 3 + 1] - m1) * s1;
-          v[kx * 3 + 2] = ((float)row[ix * 3 + 2] - m2) * s2;
+        for (int q = 0; q <= NA; ++q) wd[q] = __ldg(wp + q);
+        const uint32_t sh = 8u * (uint32_t)(b0 & 3);
+        uint32_t aw[NA];
+#pragma unroll
+        for (int q = 0; q < NA; ++q) aw[q] = __funnelshift_r(wd[q], wd[q + 1], sh);
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx) {
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const int e = kx * 3 + ch;
+            const float u = (float)((aw[e >> 2] >> (8 * (e & 3))) & 0xffu);
+            v[e] = ch == 0 ? (u - m0) * s0 : ch == 1 ? (u - m1) * s1 : (u - m2) * s2;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx) {
+          const int ix = x0 + kx;
+          if (ix >= 0 && ix < w) {
+            v[kx * 3 + 0] = ((float)row[ix * 3 + 0] - m0) * s0;
+            v[kx * 3 + 1] = ((float)row[ix * 3 + 1] - m1) * s1;
+            v[kx * 3 + 2] = ((float)row[ix * 3 + 2] - m2) * s2;
+          }
         }
       }
     }

@@ -182,3 +182,35 @@ def test_maxpool3s2_matches_torch(n, h, c):
     torch.cuda.synchronize()
     ref = torch.nn.functional.max_pool2d(x.permute(0, 3, 1, 2).float(), 3, 2, 1).permute(0, 2, 3, 1)
     assert torch.equal(y.float(), ref)
+
+
+@pytest.mark.parametrize("n,h,w,k", [(2, 17, 17, 7), (1, 224, 224, 7), (2, 9, 12, 3)])
+def test_stem_im2col_matches_numpy(n, h, w, k):
+    """uint8 NHWC images -> normalised bf16 im2col rows (K layout ky * pad8(3k) + kx * 3 + c,
+    zero halo), bit-exact vs the same fp32 arithmetic in numpy (interior word loads and the
+    border byte path)."""
+    from paper_2308_15949_b200 import _lib
+    from paper_2308_15949_b200 import device as D
+    D.require_cuda()
+    rng = np.random.default_rng(h + k)
+    img = rng.integers(0, 256, (n, h, w, 3), dtype=np.uint8)
+    mean = np.array([123.7, 116.3, 103.5], np.float32)
+    inv = (1.0 / np.array([58.4, 57.1, 57.4], np.float32)).astype(np.float32)
+    st, pad = 2, k // 2
+    ho, wo = (h + 2 * pad - k) // st + 1, (w + 2 * pad - k) // st + 1
+    seg = (3 * k + 7) // 8 * 8
+    cols = torch.empty(n * ho * wo, k * seg, dtype=torch.bfloat16, device="cuda")
+    imgd = torch.from_numpy(img).cuda()
+    md, sd = torch.from_numpy(mean).cuda(), torch.from_numpy(inv).cuda()
+    _lib.call("laud_stem_im2col", D.ptr(imgd), n, h, w, k, st, pad, D.ptr(md), D.ptr(sd), D.ptr(cols),
+              k * seg, None)
+    torch.cuda.synchronize()
+    norm = (img.astype(np.float32) - mean) * inv  # fp32, same order as the kernel
+    padded = np.zeros((n, h + 2 * pad, w + 2 * pad, 3), np.float32)
+    padded[:, pad:pad + h, pad:pad + w] = norm
+    ref = np.zeros((n, ho, wo, k, seg), np.float32)
+    for ky in range(k):
+        for kx in range(k):
+            ref[..., ky, kx * 3:kx * 3 + 3] = padded[:, ky:ky + st * ho:st, kx:kx + st * wo:st]
+    ref_bf = torch.from_numpy(ref.reshape(n * ho * wo, k * seg)).bfloat16()
+    assert torch.equal(cols.cpu(), ref_bf)
