@@ -122,7 +122,6 @@ class LaudNetwork:
         wcol = wcol.reshape(st.out_channels, 1, 1, self.stem_cols)
         self.stem_w = D.pack_weight(wcol.transpose(0, 3, 1, 2), self.stem_cols, device)
         self.stem_c = D.pad8(st.out_channels)
-        self.stem_scale = D.fvec(np.ones(st.out_channels), st.out_channels, 1.0, device)
         self.stem_bias = D.fvec(params["stem_b"], st.out_channels, 0.0, device)
         self.mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32, device=device)
         self.inv_std = torch.tensor([1.0 / s for s in IMAGENET_STD], dtype=torch.float32, device=device)
@@ -197,7 +196,7 @@ class LaudNetwork:
         stem_out = self._buf("stem", (n, ho, wo, self.stem_c))
         CH.conv(act=cols, in_hw=(n * ho * wo, 1), in_c=self.stem_cols, in_ld=self.stem_cols,
                 weight=self.stem_w, n_out=self.stem_c, out=stem_out, out_ld=self.stem_c,
-                out_hw=(ho, wo), batch=n, a_compact=1, scale=self.stem_scale, bias=self.stem_bias,
+                out_hw=(ho, wo), batch=n, a_compact=1, bias=self.stem_bias,
                 relu=1, stream=stream)
         x = stem_out
         if net.stem_pool:
