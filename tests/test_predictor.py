@@ -52,3 +52,24 @@ def test_b200_hw_spec_file_format():
                 "movement_efficiency", "const_overhead_us"):
         assert key in kv
     assert int(kv["pe_count"]) == 148 and 0 < float(kv["movement_efficiency"]) <= 1
+
+
+def test_channel_schedule_switch():
+    """Channel blocks run dense-masked from CHANNEL_DENSE_MIN samples on (capi.cu
+    channel_forward): rate-independent there, rate-dependent per-sample below."""
+    m = P.B200Predictor()
+    blk = _block()
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=1)
+    big = [m.predict_block_us(blk, cfg, r, 256) for r in (0.2, 0.8)]
+    assert abs(big[0] - big[1]) < 1e-9
+    small = [m.predict_block_us(blk, cfg, r, 1) for r in (0.2, 0.8)]
+    assert small[0] < small[1]
+    ks = P.block_kernels(blk, cfg, 0.5, P.CHANNEL_DENSE_MIN)
+    assert not any(k.cls == "small" for k in ks)  # no per-sample weight packing
+
+
+def test_grouped_to_dense_device_matches_oracle():
+    from oracle import laud_oracle as O
+    from paper_2308_15949_b200 import device as D
+    w = np.random.default_rng(0).standard_normal((48, 8, 3, 3))
+    np.testing.assert_array_equal(D.grouped_to_dense(w, 6), O.grouped_to_dense(w, 6))
