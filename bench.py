@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--ratio", type=float, default=0.5)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--no-baselines", action="store_true", help="skip static / cuDNN / CPU / sweep legs")
-    ap.add_argument("--cpu-images", type=int, default=2)
+    ap.add_argument("--cpu-images", type=int, default=24)  # ~10 s of host CPU work
     a = ap.parse_args()
     if a.plan is None:
         a.plan = "1-1-1-1" if a.paradigm == "channel" else "4-2-2-1"
