@@ -417,7 +417,7 @@ def test_regnet_se_block_matches_oracle_ext(stage, index, paradigm):
 
 
 @pytest.mark.parametrize("stage,index,s,n", [(3, 1, 2, 16), (2, 0, 2, 16), (4, 1, 1, 16), (4, 0, 1, 16),
-                                             (3, 1, 2, 128)])
+                                             (3, 1, 2, 128), (1, 1, 4, 8), (2, 1, 2, 32)])
 def test_masker_fused_into_conv1_decides_like_standalone(stage, index, s, n):
     """The masker dots accumulated from conv1's A stages (dense conv1, incl. blocks
     whose conv1 has several N tiles; n = 128 at stage 3 runs conv1 on CTA pairs,
