@@ -222,8 +222,10 @@ typedef struct laud_block_args {
   const float* se_b2;
   int se_hidden;
   /* spatial masker fused into a dense conv1 (conv1_dense, masker computed):
-   * per-cell window sums [n * cells], zero on entry and left zero (the decision
-   * pass clears what it reads); NULL = standalone masker pass. */
+   * scratch for one masker dot per conv1 input pixel [n * h_in * w_in] fp32,
+   * written (not accumulated) by conv1's readers and summed per cell in a
+   * fixed order by the decision pass, so decisions are deterministic;
+   * NULL = standalone masker pass. */
   float* cell_sums;
   /* EXT channel skipping over a grouped conv2 (RegNet; the reference's sparse
    * executor rejects groups != 1, reference.py:405-406): the grouped kernel

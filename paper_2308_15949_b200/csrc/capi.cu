@@ -31,8 +31,8 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
                                   float* dn);
 cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,
                                   void* scan, cudaStream_t stream);
-cudaError_t launch_masker_decide(const float* cell_sums, int total, int win, float bias, uint8_t* coarse,
-                                 int* list, int* count, void* scan, cudaStream_t stream);
+cudaError_t launch_masker_decide(const float* pixel_dots, int n, int h, int w, int win, float bias,
+                                 uint8_t* coarse, int* list, int* count, void* scan, cudaStream_t stream);
 cudaError_t launch_dilate_pixels(const uint8_t* coarse, int n, int h, int w, int s, int stride,
                                  int cells_h, int cells_w, int radius, int* list, int* count,
                                  void* scan, cudaStream_t stream);
@@ -276,8 +276,7 @@ int pick_bn(int n_out, int k, long long rows) {
 // fused masker dots riding on a dense 1x1 conv (ConvParams::adot_*)
 struct AdotArgs {
   const float* w;
-  float* out;
-  int win, cells_h, cells_w;
+  float* out;  // one dot per dense row (input pixel)
 };
 constexpr int LAUD_ADOT_UNAVAILABLE = 99;  // internal: conv shape cannot host the masker
 
@@ -431,9 +430,6 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     if (!p.a_tile) return LAUD_ADOT_UNAVAILABLE;
     p.adot_w = ad->w;
     p.adot_out = ad->out;
-    p.adot_win = ad->win;
-    p.adot_cells_h = ad->cells_h;
-    p.adot_cells_w = ad->cells_w;
   }
   CUtensorMap m;
   if ((rc = tensor_map_2d(a->weight, a->n_out, kw, kw, pair ? bn / 2 : bn, &m, a->b_batched ? a->batch : 0)))
@@ -932,20 +928,17 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c1.rows_max = n * a->h_in * a->w_in;
   bool conv1_done = false;
   if (fuse_masker) {
-    // masker window sums accumulate in `partial` during the dense conv1, then
-    // decisions + the active-cell list (reference.py:173-183, 133-135)
+    // per-pixel masker dots stored by conv1's readers, then decisions + the
+    // active-cell list (reference.py:173-183, 133-135)
     const int win = a->s * a->stride;
-    const int total = n * ch * cw;
     c1.row_mode = ROWS_DENSE;
-    AdotArgs ad{a->masker_wdiff, a->cell_sums, win, ch, cw};
-    // `cell_sums` is zero here: allocated zeroed, and the decision pass below
-    // clears every sum it reads (MaskerFlag)
+    AdotArgs ad{a->masker_wdiff, a->cell_sums};
     rc = run_conv(&c1, st, &ad);
     if (rc == LAUD_OK) {
       conv1_done = true;
       ProfScope ps(1, st);
-      if ((rc = cuda_check(launch_masker_decide(a->cell_sums, total, win, a->masker_bias, a->coarse_out,
-                                                a->cell_list, a->cell_count, a->scan, st),
+      if ((rc = cuda_check(launch_masker_decide(a->cell_sums, n, a->h_in, a->w_in, win, a->masker_bias,
+                                                a->coarse_out, a->cell_list, a->cell_count, a->scan, st),
                            "masker decide", 1)))
         return rc;
     } else if (rc == LAUD_ADOT_UNAVAILABLE) {  // this geometry cannot host it: standalone masker

@@ -295,18 +295,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const float acc_a = (aa[0] + aa[1]) + (aa[2] + aa[3]);
         const float acc_b = (ab[0] + ab[1]) + (ab[2] + ab[3]);
-        // rows -> pixels of the dense input grid -> masker cells
-        const int hw = p.out_h * p.out_w;
-        auto add = [&](int r, float v) {
-          const int m = ti.m0 + r;
-          if (m >= nvalid) return;
-          const int n = m / hw, rem = m - n * hw;
-          const int y = rem / p.out_w, x = rem - (rem / p.out_w) * p.out_w;
-          atomicAdd(p.adot_out + (n * p.adot_cells_h + y / p.adot_win) * p.adot_cells_w + x / p.adot_win, v);
-        };
+        // one dot per row = per pixel of the dense input grid, stored (no
+        // atomics): the decision pass sums each cell's window in a fixed
+        // row-major order, so decisions are deterministic run to run
         if (dots) {
-          add(ra, acc_a);
-          if (rb < BM) add(rb, acc_b);
+          if (ti.m0 + ra < nvalid) p.adot_out[ti.m0 + ra] = acc_a;
+          if (rb < BM && ti.m0 + rb < nvalid) p.adot_out[ti.m0 + rb] = acc_b;
         }
       }
     } else if (kTile && p.a_tile) {

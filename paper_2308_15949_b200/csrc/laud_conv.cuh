@@ -37,12 +37,11 @@ struct ConvParams {
   int a_tile;            // 1: the 128 A rows of a tile are contiguous: one 2D TMA box
   int a_box;             // 1: S x S patch rows loaded as one 4D TMA box per patch and tap
   // fused masker (dense 1x1 conv1 with contiguous A rows, a_tile): idle producer
-  // warps read each A stage from smem and accumulate dot(x_row, adot_w) per row;
-  // per tile the row dots are added into adot_out[cell] (cell of the row's
-  // pixel for an adot_win x adot_win window, adot_cells_h x adot_cells_w cells)
+  // warps read each A stage from smem and store dot(x_row, adot_w) per row
+  // (= per dense input pixel) into adot_out[row]; the decision pass sums the
+  // cell windows in a fixed order
   const float* adot_w;
   float* adot_out;
-  int adot_win, adot_cells_h, adot_cells_w;
   int a_rows;            // rows of the A tensor map (also the out-of-bounds marker)
   int ksize, stride, pad;
   int kpad;              // in_c rounded up to 64 (+64 for grouped convs)

@@ -173,16 +173,34 @@ struct MaskerFlag {  // decision from split partials; also materialises coarse
   int splits;
   float inv_area, bias;
   uint8_t* coarse;
-  bool clear;  // zero the sums after reading (conv1-fused cell_sums only)
   __device__ bool operator()(int i) const {
     float s = 0.f;
     for (int k = 0; k < splits; ++k) {
       s += partial[(size_t)i * splits + k];
-      // leave cell_sums zeroed: the next block's conv1-fused masker accumulates
-      // into it without a memset (each item is read exactly once).  Standalone
-      // masker partials stay intact (calibration reads them back).
-      if (clear) const_cast<float*>(partial)[(size_t)i * splits + k] = 0.f;
     }
+    const bool f = s * inv_area + bias >= 0.f;
+    if (coarse) coarse[i] = f ? 1 : 0;
+    return f;
+  }
+};
+
+// Conv1-fused masker: per-pixel dots (one per dense conv1 row) summed over
+// each cell's win x win input window in fixed row-major order (deterministic),
+// then d = sum / win^2 + bias >= 0 (`reference.py:173-183`).
+struct PixelWindowFlag {
+  const float* dots;
+  int h, w, win, cells_h, cells_w;
+  float inv_area, bias;
+  uint8_t* coarse;
+  __device__ bool operator()(int i) const {
+    const int cpi = cells_h * cells_w;
+    const int ni = i / cpi;
+    const int cr = i - ni * cpi;
+    const int ci = cr / cells_w, cj = cr - (cr / cells_w) * cells_w;
+    const float* base = dots + ((size_t)ni * h + ci * win) * w + cj * win;
+    float s = 0.f;
+    for (int py = 0; py < win; ++py)
+      for (int px = 0; px < win; ++px) s += base[(size_t)py * w + px];
     const bool f = s * inv_area + bias >= 0.f;
     if (coarse) coarse[i] = f ? 1 : 0;
     return f;
@@ -606,16 +624,17 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
         splits, cps, partial, prev_coarse, dn);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse, false};
+  MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse};
   return launch_compact(f, total, list, count, scan, stream);
 }
 
-// Decisions + active-cell list from per-cell window sums accumulated elsewhere
-// (conv1's fused masker dots): d = sum / win^2 + bias >= 0.
-cudaError_t launch_masker_decide(const float* cell_sums, int total, int win, float bias, uint8_t* coarse,
-                                 int* list, int* count, void* scan, cudaStream_t stream) {
-  MaskerFlag f{cell_sums, 1, 1.0f / (float)(win * win), bias, coarse, true};
-  return launch_compact(f, total, list, count, scan, stream);
+// Decisions + active-cell list from the per-pixel masker dots conv1's fused
+// readers stored (dots [n][h][w] on conv1's input grid, win = S * stride).
+cudaError_t launch_masker_decide(const float* pixel_dots, int n, int h, int w, int win, float bias,
+                                 uint8_t* coarse, int* list, int* count, void* scan, cudaStream_t stream) {
+  const int cells_h = h / win, cells_w = w / win;
+  PixelWindowFlag f{pixel_dots, h, w, win, cells_h, cells_w, 1.0f / (float)(win * win), bias, coarse};
+  return launch_compact(f, n * cells_h * cells_w, list, count, scan, stream);
 }
 
 cudaError_t launch_list_from_mask(const uint8_t* coarse, int total, int* list, int* count,

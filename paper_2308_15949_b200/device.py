@@ -332,7 +332,7 @@ class DeviceBlock:
             ss = s if paradigm == "spatial" else ho
             partial_n = max(1, lib.laud_masker_partial_floats(n, h, w, self.cin_p, ss, blk.stride))
         partial = ws.get("partial", partial_n * 4)
-        cell_sums = ws.get("cell_sums", cells * 4, zero=True)  # zero-invariant (laud.h)
+        cell_sums = ws.get("pixel_dots", pix * 4)  # conv1-fused masker: one dot per input pixel (laud.h)
         scan = ws.get("scan", lib.laud_scan_workspace_bytes(max(pix, cells)), zero=True)
         v = self.vec
         a = _lib.BlockArgs(

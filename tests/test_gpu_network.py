@@ -29,6 +29,7 @@ def _net(arch, paradigm, plan="4-2-2-1", ratio=0.5):
 
 @pytest.mark.parametrize("arch,paradigm,plan", [
     ("resnet50", "spatial", "4-2-2-1"), ("resnet101", "spatial", "4-2-2-1"),
+    ("resnet50", "spatial", "4-4-2-1"),  # BASELINE config 2's plan
     ("resnet50", "layer", "4-2-2-1"), ("resnet50", "static", "4-2-2-1"),
     ("resnet50", "channel", "1-1-1-1"), ("resnet50", "channel", "2-2-2-2"),
     ("regnety-1.6gf", "spatial", "4-4-2-1"), ("regnety-1.6gf", "layer", "4-4-2-1"),

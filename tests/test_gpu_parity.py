@@ -231,6 +231,38 @@ def test_channel_block_large(r):
     assert _rel(y, yd) <= BF16_TOL
 
 
+@pytest.mark.parametrize("n,g,stride", [(16, 1, 1), (16, 2, 1), (64, 1, 1), (16, 1, 2)])
+def test_channel_block_throughput_batch(n, g, stride):
+    """The channel schedule the benchmark runs (batch >= 8, R101 stage-3 geometry,
+    bf16) vs the bf16-emulating oracle at 1e-3: exact-count per-sample masks at
+    r = 0.5 plus a sample that keeps no channel and one that keeps all."""
+    R = _R()
+    cin = 512 if stride == 2 else 1024
+    hw = 28 if stride == 2 else 14
+    blk = BlockSpec(ConvLayerSpec(cin, 256, 1), ConvLayerSpec(256, 256, 3, stride), ConvLayerSpec(256, 1024, 1),
+                    TensorShape(cin, hw, hw), has_downsample=stride > 1)
+    rng = np.random.default_rng(50 + n + g)
+    bw = R.make_block_weights(blk, rng)
+    x = rng.standard_normal((n, cin, hw, hw))
+    d = 256 // g
+    coarse = np.zeros((n, d), bool)
+    for i in range(2, n):
+        coarse[i, rng.permutation(d)[: d // 2]] = True
+    coarse[1] = True  # sample 0 keeps nothing, sample 1 everything
+    exp = np.repeat(coarse, g, axis=1)
+    m = R.ChannelMask(coarse, exp, g)
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=g)
+    y = R.block_forward_sparse(x, bw, blk, cfg, m)
+    obw = O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
+    emu = O.block_forward_sparse(x, obw, blk, cfg, O.ChannelMask(coarse, exp, g), emulate_bf16=True)
+    assert _rel(y, emu) <= BF16_TOL, _rel(y, emu)
+    # the sample that keeps no channel is exactly its (bf16) skip path
+    xr = O.round_bf16(x[:1])
+    skip = O.skip_path(xr, blk, O.BlockWeights(*(O.round_bf16(w) for w in (bw.w1, bw.w2, bw.w3, bw.w_down))),
+                       rnd=O.round_bf16) if stride > 1 else xr
+    assert _rel(y[:1], skip) <= BF16_TOL
+
+
 @pytest.mark.parametrize("stage,index,paradigm", [(1, 0, "spatial"), (2, 1, "spatial"), (3, 0, "spatial"),
                                                    (3, 1, "spatial"), (4, 1, "spatial"), (3, 1, "layer"),
                                                    (2, 0, "static")])
