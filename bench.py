@@ -2,18 +2,35 @@
 
 Contract (one JSON line on rank 0):
   python bench.py --gpus N --steps K --warmup W [--impl reference]
-For N>1 run under torchrun: one process per GPU, weak scaling (each rank
-processes its own batch of --batch images), no collective on the data path;
-the timed region is bracketed by barriers and the max over ranks is reported.
+With N > 1 and no torchrun environment the script launches itself under
+``torch.distributed.run`` (one process per GPU, NCCL).  SURVEY §8(e): a
+global batch of independent synthetic images is split contiguously across
+the ranks (``dist.shard_range``) — weak scaling by default (``--batch`` images
+per GPU), strong scaling with ``--global-batch G`` (G/N per GPU, BASELINE
+config 5).  No collective on the data path; the timed region is bracketed by
+barriers and the MAX over ranks is reported.  After timing, the logits of
+every shard are all-gathered over NCCL and compared on rank 0 with a
+single-GPU forward of the same images; per-rank active-patch counts P are
+reported.
 
-Step = one forward of the whole LAUD-R101 (stem, 33 dynamic bottleneck
-blocks with their maskers computed inside the step, GAP, FC) over a batch of
-synthetic 224x224 uint8 images already resident in HBM, replayed as one CUDA
-graph.  L2 is flushed (256 MiB write) before every timed step and each step
-is timed with CUDA events on the launching stream.  ``e2e`` repeats the step
-through the public API with the pinned-host image upload and the logits
-download inside the timed region.  ``--impl reference`` times the CPU
-oracle (numpy fp64 restatement of the reference executor) on this host.
+Step = one forward of the whole LAUD network (stem, the dynamic bottleneck
+blocks with their maskers computed inside the step, GAP, FC) over the rank's
+shard of synthetic 224x224 uint8 images already resident in HBM, replayed as
+one CUDA graph.  L2 is flushed (256 MiB write) before every timed step and
+each step is timed with CUDA events on the launching stream.  ``e2e``
+repeats the step through the public streaming API with the pinned-host image
+upload and the logits download inside the timed region.
+
+Masker biases (the role a trained masker's FLOPs loss plays) are calibrated
+on a HELD-OUT batch to hit ``--ratio`` — or read from the committed
+calibration file for the configuration — and are identical on every rank
+and in the ``--impl reference`` arm.
+
+``--impl reference`` times the reference's own CPU implementation: per step
+one image through the network, every bottleneck block through the SHIPPED
+``dynlat.reference.block_forward_sparse`` (installed in ``baseline/_ref``)
+on the same per-block inputs and masker decisions as the GPU arm; stem,
+max-pool, GAP and FC (which the reference lacks) through the numpy port.
 """
 
 from __future__ import annotations
@@ -21,6 +38,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,6 +52,8 @@ sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+BIAS_FILE = ROOT / "paper_2308_15949_b200" / "data" / "masker_biases.json"
+IMG_CHUNK = 64
 
 
 def peaks():
@@ -44,7 +64,7 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -55,10 +75,15 @@ def parse():
     ap.add_argument("--plan", default=None, help="S per stage (spatial, default 4-2-2-1) or "
                     "G per stage (channel, default 1-1-1-1)")
     ap.add_argument("--ratio", type=float, default=0.5)
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=256, help="images per GPU (weak scaling)")
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling: this many images split across the GPUs")
+    ap.add_argument("--calib-images", type=int, default=64, help="held-out calibration batch")
     ap.add_argument("--no-baselines", action="store_true", help="skip static / cuDNN / CPU / sweep legs")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic pass")
     ap.add_argument("--cpu-images", type=int, default=24)  # ~10 s of host CPU work
-    a = ap.parse_args()
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
+    a = ap.parse_args(argv)
     if a.plan is None:
         a.plan = "1-1-1-1" if a.paradigm == "channel" else "4-2-2-1"
     return a
@@ -72,23 +97,102 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# reference arm: CPU oracle
+# shared workload definition (both arms, every rank)
 # ---------------------------------------------------------------------------
 
 
-def cpu_oracle_images_per_s(args, n_images, params=None, biases=None):
-    from oracle import laud_oracle as O
-    from paper_2308_15949_b200.network import make_params
-    params = params or make_params(args.arch, 0)
-    plan = tuple(int(v) for v in args.plan.split("-"))
-    rng = np.random.default_rng(1)
-    img = rng.integers(0, 256, (1, 224, 224, 3), dtype=np.uint8)
-    t = []
-    for _ in range(n_images):
-        t0 = time.perf_counter()
-        O.network_forward(params, img, args.paradigm, plan, biases)
-        t.append(time.perf_counter() - t0)
-    return 1.0 / statistics.median(t), t
+def image_range(lo: int, hi: int, h: int = 224, w: int = 224) -> np.ndarray:
+    """Synthetic uint8 images [lo, hi) of the global set, NHWC.  Image i depends
+    only on i (chunks of IMG_CHUNK seeded by chunk index), so every rank and
+    every world size sees the same global batch."""
+    out = np.empty((max(hi - lo, 0), h, w, 3), np.uint8)
+    c = lo // IMG_CHUNK
+    while c * IMG_CHUNK < hi:
+        blk = np.random.default_rng(10_000 + c).integers(0, 256, (IMG_CHUNK, h, w, 3), dtype=np.uint8)
+        a, b = max(lo, c * IMG_CHUNK), min(hi, (c + 1) * IMG_CHUNK)
+        out[a - lo:b - lo] = blk[a - c * IMG_CHUNK:b - c * IMG_CHUNK]
+        c += 1
+    return out
+
+
+def calib_images(n: int, h: int = 224, w: int = 224) -> np.ndarray:
+    """Held-out calibration images (disjoint seed space from ``image_range``)."""
+    return np.random.default_rng(999).integers(0, 256, (n, h, w, 3), dtype=np.uint8)
+
+
+def bias_key(args) -> str:
+    return f"{args.arch}/{args.paradigm}/{args.plan}/{args.ratio:g}"
+
+
+def committed_biases(args):
+    if BIAS_FILE.exists():
+        d = json.loads(BIAS_FILE.read_text())
+        e = d.get("configs", {}).get(bias_key(args))
+        if e is not None:
+            return e["biases"], e
+    return None, None
+
+
+def plan_shard(args, ws: int, rank: int):
+    """(global batch, lo, hi, scaling) of this rank."""
+    from paper_2308_15949_b200.dist import shard_range
+    if args.global_batch:
+        g, scaling = int(args.global_batch), "strong"
+    else:
+        g, scaling = ws * args.batch, "weak"
+    lo, hi = shard_range(g, rank, ws)
+    return g, lo, hi, scaling
+
+
+def bench_config(args, ws: int, g: int, scaling: str) -> dict:
+    """The workload both arms report (identical dicts => same configuration)."""
+    per = f"batch {args.batch} per GPU" if scaling == "weak" else f"global batch {g} split over {ws} GPU(s)"
+    return {"workload": f"LAUDNet-{args.arch} {args.paradigm} S/G={args.plan} ratio {args.ratio}, 224x224, "
+                        f"{per} (BASELINE config {'3' if args.arch == 'resnet101' and args.paradigm == 'spatial' else '2-5'})",
+            "global_batch": g, "arch": args.arch, "paradigm": args.paradigm, "plan": args.plan,
+            "target_ratio": args.ratio, "masker_biases": bias_key(args),
+            "l2_policy": "256 MiB L2 flush before every timed step",
+            "parallelism": f"batch-shard x{ws} ({scaling} scaling, no collective on the hot path)",
+            "graph": True}
+
+
+# ---------------------------------------------------------------------------
+# rank logic around the forward (no GPU specifics: gloo-testable)
+# ---------------------------------------------------------------------------
+
+
+def gather_scalars(vals, device=None):
+    """All-gather a short vector of floats per rank -> list of lists (rank order)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [t.tolist()]
+    outs = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(outs, t)
+    return [o.tolist() for o in outs]
+
+
+def check_shards(local_logits, g: int, ws: int, rank: int, recompute):
+    """All-gather every rank's logits (checking only, outside the timed region)
+    and, on rank 0, compare them with ``recompute(lo, hi)`` — a single-device
+    forward of the same global images — shard by shard."""
+    import torch
+    from paper_2308_15949_b200.dist import gather_rows, shard_range
+    allrows = gather_rows(local_logits)
+    if rank != 0:
+        return None
+    ref = torch.cat([recompute(*shard_range(g, r, ws)).to(allrows.device, allrows.dtype) for r in range(ws)])
+    diff = (allrows - ref).abs()
+    return {"ranks": ws, "rows": int(allrows.shape[0]), "rows_expected": g,
+            "bitwise_equal": bool(torch.equal(allrows, ref)),
+            "max_abs_diff": float(diff.max().item()) if diff.numel() else 0.0,
+            "vs": "rank 0 re-running each shard's images on one GPU (eager forward)"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the shipped CPU implementation
+# ---------------------------------------------------------------------------
 
 
 def blas_threads():
@@ -101,6 +205,80 @@ def blas_threads():
         return os.cpu_count()
 
 
+def shipped_reference():
+    """``dynlat.reference`` installed from /root/reference into baseline/_ref."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "dynlat").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import dynlat.core as DC
+        import dynlat.reference as DR
+        import dynlat.zoo as DZ
+        return DR, DC, DZ
+    except Exception:
+        return None
+
+
+def record_block_inputs(params, img, paradigm, plan, biases):
+    """One image through the port with the GPU arm's biases: per block its
+    input and the masker's decision (what the shipped executor is fed)."""
+    from oracle import laud_oracle as O
+    rec, xs = [], []
+    orig = O.block_forward_sparse
+
+    def hook(x, *a, **k):
+        xs.append(x)
+        return orig(x, *a, **k)
+
+    O.block_forward_sparse = hook
+    try:
+        O.network_forward(params, img, paradigm, plan, biases, record=rec)
+    finally:
+        O.block_forward_sparse = orig
+    return xs, rec
+
+
+def shipped_network_seconds(params, img, paradigm, plan, xs, rec, mods):
+    """Wall time of one image: stem/pool/GAP/FC via the port + every block via
+    the shipped ``dynlat.reference.block_forward_sparse`` (same inputs/masks)."""
+    from oracle import laud_oracle as O
+    DR, DC, DZ = mods
+    dnet = DZ.build_network(params["arch"])
+    t0 = time.perf_counter()
+    x = (img.astype(np.float64) - O.IMAGENET_MEAN) / O.IMAGENET_STD
+    x = x.transpose(0, 3, 1, 2)
+    st = params["net"].stem
+    y = np.maximum(O.conv_raw(x, params["stem_w"], st.stride, st.kernel // 2)
+                   + params["stem_b"].reshape(1, -1, 1, 1), 0.0)
+    if params["net"].stem_pool:
+        y = O.maxpool3s2(y)
+    t_glue = time.perf_counter() - t0
+    t_blocks = 0.0
+    for bp, bi, xin, m in zip(params["blocks"], dnet.blocks, xs, rec):
+        bw = DR.BlockWeights(bp["w1"], bp["w2"], bp["w3"], bp["wd"])
+        if paradigm == "spatial":
+            s = m.granularity
+            cfg = DC.DynamicConfig(DC.Paradigm.SPATIAL, spatial_granularity=s)
+            mask = DR.SpatialMask(m.coarse, m.upsampled, s)
+        elif paradigm == "layer":
+            cfg, mask = DC.DynamicConfig(DC.Paradigm.LAYER), DR.LayerMask(m.decisions)
+        elif paradigm == "channel":
+            cfg = DC.DynamicConfig(DC.Paradigm.CHANNEL, channel_granularity=m.granularity)
+            mask = DR.ChannelMask(m.coarse, m.expanded, m.granularity)
+        else:
+            cfg, mask = DC.DynamicConfig(DC.Paradigm.STATIC), None
+        t1 = time.perf_counter()
+        DR.block_forward_sparse(xin, bw, bi.block, cfg, mask)
+        t_blocks += time.perf_counter() - t1
+    t2 = time.perf_counter()
+    feat = xs[-1].mean(axis=(2, 3))
+    _ = feat @ params["fc_w"].T + params["fc_b"]
+    t_glue += time.perf_counter() - t2
+    return t_glue + t_blocks, t_blocks
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -110,29 +288,41 @@ def run_reference(args):
     plan = tuple(int(v) for v in args.plan.split("-"))
     if args.paradigm == "channel":
         add_channel_maskers(params, plan, 0)
+    biases, bent = committed_biases(args)
+    g, _, _, scaling = plan_shard(args, max(ws, args.gpus), 0)
+    img = image_range(0, 1)
+    xs, rec = record_block_inputs(params, img, args.paradigm, plan, biases)
+    mods = shipped_reference()
     from oracle import laud_oracle as O
-    img = np.random.default_rng(1).integers(0, 256, (1, 224, 224, 3), dtype=np.uint8)
+    if mods is not None:
+        kind = "reference"
+        step = lambda: shipped_network_seconds(params, img, args.paradigm, plan, xs, rec, mods)[0]  # noqa: E731
+        sample = ("1 synthetic 224x224 image per step (image 0 of the GPU arm's global batch): all "
+                  f"{len(xs)} bottleneck blocks through the SHIPPED dynlat.reference.block_forward_sparse "
+                  "(baseline/_ref, numpy fp64) on the block inputs and calibrated masker decisions of the same "
+                  "network; stem / max-pool / GAP / FC (absent from the reference) through the numpy port")
+    else:
+        kind = "port"
+
+        def step():
+            t0 = time.perf_counter()
+            O.network_forward(params, img, args.paradigm, plan, biases)
+            return time.perf_counter() - t0
+        sample = "1 synthetic 224x224 image per step through the numpy fp64 port (oracle/laud_oracle.py)"
     for _ in range(max(1, min(args.warmup, 1))):
-        O.network_forward(params, img, args.paradigm, plan)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.network_forward(params, img, args.paradigm, plan)
-        times.append(time.perf_counter() - t0)
+        step()
+    times = [step() for _ in range(args.steps)]
     tot = sum(times)
     v = args.steps / tot
-    cores = blas_threads()
     line = {
         "impl": "reference", "metric": "images_per_sec", "value": v, "unit": "images/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": max(ws, args.gpus), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"LAUD-{args.arch} {args.paradigm} S={args.plan} r={args.ratio}, "
-                               "1 image per step (bounded CPU sample)",
-                   "arch": args.arch, "plan": args.plan, "ratio": args.ratio},
-        "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": "1 synthetic 224x224 image per step through the numpy fp64 "
-                                   "oracle network (oracle/laud_oracle.py)"},
+        "config": bench_config(args, max(ws, args.gpus), g, scaling),
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": blas_threads(), "kind": kind,
+                         "sample": sample},
+        "masker_biases_source": "committed calibration file" if bent else "none (bias 0)",
         "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -248,20 +438,16 @@ def capture(torch, fn, warmup):
 
 
 def _alg(r):
-    """Algorithmic FLOPs and compulsory bytes of one conv-engine launch."""
+    """Algorithmic FLOPs and compulsory bytes of one conv-engine launch (rows =
+    the launch's actual active rows; K = taps * C_in / groups)."""
     flops = 2.0 * r.rows * r.n_out * r.k
     cin = r.k // max(1, r.taps)
     nbytes = 2.0 * r.rows * (cin + r.n_out * (2 if r.resid else 1))
     return flops, nbytes
 
 
-def conv_roofline(torch, net, images, pk, pk_kind):
-    """Per-launch CUDA-event profile of one eager forward (outside the timed region).
-
-    The roofline object describes the dominant launch shape of the conv engine
-    (largest total time in the step): achieved = algorithmic FLOPs (or bytes,
-    whichever bounds it) per launch / average launch duration of that shape.
-    """
+def profile_launches(torch, net, images):
+    """Per-launch CUDA-event records of one eager forward (outside timing)."""
     from paper_2308_15949_b200 import _lib
     lib = _lib.lib()
     torch.cuda.synchronize()
@@ -269,29 +455,28 @@ def conv_roofline(torch, net, images, pk, pk_kind):
     net.forward(images)
     recs = (_lib.ProfileRecord * 4096)()
     n = lib.laud_profile_end(recs, 4096)
-    recs = recs[:n]
+    return list(recs[:n])
+
+
+def conv_roofline(recs, pk, pk_kind):
+    """Roofline of the dominant conv-engine launch shape (largest total time in
+    the step): achieved = algorithmic FLOPs (or bytes, whichever bounds it) per
+    launch / average CUDA-event duration of those launches."""
     convs = [r for r in recs if r.tag == 0]
     maskers = [r for r in recs if r.tag == 1]
     all_ms = sum(r.ms for r in recs)
     groups = {}
-    for r in convs:
-        key = (r.rows, r.n_out, r.k, r.taps, r.resid)
-        groups.setdefault(key, []).append(r)
-    key, grp = max(groups.items(), key=lambda kv: sum(x.ms for x in kv[1]))
-    flops, nbytes = _alg(grp[0])
-    avg_ms = sum(x.ms for x in grp) / len(grp)
+    for i, r in enumerate(convs):
+        groups.setdefault((r.rows, r.n_out, r.k, r.taps, r.resid), []).append((i, r))
+    key, grp = max(groups.items(), key=lambda kv: sum(x.ms for _, x in kv[1]))
+    flops, nbytes = _alg(grp[0][1])
+    avg_ms = sum(x.ms for _, x in grp) / len(grp)
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     peak_b = pk["hbm_gbs"]
-    t_tensor = flops / (peak_t * 1e12)
-    t_hbm = nbytes / (peak_b * 1e9)
-    if t_tensor >= t_hbm:
+    if flops / (peak_t * 1e12) >= nbytes / (peak_b * 1e9):
         bound, ach, peak, unit = "tensor", flops / (avg_ms * 1e-3) / 1e12, peak_t, "TFLOP/s"
     else:
         bound, ach, peak, unit = "hbm", nbytes / (avg_ms * 1e-3) / 1e9, peak_b, "GB/s"
-    tot_f = sum(_alg(r)[0] for r in convs)
-    tot_ms = sum(r.ms for r in convs)
-    # step-level roofline of the conv engine: slower of FLOPs and bytes per launch, summed
-    ideal_ms = sum(max(_alg(r)[0] / (peak_t * 1e12), _alg(r)[1] / (peak_b * 1e9)) for r in convs) * 1e3
     mb = sum(r.bytes for r in maskers)
     mms = sum(r.ms for r in maskers)
     rows, n_out, k, taps, resid = key
@@ -304,18 +489,105 @@ def conv_roofline(torch, net, images, pk, pk_kind):
         "peak_source": f"{pk_kind} MEASURED_PEAKS.json ({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})",
         "alg_flops_per_launch": flops, "alg_bytes_per_launch": nbytes,
         "avg_launch_us": round(avg_ms * 1e3, 2),
-        "share_of_profiled_step": round(sum(x.ms for x in grp) / all_ms, 3) if all_ms else None,
-        "engine_all_launches": {"launches": len(convs), "ms": round(tot_ms, 3),
-                                "tflops": round(tot_f / (tot_ms * 1e-3) / 1e12, 1),
-                                "roofline_ms": round(ideal_ms, 3),
-                                "frac_of_roofline": round(ideal_ms / tot_ms, 4),
-                                "share_of_step": round(tot_ms / all_ms, 3) if all_ms else None},
-        "masker_gbs": round(mb / (mms * 1e-3) / 1e9, 1) if mms else None,
+        "share_of_profiled_step": round(sum(x.ms for _, x in grp) / all_ms, 3) if all_ms else None,
+        "launch_ordinals": [i for i, _ in grp],  # positions among the conv launches (traffic pass)
+        "conv_launches_per_forward": len(convs),
+        "engine_launches": {"launches": len(convs), "ms": round(sum(r.ms for r in convs), 3),
+                            "share_of_step": round(sum(r.ms for r in convs) / all_ms, 3) if all_ms else None},
+        "masker_decide_gbs": round(mb / (mms * 1e-3) / 1e9, 1) if mms and mb else None,
     }
 
 
-TV_MODELS = {"resnet50": "resnet50", "resnet101": "resnet101", "regnety-400mf": "regnet_y_400mf",
-             "regnety-800mf": "regnet_y_800mf", "regnety-1.6gf": "regnet_y_1_6gf"}
+def network_roofline(net, images, ms_step, pk):
+    """Whole-step roofline from the §8(d) per-block formulas under the masks the
+    step actually used (SURVEY: 'fraction of the per-block roofline')."""
+    import torch
+    from paper_2308_15949_b200 import roofline as RF
+    n = images.shape[0]
+    rec = []
+    net.forward(images, record=rec)
+    torch.cuda.synchronize()
+    peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    peak_b = pk["hbm_gbs"]
+    blocks = []
+    masks = {id(s): (c, k) for s, c, k in rec}
+    tot_f = tot_b = tot_t = 0.0
+    for slot in net.slots:
+        blk = slot.db.block
+        para = net._block_paradigm(slot)
+        if para == "spatial":
+            c = masks[id(slot)][0].cpu().numpy().astype(bool)
+            o = blk.output_shape
+            a = RF.block_algorithmic(blk, "spatial", n, coarse=c.reshape(n, o.height // slot.s, o.width // slot.s),
+                                     s=slot.s)
+        elif para == "layer":
+            a = RF.block_algorithmic(blk, "layer", n, decisions=masks[id(slot)][0].cpu().numpy())
+        elif para == "channel":
+            c = masks[id(slot)][0].cpu().numpy().reshape(n, -1).astype(bool)
+            a = RF.block_algorithmic(blk, "channel", n, keep=np.repeat(c, slot.db.ch_g, axis=1))
+        else:
+            a = RF.block_algorithmic(blk, "static", n)
+        t = RF.roofline_seconds(a["flops"], a["bytes"], peak_t, peak_b)
+        tot_f += a["flops"]
+        tot_b += a["bytes"]
+        tot_t += t
+        blocks.append(round(a["r"], 4))
+    sf = RF.stem_fc_algorithmic(net.net, n)
+    tot_t += RF.roofline_seconds(sf["flops"], sf["bytes"], peak_t, peak_b)
+    tot_f += sf["flops"]
+    return {"alg_gflop_per_step": round(tot_f / 1e9, 2), "alg_gbytes_per_step": round(tot_b / 1e9, 3),
+            "roofline_ms": round(tot_t * 1e3, 4), "measured_ms": round(ms_step, 4),
+            "frac_of_roofline": round(tot_t * 1e3 / ms_step, 4),
+            "alg_tflops": round(tot_f / (ms_step * 1e-3) / 1e12, 1),
+            "credit": "§8(d): spatial 2(r_dil_in F1 + r F2 + r F3 + F_down + masker), channel "
+                      "2 sum_i(r_i F1 + r_i^2 F2 + r_i F3), layer 2 r sum F, grouped K = C_in/groups; "
+                      "per block max(FLOPs/peak, bytes/BW), summed",
+            "block_ratios": blocks}
+
+
+def traffic_pass(args, roof):
+    """DRAM bytes of the dominant launch shape measured in THIS run: a short ncu
+    pass (dram__bytes_read/write of the conv launches of one forward) over a
+    fresh process running the same network and batch (outside any timing)."""
+    ords = roof.get("launch_ordinals") or []
+    nconv = roof.get("conv_launches_per_forward") or 0
+    if not ords or not nconv:
+        return None
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    log = out / "bench_traffic.csv"
+    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "--print-units", "base", "--nvtx", "--nvtx-include", "laud_probe/",
+           "-k", "regex:conv_gemm_kernel", "-c", str(nconv),
+           "--csv", "--log-file", str(log), sys.executable, str(ROOT / "bench.py"), "--traffic-probe",
+           "--arch", args.arch, "--paradigm", args.paradigm, "--plan", args.plan, "--ratio", str(args.ratio),
+           "--batch", str(args.batch)]
+    try:
+        subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=600, check=False)
+        import csv
+        vals = {}
+        with open(log) as f:
+            rows = [r for r in csv.reader(f) if len(r) > 10]
+        hdr = rows[0]
+        assert hdr[0] == "ID", hdr[:3]
+        iid, iname, ival = hdr.index("ID"), hdr.index("Metric Name"), hdr.index("Metric Value")
+        iunit = hdr.index("Metric Unit")
+        for r in rows[1:]:
+            v = float(r[ival].replace(",", ""))
+            u = r[iunit]
+            if r[iname].startswith("dram__bytes"):
+                v *= {"byte": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 1e9, "GB": 1e9}.get(u, 1)
+            vals.setdefault(int(r[iid]), {})[r[iname]] = v
+        ids = sorted(vals)
+        sel = [vals[ids[i]] for i in ords if i < len(ids)]
+        if not sel:
+            return None
+        per = [s["dram__bytes_read.sum"] + s["dram__bytes_write.sum"] for s in sel]
+        return {"traffic": float(np.mean(per)), "launches_measured": len(per),
+                "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (this bench run, "
+                          "conv launches of one forward, same network/batch; cold-cache serialised)"}
+    except Exception as exc:  # the traffic pass never costs the headline line
+        return {"traffic": None, "error": repr(exc)[:200]}
 
 
 def static_cudnn_ms(torch, batch, steps, warmup, flush, arch="resnet101"):
@@ -335,12 +607,16 @@ def static_cudnn_ms(torch, batch, steps, warmup, flush, arch="resnet101"):
     return tot / steps
 
 
+TV_MODELS = {"resnet50": "resnet50", "resnet101": "resnet101", "regnety-400mf": "regnet_y_400mf",
+             "regnety-800mf": "regnet_y_800mf", "regnety-1.6gf": "regnet_y_1_6gf"}
+
+
 def batch1_latency(torch, args, net, flush, reps=20):
     """BASELINE config 3's latency leg: one image, whole network as one CUDA graph
     (L2 flushed before each replay): the dynamic net (its calibrated maskers),
     the in-house static net and the torchvision/cuDNN static net, median ms."""
-    from paper_2308_15949_b200.network import LaudNetwork, random_images
-    img = random_images(1, seed=7)
+    from paper_2308_15949_b200.network import LaudNetwork
+    img = torch.from_numpy(image_range(0, 1)).cuda()
 
     def med(g):
         _, per = timed_graph(torch, g, reps, flush, torch.cuda.current_stream())
@@ -369,20 +645,32 @@ def batch1_latency(torch, args, net, flush, reps=20):
     return out
 
 
+def _exact_masks(rng, n, cells, r):
+    k = int(round(r * cells))  # P = round(r * cells) per sample (latency.py:363)
+    cz = np.zeros((n, cells), np.uint8)
+    for i in range(n):
+        cz[i, rng.permutation(cells)[:k]] = 1
+    return cz
+
+
 def block_sweep_b1_vs_cpu(torch, args, flush, reps_cpu=3):
     """Per-block latency vs activation ratio at batch 1 (SURVEY §8d CPU baseline):
-    the device (CUDA graph, L2 flushed) next to the numpy fp64 oracle's
-    ``block_forward_sparse`` (the reference's algorithm) on this box's host
-    cores, same block geometry, exact-count masks, median of ``reps_cpu``."""
+    the device (CUDA graph, L2 flushed) next to the CPU on this box's host cores,
+    same block geometry and exact-count masks, median of ``reps_cpu``: the SHIPPED
+    ``dynlat.reference.block_forward_sparse`` (baseline/_ref) and the numpy port."""
     from oracle import laud_oracle as O
     from paper_2308_15949_b200 import device as D
     from paper_2308_15949_b200.core import DynamicConfig, Paradigm
     from paper_2308_15949_b200.network import make_params
+    mods = shipped_reference()
     params = make_params(args.arch, 0)
     plan = tuple(int(v) for v in args.plan.split("-"))
     out = {}
     rng = np.random.default_rng(0)
     seen = set()
+    if mods is not None:
+        DR, DC, DZ = mods
+        dblocks = {(b.stage, b.index): b.block for b in DZ.build_network(args.arch).blocks}
     for bp in params["blocks"]:
         if bp["stage"] in seen or bp["index"] != 1:
             continue
@@ -400,10 +688,9 @@ def block_sweep_b1_vs_cpu(torch, args, flush, reps_cpu=3):
         for r in (0.2, 0.5, 0.8, 1.0, "static"):
             if r == "static":
                 fn = lambda: db.forward(xx, "static", out=xx, ws=wsp)  # noqa: E731
-                cfg, om = DynamicConfig(Paradigm.STATIC), None
+                cfg, om, c3 = DynamicConfig(Paradigm.STATIC), None, None
             else:
-                cz = np.zeros(cells, np.uint8)
-                cz[rng.permutation(cells)[:int(round(r * cells))]] = 1
+                cz = _exact_masks(rng, 1, cells, r)[0]
                 coarse = torch.from_numpy(cz).cuda()
                 fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp)  # noqa: E731
                 c3 = cz.reshape(1, o.height // s, o.width // s).astype(bool)
@@ -418,19 +705,39 @@ def block_sweep_b1_vs_cpu(torch, args, flush, reps_cpu=3):
                 t0 = time.perf_counter()
                 O.block_forward_sparse(xh, bw, blk, cfg, om)
                 ts.append(time.perf_counter() - t0)
-            row[str(r)] = {"gpu_us": round(1e3 * tot / 20, 1),
-                           "cpu_oracle_us": round(1e6 * statistics.median(ts), 1)}
+            ent = {"gpu_us": round(1e3 * tot / 20, 1), "cpu_port_us": round(1e6 * statistics.median(ts), 1)}
+            if mods is not None:
+                dbw = DR.BlockWeights(bp["w1"], bp["w2"], bp["w3"], None)
+                if r == "static":
+                    dcfg, dm = DC.DynamicConfig(DC.Paradigm.STATIC), None
+                else:
+                    dcfg = DC.DynamicConfig(DC.Paradigm.SPATIAL, spatial_granularity=s)
+                    dm = DR.SpatialMask(c3, DR.upsample_coarse(c3, s), s)
+                ts = []
+                for _ in range(reps_cpu):
+                    t0 = time.perf_counter()
+                    DR.block_forward_sparse(xh, dbw, dblocks[(bp["stage"], 1)], dcfg, dm)
+                    ts.append(time.perf_counter() - t0)
+                ent["cpu_shipped_reference_us"] = round(1e6 * statistics.median(ts), 1)
+            row[str(r)] = ent
         out[f"s{bp['stage']}b1_S{s}"] = row
-    return {"blocks": out, "cpu_cores": blas_threads(), "cpu_kind": "port (numpy fp64 oracle)",
+    return {"blocks": out, "cpu_cores": blas_threads(), "cpu_threads_note": "numpy/BLAS threads of this host",
+            "cpu_kinds": {"cpu_shipped_reference_us": "dynlat.reference.block_forward_sparse as shipped "
+                                                      "(baseline/_ref)" if mods else "absent",
+                          "cpu_port_us": "oracle/laud_oracle.py (vectorised numpy fp64 restatement)"},
             "batch": 1}
 
 
-def block_sweep(torch, args, flush):
-    """Per-block device latency vs activation ratio (exact-count masks), batch = args.batch."""
+def block_sweep(torch, args, flush, pk):
+    """Per-block device latency vs activation ratio (exact-count masks), batch =
+    args.batch, with each point's fraction of its §8(d) per-block roofline."""
     from paper_2308_15949_b200 import device as D
+    from paper_2308_15949_b200 import roofline as RF
     from paper_2308_15949_b200.network import make_params
     params = make_params(args.arch, 0)
     plan = tuple(int(v) for v in args.plan.split("-"))
+    peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    peak_b = pk["hbm_gbs"]
     out = {}
     rng = np.random.default_rng(0)
     seen = set()
@@ -450,36 +757,87 @@ def block_sweep(torch, args, flush):
         o = blk.output_shape
         cells = (o.height // s) * (o.width // s)
         row = {}
-        for r in (0.2, 0.5, 0.8, 1.0):
+        for r in (0.2, 0.5, 0.8, 1.0, "static"):
             xx = x.clone()
-            if args.paradigm == "channel":
+            if r == "static":
+                fn = lambda: db.forward(xx, "static", out=xx, ws=wsp)  # noqa: E731
+                a = RF.block_algorithmic(blk, "static", n)
+            elif args.paradigm == "channel":
                 # exact-count per-sample channel masks (G = plan entry), SURVEY §8(d) config 4
                 cm, g_ = blk.conv2.out_channels, s
                 d = cm // g_
                 k = int(round(r * d))
                 mm = np.zeros((n, db.cmid_p), np.uint8)
                 for i in range(n):
-                    keep = np.repeat(np.isin(np.arange(d), rng.permutation(d)[:k]), g_)
-                    mm[i, :cm] = keep
+                    mm[i, :cm] = np.repeat(np.isin(np.arange(d), rng.permutation(d)[:k]), g_)
                 chm = torch.from_numpy(mm.reshape(-1)).cuda()
                 fn = lambda: db.forward(xx, "channel", out=xx, ws=wsp, chmask=chm)  # noqa: E731
+                a = RF.block_algorithmic(blk, "channel", n, keep=mm[:, :cm].astype(bool))
+            elif args.paradigm == "layer":
+                k = int(round(r * n))
+                dec = np.zeros(n, np.uint8)
+                dec[rng.permutation(n)[:k]] = 1
+                coarse = torch.from_numpy(dec).cuda()
+                fn = lambda: db.forward(xx, "layer", 0, coarse=coarse, out=xx, ws=wsp)  # noqa: E731
+                a = RF.block_algorithmic(blk, "layer", n, decisions=dec.astype(bool))
             else:
-                k = int(round(r * cells))
-                cz = np.zeros((n, cells), np.uint8)
-                for i in range(n):
-                    cz[i, rng.permutation(cells)[:k]] = 1
+                cz = _exact_masks(rng, n, cells, r)
                 coarse = torch.from_numpy(cz.reshape(-1)).cuda()
                 fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp)  # noqa: E731
+                a = RF.block_algorithmic(blk, "spatial", n, coarse=cz.reshape(n, o.height // s, o.width // s), s=s)
             g, _ = capture(torch, fn, 2)
             tot, _ = timed_graph(torch, g, 10, flush, torch.cuda.current_stream())
-            row[str(r)] = round(1e3 * tot / 10, 1)
+            us = 1e3 * tot / 10
+            roof_us = 1e6 * RF.roofline_seconds(a["flops"], a["bytes"], peak_t, peak_b)
+            row[str(r)] = {"us": round(us, 1), "roofline_us": round(roof_us, 1), "frac": round(roof_us / us, 3),
+                           "bound": "tensor" if a["flops"] / (peak_t * 1e12) >= a["bytes"] / (peak_b * 1e9) else "hbm"}
             del g
-        xx = x.clone()
-        g, _ = capture(torch, lambda: db.forward(xx, "static", out=xx, ws=wsp), 2)
-        tot, _ = timed_graph(torch, g, 10, flush, torch.cuda.current_stream())
-        row["static"] = round(1e3 * tot / 10, 1)
         out[f"s{bp['stage']}b1_{'G' if args.paradigm == 'channel' else 'S'}{s}"] = row
     return out
+
+
+def gemm_leg(torch, flush):
+    """Dense mainloop vs cuBLAS on the same box: the conv engine as a plain GEMM
+    (contiguous A rows, 1x1) against torch.matmul at the dominant 1x1 shape and 8192^3."""
+    from paper_2308_15949_b200 import channel as CH
+    out = {}
+    for m, n, k in ((50176, 256, 1024), (50176, 1024, 256), (8192, 8192, 8192)):
+        a = torch.randn(m, k, device="cuda").bfloat16()
+        w = torch.randn(n, 1, k, device="cuda").bfloat16()
+        y = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        fn = lambda: CH.conv(act=a, in_hw=(m, 1), in_c=k, in_ld=k, weight=w, n_out=n, out=y, out_ld=n,  # noqa: E731
+                             out_hw=(m, 1), batch=1, a_compact=1)
+        g, _ = capture(torch, fn, 2)
+        t_l, _ = timed_graph(torch, g, 10, flush, torch.cuda.current_stream())
+        del g
+        wt = w.view(n, k)
+        g, _ = capture(torch, lambda: torch.matmul(a, wt.t()), 2)
+        t_c, _ = timed_graph(torch, g, 10, flush, torch.cuda.current_stream())
+        del g
+        f = 2.0 * m * n * k
+        out[f"{m}x{n}x{k}"] = {"laud_tflops": round(f / (t_l / 10 * 1e-3) / 1e12, 1),
+                               "cublas_tflops": round(f / (t_c / 10 * 1e-3) / 1e12, 1)}
+    torch.cuda.empty_cache()
+    return out
+
+
+def calibrate(torch, args, net, ws, rank):
+    """Masker biases: the committed calibration of this configuration if present,
+    else calibrated live on the held-out batch; broadcast from rank 0."""
+    biases, ent = committed_biases(args)
+    src = "committed calibration file (held-out images)" if ent else None
+    if args.paradigm == "static":
+        return {"source": "none (static)"}
+    if biases is None:
+        cal = torch.from_numpy(calib_images(args.calib_images)).cuda()
+        net.calibrate(cal)
+        biases = net.masker_biases()
+        src = f"live on {args.calib_images} held-out images"
+    t = torch.tensor([float(b) for b in biases], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        torch.distributed.broadcast(t, 0)
+    net.set_masker_biases(t.tolist())
+    return {"source": src, "key": bias_key(args)}
 
 
 def run_gpu(args):
@@ -492,14 +850,18 @@ def run_gpu(args):
     else:
         torch.cuda.set_device(0)
     from paper_2308_15949_b200 import _lib
-    from paper_2308_15949_b200.network import LaudNetwork, random_images
+    from paper_2308_15949_b200.network import LaudNetwork, PipelinedRunner
     pk, pk_kind = peaks()
     lib = _lib.lib()
 
+    g, lo, hi, scaling = plan_shard(args, ws, rank)
+    nb = hi - lo
     net = LaudNetwork(args.arch, args.paradigm, args.plan, args.ratio, seed=0)
-    images = random_images(args.batch, seed=1000 + rank)
-    net.calibrate(images)
+    calib = calibrate(torch, args, net, ws, rank)
+    images = torch.from_numpy(image_range(lo, hi)).cuda()
     rates = net.rate_stats(images) if args.paradigm != "static" else []
+    p_local = sum(r.get("patches", r.get("kept", 0)) for r in rates)
+    r_local = float(np.mean([r["r"] for r in rates])) if rates else 1.0
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -524,46 +886,53 @@ def run_gpu(args):
         clk.mark(t_start, time.time())
     torch.cuda.synchronize()
     if ws > 1:
-        t = torch.tensor([tot_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
         torch.distributed.barrier()
+    per_rank_ms = [v[0] for v in gather_scalars([tot_ms], "cuda")]
+    tot_ms = max(per_rank_ms)
     ms_step = tot_ms / args.steps
-    value = ws * args.batch * args.steps / (tot_ms * 1e-3)
+    value = g * args.steps / (tot_ms * 1e-3)
 
     # ---- e2e: pinned host images -> device, forward, logits -> host, every step,
     # through the public streaming runner (upload of batch i+1 overlaps batch i)
-    from paper_2308_15949_b200.network import PipelinedRunner
     host_img = torch.empty(images.shape, dtype=torch.uint8, pin_memory=True)
     host_img.copy_(images.cpu())
     n_cls = logits.shape[1]
-    host_out = torch.empty((args.steps, args.batch, n_cls), dtype=torch.float32, pin_memory=True)
-    runner = PipelinedRunner(net, args.batch, images.shape[1], images.shape[2])
+    host_out = torch.empty((args.steps, nb, n_cls), dtype=torch.float32, pin_memory=True)
+    runner = PipelinedRunner(net, nb, images.shape[1], images.shape[2])
     runner.run([host_img] * 2, host_out)  # warm
     if ws > 1:
         torch.distributed.barrier()
     e_tot = runner.run([host_img] * args.steps, host_out, before_step=flush.zero_)
-    if ws > 1:
-        t = torch.tensor([e_tot], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e_tot = float(t.item())
-    e2e = {"value": ws * args.batch * args.steps / (e_tot * 1e-3), "unit": "images/s",
-           "h2d_bytes_per_step": int(host_img.numel()), "d2h_bytes_per_step": int(args.batch * n_cls * 4),
+    e_tot = max(v[0] for v in gather_scalars([e_tot], "cuda"))
+    e2e = {"value": g * args.steps / (e_tot * 1e-3), "unit": "images/s",
+           "h2d_bytes_per_step": int(host_img.numel()) * ws, "d2h_bytes_per_step": int(nb * n_cls * 4) * ws,
            "path": "network.PipelinedRunner (public API): per step a pinned uint8 upload (copy stream, "
                    "overlapping the previous step's forward), the forward as a CUDA graph and the fp32 "
                    "logits download; the 256 MiB L2 flush before every step is inside the timed region"}
     del runner
 
+    # ---- checking (outside timing): NCCL gather of logits vs single-GPU forwards; per-rank P
+    graph.replay()
+    torch.cuda.synchronize()
+    local_logits = logits[:, :1000].float().clone()
+
+    def recompute(a, b):
+        out = net.forward(torch.from_numpy(image_range(a, b)).cuda())[:, :1000].float().clone()
+        torch.cuda.synchronize()
+        return out
+
+    logits_check = check_shards(local_logits, g, ws, rank, recompute)
+    per_rank = gather_scalars([p_local, r_local, nb], "cuda")
+
     extra = {}
-    roof = conv_roofline(torch, net, images, pk, pk_kind)
-    prof = ROOT / "profiles" / "conv_traffic.json"
-    if prof.exists():  # ncu --set full dram bytes of the same launch shape (profiles/)
-        try:
-            t = json.loads(prof.read_text())
-            if t.get("shape") == roof.get("shape"):
-                roof["traffic"] = t.get("traffic_per_launch")
-        except Exception:
-            pass
+    recs = profile_launches(torch, net, images)
+    roof = conv_roofline(recs, pk, pk_kind)
+    if rank == 0 and ws == 1 and not args.no_traffic:
+        tr = traffic_pass(args, roof)
+        if tr:
+            roof["traffic"] = tr.get("traffic")
+            roof["traffic_source"] = tr
+    step_roof = network_roofline(net, images, ms_step, pk)
     if rank == 0 and not args.no_baselines and ws == 1:
         # static baselines on the same weights and a cuDNN library baseline
         snet = LaudNetwork(args.arch, "static", args.plan, 1.0, seed=0)
@@ -572,62 +941,109 @@ def run_gpu(args):
         static_ms = s_tot / max(3, args.steps // 2)
         del sg, snet
         torch.cuda.empty_cache()
-        cud = static_cudnn_ms(torch, args.batch, max(3, args.steps // 2), 2, flush, args.arch)
+        cud = static_cudnn_ms(torch, nb, max(3, args.steps // 2), 2, flush, args.arch)
         extra["static_inhouse_ms"] = round(static_ms, 3)
         extra["static_cudnn_ms"] = round(cud, 3) if cud else None
         extra["latency_reduction_vs_static_inhouse"] = round(1 - ms_step / static_ms, 4)
         if cud:
             extra["latency_reduction_vs_static_cudnn"] = round(1 - ms_step / cud, 4)
-        try:
-            extra["batch1_latency_ms"] = batch1_latency(torch, args, net, flush)
-        except Exception as exc:
-            extra["batch1_latency_ms"] = f"failed: {exc!r}"
-        try:
-            extra["per_block_us_vs_ratio"] = block_sweep(torch, args, flush)
-        except Exception as exc:  # never lose the headline line to the sweep
-            extra["per_block_us_vs_ratio"] = f"failed: {exc!r}"
-        if args.paradigm == "spatial" and ws == 1:
+        for name, fn in (("batch1_latency_ms", lambda: batch1_latency(torch, args, net, flush)),
+                         ("per_block_us_vs_ratio", lambda: block_sweep(torch, args, flush, pk)),
+                         ("gemm_vs_cublas", lambda: gemm_leg(torch, flush))):
+            try:
+                extra[name] = fn()
+            except Exception as exc:  # never lose the headline line to a side leg
+                extra[name] = f"failed: {exc!r}"
+        if args.paradigm == "spatial":
             try:
                 extra["per_block_b1_vs_cpu"] = block_sweep_b1_vs_cpu(torch, args, flush)
             except Exception as exc:
                 extra["per_block_b1_vs_cpu"] = f"failed: {exc!r}"
     cpu = None
     if rank == 0 and ws == 1 and not args.no_baselines:
-        v, ts = cpu_oracle_images_per_s(args, args.cpu_images, params=net.params,
-                                        biases=net.masker_biases())
+        v, ts = cpu_port_images_per_s(args, args.cpu_images, net)
         cpu = {"value": round(v, 4), "unit": "images/s", "cores": blas_threads(), "kind": "port",
-               "sample": f"{args.cpu_images} synthetic images, batch 1, through the numpy fp64 oracle "
-                         f"network (same weights and masker biases), median of {len(ts)}"}
+               "sample": f"{args.cpu_images} synthetic images, batch 1, through the numpy fp64 port of the "
+                         f"network (same weights and masker biases), median of {len(ts)}; the shipped "
+                         "reference's per-block times are in per_block_b1_vs_cpu and the --impl reference arm"}
     if rank == 0:
-        r_mean = float(np.mean([r["r"] for r in rates])) if rates else 1.0
         line = {
             "metric": "images_per_sec", "value": round(value, 2), "unit": "images/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic",
-            "config": {"workload": f"LAUDNet-{args.arch} {args.paradigm} S={args.plan} ratio {args.ratio}, "
-                                   f"224x224, batch {args.batch} per GPU (BASELINE config 3, throughput)",
-                       "global_batch": ws * args.batch, "arch": args.arch, "plan": args.plan,
-                       "target_ratio": args.ratio, "measured_ratio_mean": round(r_mean, 4),
-                       "l2_policy": "256 MiB L2 flush before every timed step",
-                       "parallelism": f"batch-shard x{ws} (no collective on the hot path)",
-                       "graph": True},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches_per_step * args.steps),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded uint8 images, random-init weights)",
+            "config": bench_config(args, ws, g, scaling),
+            "measured_ratio_mean": round(float(np.mean([p[1] for p in per_rank])), 4),
+            "masker_calibration": calib,
+            "per_rank": [{"rank": i, "images": int(p[2]), "active_patches_P": int(p[0]), "ratio": round(p[1], 4),
+                          "ms_total": round(per_rank_ms[i], 3)} for i, p in enumerate(per_rank)],
+            "logits_check": logits_check,
+            "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu,
+            "gpu_launches": int(launches_per_step * args.steps), "launches_per_step": int(launches_per_step),
             "clocks": clk.summary(),
         }
         line.update(extra)
         print(json.dumps(line), flush=True)
     if ws > 1:
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 
 
-def main():
-    args = parse()
+def cpu_port_images_per_s(args, n_images, net):
+    """The numpy port of the whole network (same weights and biases), batch 1."""
+    from oracle import laud_oracle as O
+    plan = tuple(int(v) for v in args.plan.split("-"))
+    img = image_range(0, 1)
+    t = []
+    for _ in range(n_images):
+        t0 = time.perf_counter()
+        O.network_forward(net.params, img, args.paradigm, plan, net.masker_biases())
+        t.append(time.perf_counter() - t0)
+    return 1.0 / statistics.median(t), t
+
+
+def run_traffic_probe(args):
+    """Child of ``traffic_pass`` under ncu: two eager forwards of the network."""
+    import torch
+    from paper_2308_15949_b200.network import LaudNetwork
+    torch.cuda.set_device(0)
+    net = LaudNetwork(args.arch, args.paradigm, args.plan, args.ratio, seed=0)
+    b, _ = committed_biases(args)
+    images = torch.from_numpy(image_range(0, args.batch)).cuda()
+    if b is not None:
+        net.set_masker_biases(b)
+    elif args.paradigm != "static":
+        net.calibrate(torch.from_numpy(calib_images(args.calib_images)).cuda())
+    net.forward(images)
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("laud_probe")  # the forward ncu measures
+    net.forward(images)
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def main(argv=None):
+    args = parse(argv)
+    if args.traffic_probe:
+        return run_traffic_probe(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torch.distributed.run (rank 0 prints the line)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve())]
+        cmd += sys.argv[1:] if argv is None else list(argv)
+        return subprocess.call(cmd)
     if args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

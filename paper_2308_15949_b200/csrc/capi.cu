@@ -22,6 +22,9 @@ namespace laud {
 cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn,
                              const ConvParams& p, int num_sms, cudaStream_t stream, int pair);
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t stream);
+bool patch_conv_supported(int s, int bn);
+cudaError_t launch_patch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, int s, int bn,
+                              int num_sms, cudaStream_t stream);
 size_t scan_state_bytes(int total);
 int masker_splits(int win, int c, int* chunks_per_split);
 cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h, int w, int c,
@@ -369,6 +372,40 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
     return cuda_check(launch_conv_f32(p, st), "conv_f32 launch", 1);
   }
+  // Patch conv2 with the halo in shared memory (patch_conv.cu): stride-1 3x3
+  // over S = 2 / 4 patches, compact output rows, plain affine epilogue
+  static const int halo_env = [] {
+    const char* e = getenv("LAUD_HALO");
+    return e ? atoi(e) : 1;
+  }();
+  if (halo_env && !ad && a->row_mode == ROWS_PATCH && a->ksize == 3 && a->stride == 1 && a->pad == 1 &&
+      p.groups == 1 && !a->a_compact && !a->sample_rows && !a->chan_count && !a->b_batched &&
+      a->out_mode == OUT_ROW && !a->resid && !a->ymask_coarse && !a->ymask_channel && !a->mdot_w &&
+      !a->relu_inactive_coarse && !a->out_f32 && !a->col_index && !a->misplace_first &&
+      a->patch_h == a->patch_w && a->in_h == a->out_h && a->in_w == a->out_w && a->n_out <= 512 &&
+      (reinterpret_cast<uintptr_t>(a->act) % 16) == 0 && (long long)a->batch * a->in_h * a->in_w < (1ll << 31) - 1) {
+    const int s = a->patch_h;
+    const int hbn = s == 4 ? 64 : (a->n_out % 128 == 0 ? 128 : 64);
+    if (patch_conv_supported(s, hbn)) {
+      p.a_rows = a->batch * a->in_h * a->in_w;
+      int rc;
+      CUtensorMap ma, mb;
+      const int kw = 9 * p.kpad;
+      if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, 1, &ma)) ||
+          (rc = tensor_map_2d(a->weight, a->n_out, kw, kw, hbn, &mb)))
+        return rc;
+      ProfScope ps(0, st, a->count);
+      if (ps.on) {
+        ps.rec.rows_per_count = (long long)s * s;
+        ps.rec.rows_max = a->rows_max;
+        ps.rec.n_out = a->n_out;
+        ps.rec.k_alg = 9LL * a->in_c;
+        ps.rec.taps = 9;
+        ps.rec.resid = 0;
+      }
+      return cuda_check(launch_patch_conv(ma, mb, p, s, hbn, num_sms(), st), "patch conv launch", 1);
+    }
+  }
   // grouped: narrow tiles keep the block-diagonal K window short
   const int bn = p.groups > 1 ? 64 : pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   const int kw = a->ksize * a->ksize * p.kpad;
@@ -439,7 +476,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     ps.rec.rows_per_count = a->row_mode == ROWS_PATCH ? (long long)p.patch_h * p.patch_w : 1;
     ps.rec.rows_max = a->rows_max;
     ps.rec.n_out = a->n_out;
-    ps.rec.k_alg = (long long)a->ksize * a->ksize * a->in_c;
+    ps.rec.k_alg = (long long)a->ksize * a->ksize * a->in_c / p.groups;  // grouped: C_in / groups per output
     ps.rec.taps = a->ksize * a->ksize;
     ps.rec.resid = a->resid != nullptr;
   }

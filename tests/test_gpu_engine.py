@@ -88,6 +88,43 @@ def test_patch_rows_gather_scatter():
     assert err < 6e-3, float(err)
 
 
+@pytest.mark.parametrize("s,cin,cout,n,h,density", [
+    (2, 256, 256, 8, 14, 0.5), (2, 128, 128, 4, 28, 0.5), (4, 64, 64, 4, 56, 0.5), (2, 64, 64, 3, 16, 0.3),
+    (4, 128, 128, 2, 28, 0.7), (2, 256, 256, 64, 14, 0.5), (2, 40, 24, 2, 8, 1.0), (4, 64, 64, 1, 8, 0.0)])
+def test_patch_conv_halo_smem(s, cin, cout, n, h, density):
+    """3x3 patch conv over active S x S cells (the halo-in-shared-memory kernel for
+    S = 2 / 4, stride 1): ragged patch counts (not a multiple of the tile's patch
+    count), image-border cells (zero halo), several N tiles, scale/bias/ReLU."""
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(s * 1000 + cin + n)
+    x = torch.randn(n, h, h, cin, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(cout, cin, 3, 3, generator=g) / np.sqrt(9 * cin)).to(torch.bfloat16).float()
+    sc = torch.rand(cout, generator=g) + 0.5
+    bi = torch.randn(cout, generator=g) * 0.1
+    hc = h // s
+    rng = np.random.default_rng(n + h)
+    cells = np.flatnonzero(rng.random(n * hc * hc) < density).astype(np.int32)
+    lst = torch.from_numpy(np.concatenate([cells, np.zeros(4, np.int32)])).cuda()
+    cnt = torch.tensor([len(cells)], dtype=torch.int32, device="cuda")
+    rows = torch.full((max(len(cells), 1) * s * s, cout), 7.0, dtype=torch.bfloat16, device="cuda")
+    CH.conv(act=x, in_hw=(h, h), in_c=cin, in_ld=cin, weight=D.pack_weight(w, cin), n_out=cout, out=rows,
+            out_ld=cout, out_hw=(h, h), batch=n, ksize=3, pad=1, row_mode=CH.ROWS_PATCH,
+            rows_max=n * h * h, lst=lst, count=cnt, patch=(s, s), cells=(hc, hc),
+            out_mode=CH.OUT_ROW, scale=sc.cuda(), bias=bi.cuda(), relu=1)
+    torch.cuda.synchronize()
+    if len(cells) == 0:
+        assert (rows.float() == 7.0).all()
+        return
+    ref = torch.relu(_torch_conv_nhwc(x, w.cuda(), 1, 1) * sc.cuda() + bi.cuda())
+    idx = torch.from_numpy(cells.astype(np.int64))
+    ni, r = idx // (hc * hc), idx % (hc * hc)
+    ci, cj = r // hc, r % hc
+    exp = torch.stack([ref[a, b * s:(b + 1) * s, c * s:(c + 1) * s].reshape(s * s, cout)
+                       for a, b, c in zip(ni.tolist(), ci.tolist(), cj.tolist())]).reshape(-1, cout)
+    err = (rows.float() - exp).norm() / exp.norm()
+    assert err < 6e-3, float(err)
+
+
 def test_compaction_matches_argwhere():
     from paper_2308_15949_b200 import reference as R
     rng = np.random.default_rng(0)

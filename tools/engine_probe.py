@@ -36,6 +36,11 @@ def shape_defs():
     d["conv2_s1"] = dict(kind="conv3x3", n=256, h=56, c=64)
     d["conv1_s1"] = dict(kind="gemm", m=256 * 56 * 56, n=64, k=256)
     d["conv3_s3"] = dict(kind="conv3", m=25088, n=1024, k=256)
+    # patch conv2 over active S x S cells at r = 0.5 (the LAUD schedule's conv2)
+    d["pconv_s3"] = dict(kind="patch", n=256, h=14, c=256, s=2)
+    d["pconv_s2"] = dict(kind="patch", n=256, h=28, c=128, s=2)
+    d["pconv_s1"] = dict(kind="patch", n=256, h=56, c=64, s=4)
+    d["pconv_s3_b1"] = dict(kind="patch", n=1, h=14, c=256, s=2)
     d["conv3_s1"] = dict(kind="conv3", m=256 * 56 * 56 // 2, n=256, k=64)
     return d
 
@@ -54,6 +59,22 @@ def run(name, spec, flush, reps=20):
                   relu=1)
         flops = 2.0 * m * n * k
         nbytes = 2.0 * (m * k + n * k + m * n * (2 if resid is not None else 1))
+    elif spec["kind"] == "patch":
+        import numpy as np
+        b, h, c, s = spec["n"], spec["h"], spec["c"], spec["s"]
+        a = bf(b, h, h, c)
+        w = bf(c, 9, c)
+        hc = h // s
+        cells = np.sort(np.random.default_rng(0).permutation(b * hc * hc)[: b * hc * hc // 2]).astype(np.int32)
+        lst = torch.from_numpy(cells).cuda()
+        cnt = torch.tensor([len(cells)], dtype=torch.int32, device="cuda")
+        m = len(cells) * s * s
+        out = torch.empty(m, c, dtype=torch.bfloat16, device="cuda")
+        kw = dict(act=a, in_hw=(h, h), in_c=c, in_ld=c, weight=w, n_out=c, out=out, out_ld=c,
+                  out_hw=(h, h), batch=b, ksize=3, pad=1, relu=1, out_mode=CH.OUT_ROW, row_mode=CH.ROWS_PATCH,
+                  rows_max=b * h * h, lst=lst, count=cnt, patch=(s, s), cells=(hc, hc))
+        flops = 2.0 * m * c * 9 * c
+        nbytes = 2.0 * (b * h * h * c + m * c + 9 * c * c)
     else:
         b, h, c = spec["n"], spec["h"], spec["c"]
         a = bf(b, h, h, c)
@@ -82,7 +103,7 @@ def run(name, spec, flush, reps=20):
     return dict(name=name, us=round(ms * 1e3, 2), tflops=round(flops / ms / 1e9, 1),
                 gbs=round(nbytes / ms / 1e6, 1), ideal_us_tensor=round(flops / 1.3841e15 * 1e6, 2),
                 ideal_us_hbm=round(nbytes / 6.55e12 * 1e6, 2),
-                env={k: os.environ.get(k) for k in ("LAUD_BN", "LAUD_A_TMA", "LAUD_CTA2") if os.environ.get(k)})
+                env={k: os.environ.get(k) for k in ("LAUD_BN", "LAUD_A_TMA", "LAUD_CTA2", "LAUD_HALO") if os.environ.get(k)})
 
 
 def main():
