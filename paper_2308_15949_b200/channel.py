@@ -94,15 +94,11 @@ def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None):
     D.require_cuda()
     w1, w2 = (np.asarray(w, dtype=np.float64) for w in weights)
     hd, c = w1.shape
-    xn = np.asarray(x)
-    if xn.shape[1] != c:
-        raise ShapeMismatch(f"input has {xn.shape[1]} channels, masker expects {c}")
     if w2.shape[1] != hd or w2.shape[0] % 2:
         raise ShapeMismatch("second MLP layer must map hidden -> 2*D")
     d = w2.shape[0] // 2
-    n, _, h, w = xn.shape
-    xd = D.to_device_nhwc(xn, dtype=torch.float32)
-    cp = xd.shape[-1]
+    xd, numpy_in = R._dev_in(x, c, x.dtype if isinstance(x, torch.Tensor) else torch.float32)
+    n, h, w, cp = xd.shape
     cm = d * g
     cmp = D.pad8(cm)
     w1p = np.zeros((hd, cp), np.float32)
@@ -114,10 +110,14 @@ def channel_masker_forward(x, weights, g, mode="inference", tau=None, rng=None):
     exp = torch.empty(n * cmp, dtype=torch.uint8, device="cuda")
     sel = torch.empty(n * cmp, dtype=torch.int32, device="cuda")
     cnt = torch.empty(n, dtype=torch.int32, device="cuda")
-    _lib.call("laud_channel_masker", D.ptr(xd), 1, cp, n, h * w, cp, D.ptr(t_w1), hd, D.ptr(t_w2),
+    _lib.call("laud_channel_masker", D.ptr(xd), int(xd.dtype == torch.float32), cp, n, h * w, cp, D.ptr(t_w1),
+              hd, D.ptr(t_w2),
               d, g, cm, cmp, D.ptr(coarse), D.ptr(dvals), D.ptr(exp), D.ptr(sel), D.ptr(cnt),
               None, D.stream_handle())
     soft = None
+    if mode == "inference" and not numpy_in:  # stays on the device
+        cz = coarse.view(n, d).bool()
+        return R.ChannelMask(cz, cz.repeat_interleave(g, dim=1), g, None)
     if mode == "inference":
         cz = coarse.view(n, d).bool().cpu().numpy()
     else:
@@ -133,19 +133,15 @@ def channel_block_sparse(x, bw, block, mask, grouped_channel_ext: bool = False):
     (`reference.py:405-406`): a grouped conv2 runs as its block-diagonal dense
     kernel, the sparse form of the reference's dense-masked channel forward."""
     import numpy as np
-    from .errors import MaskShapeMismatch, ShapeMismatch
+    from .errors import ShapeMismatch
     R = _rm()
     if block.conv2.groups != 1 and not grouped_channel_ext:
         raise ShapeMismatch("sparse channel execution requires groups == 1")
-    n = x.shape[0]
-    m = np.asarray(mask.expanded)
-    if m.shape != (n, block.conv2.out_channels):
-        raise MaskShapeMismatch(f"channel mask {m.shape} != {(n, block.conv2.out_channels)}")
     db = R.device_block(bw, block)
     if block.conv2.groups != 1:
         db.enable_grouped_channel()
-    mm = np.zeros((n, db.cmid_p), np.uint8)
-    mm[:, : m.shape[1]] = m
-    xd = D.to_device_nhwc(x, dtype=db.dtype)
-    y, *_ = db.forward(xd, "channel", chmask=torch.from_numpy(mm.reshape(-1)).cuda())
-    return D.from_device_nhwc(y, block.output_shape.channels)
+    xd, numpy_in = R._dev_in(x, block.input_shape.channels, db.dtype)
+    n = xd.shape[0]
+    chm = R._channel_mask_u8(mask.expanded, n, block.conv2.out_channels, db.cmid_p)
+    y, *_ = db.forward(xd, "channel", chmask=chm)
+    return R._dev_out(y, block.output_shape.channels, numpy_in)

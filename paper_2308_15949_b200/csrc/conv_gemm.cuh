@@ -223,6 +223,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   pdl_wait();
   pdl_trigger();
   const int nvalid = rows_valid(p);
+  // K order: for each 64-channel block, the k x k taps (the order of the halo
+  // patch conv, patch_conv.cu, so the sparse and dense conv2 sum identically)
+  const int taps = p.ksize * p.ksize;
   const int n_tiles = (p.n_out + BN - 1) / BN;
   const int m_tiles = (nvalid + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
   const int tiles = m_tiles * n_tiles;
@@ -354,8 +357,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
           if (trc && tid == 0 && it < 4096) trc[TRACE_A + it] = global_ns();
-          const int tap = kb / ti.kpt;
-          const int c0 = ti.c_lo + (kb - tap * ti.kpt) * BK;
+          const int cblk = kb / taps, tap = kb - cblk * taps;  // channel-block-major K order
+          const int c0 = ti.c_lo + cblk * BK;
           const int ky = tap / p.ksize;
           const int kx = tap - ky * p.ksize;
           const uint32_t sA = base_u32 + L::A_OFF + stage * A_STAGE_BYTES;
@@ -378,8 +381,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
           if (trc && tid == 0 && it < 4096) trc[TRACE_A + it] = global_ns();
-          const int tap = kb / ti.kpt;
-          const int c0 = ti.c_lo + (kb - tap * ti.kpt) * BK;
+          const int cblk = kb / taps, tap = kb - cblk * taps;  // channel-block-major K order
+          const int c0 = ti.c_lo + cblk * BK;
           const int ky = tap / p.ksize;
           const int kx = tap - ky * p.ksize;
           int row = p.a_rows;  // out of bounds -> zero fill
@@ -425,8 +428,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
         mbar_wait(&empty[stage], phase ^ 1);
-        const int tap = kb / ti.kpt;
-        const int ch = ti.c_lo + (kb - tap * ti.kpt) * BK + chunk * 8;
+        const int cblk = kb / taps, tap = kb - cblk * taps;
+        const int ch = ti.c_lo + cblk * BK + chunk * 8;
         const int ky = tap / p.ksize;
         const int kx = tap - ky * p.ksize;
         const bool chv = ch < p.in_c;
@@ -468,8 +471,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             continue;
           }
           if (leader) mbar_arrive_expect_tx(&full[stage], XMUL * L::B_STAGE_BYTES);
-          const int tap = kb / ti.kpt;
-          const int kcoord = tap * p.kpad + ti.c_lo + (kb - tap * ti.kpt) * BK;  // per-tap stride kpad
+          const int cblk = kb / taps, tap = kb - cblk * taps;
+          const int kcoord = tap * p.kpad + ti.c_lo + cblk * BK;  // per-tap stride kpad
           const uint32_t dst = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
           if constexpr (PAIR) {  // this CTA's half of the tile's B rows
             tma_load_2d_pair(dst, &tmap_b, full_tx(stage), kcoord, ti.n0 + rank * (BN / 2));

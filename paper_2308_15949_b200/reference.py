@@ -120,6 +120,34 @@ def _scan(ws: D.Workspace, items: int) -> torch.Tensor:
     return ws.get("scan", _lib.lib().laud_scan_workspace_bytes(max(1, items)), zero=True)
 
 
+def _dev_in(x, channels: int, dtype):
+    """Block/masker input -> (device NHWC tensor, came_from_numpy).
+
+    numpy arrays are the reference's (N, C, H, W) float64 layout and are
+    converted on the device; CUDA tensors are the native layout, (N, H, W,
+    pad8(C)) in the compute dtype, and are used in place (no host round trip).
+    """
+    if isinstance(x, torch.Tensor):
+        if not x.is_cuda:
+            raise ShapeMismatch("torch inputs must be CUDA tensors in NHWC layout")
+        if x.ndim != 4:
+            raise ShapeMismatch("expected an (N, H, W, C) CUDA tensor")
+        if x.shape[-1] != D.pad8(channels):
+            raise ShapeMismatch(f"input has {x.shape[-1]} (padded NHWC) channels, expected {D.pad8(channels)}")
+        return (x if x.dtype == dtype else x.to(dtype)).contiguous(), False
+    xn = np.asarray(x)
+    if xn.ndim != 4:
+        raise ShapeMismatch("expected (N, C, H, W) input")
+    if xn.shape[1] != channels:
+        raise ShapeMismatch(f"input has {xn.shape[1]} channels, expected {channels}")
+    return D.to_device_nhwc(xn, dtype=dtype), True
+
+
+def _dev_out(y: torch.Tensor, channels: int, numpy_in: bool):
+    """numpy in -> numpy (N, C, H, W) float64 out; CUDA in -> the device NHWC tensor."""
+    return D.from_device_nhwc(y, channels) if numpy_in else y
+
+
 def _decide_train(dbar: np.ndarray, tau, rng):
     """Train-mode decision from the device logit difference d = l0 - l1.
 
@@ -146,12 +174,16 @@ def spatial_masker_forward(x, weights, s: int, mode: str = "inference",
     if mode not in ("inference", "train"):
         raise ValueError(f"unknown mode {mode!r}")
     D.require_cuda()
-    xn = np.asarray(x)
-    n, c, h, w = xn.shape
+    c = int(np.prod(np.asarray(weights).shape)) // 2
+    if isinstance(x, torch.Tensor):  # native: CUDA NHWC (bf16 or fp32), decided in fp32
+        xd, numpy_in = _dev_in(x, c, x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32)
+        n, h, w, _ = xd.shape
+    else:
+        xd, numpy_in = _dev_in(x, c, torch.float32)
+        n, h, w = xd.shape[0], xd.shape[1], xd.shape[2]
     if h % s or w % s:
         raise GranularityMismatch(f"S={s} does not divide {h}x{w}")
     wts = np.asarray(weights, dtype=np.float64).reshape(2, c)
-    xd = D.to_device_nhwc(xn, dtype=torch.float32)
     cp = xd.shape[-1]
     wd = np.zeros(cp, np.float32)
     wd[:c] = (wts[0] - wts[1]).astype(np.float32)
@@ -164,11 +196,15 @@ def spatial_masker_forward(x, weights, s: int, mode: str = "inference",
     coarse = torch.empty(cells, dtype=torch.uint8, device="cuda")
     lst = torch.empty(max(1, cells), dtype=torch.int32, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.call("laud_spatial_masker", D.ptr(xd), 1, cp, n, h, w, cp, s, 1, D.ptr(wdt), 0.0,
+    _lib.call("laud_spatial_masker", D.ptr(xd), int(xd.dtype == torch.float32), cp, n, h, w, cp, s, 1,
+              D.ptr(wdt), 0.0,
               D.ptr(coarse), D.ptr(lst), D.ptr(cnt), D.ptr(part), D.ptr(_scan(ws, cells)),
               D.stream_handle())
     shape = (n, h // s, w // s)
     soft = None
+    if mode == "inference" and not numpy_in:  # stays on the device, no host sync
+        cz = coarse.view(shape).bool()
+        return SpatialMask(cz, upsample_coarse(cz, s), s, None)
     if mode == "inference":
         cz = coarse.view(shape).bool().cpu().numpy()
     else:
@@ -272,6 +308,48 @@ def make_block_weights(block: BlockSpec, rng: np.random.Generator) -> BlockWeigh
     return BlockWeights(draw(block.conv1), draw(block.conv2), draw(block.conv3), wd)
 
 
+_DEV_CONVS: dict = {}
+
+
+def conv2d_direct(x, layer: ConvLayerSpec, weights: np.ndarray):
+    """Validated direct convolution, k//2 zero padding, stride, groups, bias-free
+    (`reference.py:52-69`), as one tcgen05 implicit GEMM (fp32 FFMA engine in
+    fp32 precision mode).  numpy (N, C, H, W) in -> numpy out; a CUDA NHWC
+    tensor in -> the NHWC device tensor out (pad8(C_out) channels)."""
+    D.require_cuda()
+    from . import channel as CH
+    w = np.asarray(weights)
+    want = (layer.out_channels, layer.in_channels // layer.groups, layer.kernel, layer.kernel)
+    if isinstance(x, torch.Tensor):
+        if x.ndim != 4:
+            raise ShapeMismatch("expected an (N, H, W, C) CUDA tensor")
+    elif np.asarray(x).ndim != 4:
+        raise ShapeMismatch("expected (N, C, H, W) input")
+    elif np.asarray(x).shape[1] != layer.in_channels:
+        raise ShapeMismatch(f"input has {np.asarray(x).shape[1]} channels, layer expects {layer.in_channels}")
+    if w.shape != want:
+        raise ShapeMismatch(f"weights {w.shape} != expected {want}")
+    dt = _PRECISION["dtype"]
+    g = layer.groups
+    if g > 1 and ((layer.in_channels // g) % 8 or (layer.out_channels // g) % 8):
+        w, g = D.grouped_to_dense(w, g), 1  # narrow groups: the block-diagonal dense kernel (same sums)
+    xd, numpy_in = _dev_in(x, layer.in_channels, dt)
+    key = (id(weights), want, dt)
+    ent = _DEV_CONVS.get(key)
+    if ent is None or ent[0] is not weights:
+        ent = (weights, D.pack_weight(w, D.pad8(layer.in_channels), groups=g, dtype=dt), g)
+        _DEV_CONVS[key] = ent
+    n, h, ww, cp = xd.shape
+    k, st = layer.kernel, layer.stride
+    ho, wo = (h + 2 * (k // 2) - k) // st + 1, (ww + 2 * (k // 2) - k) // st + 1
+    co = D.pad8(layer.out_channels)
+    y = torch.empty((n, ho, wo, co), dtype=dt, device=xd.device)
+    CH.conv(act=xd, in_hw=(h, ww), in_c=cp, in_ld=cp, weight=ent[1], n_out=co, out=y, out_ld=co,
+            out_hw=(ho, wo), batch=n, ksize=k, stride=st, pad=k // 2, groups=ent[2],
+            fp32=int(dt == torch.float32))
+    return _dev_out(y, layer.out_channels, numpy_in)
+
+
 _DEV_BLOCKS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
@@ -332,6 +410,8 @@ def _check_input(x, block: BlockSpec):
 
 
 def _u8(a) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.uint8).reshape(-1).contiguous()
     return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.uint8).reshape(-1)).cuda()
 
 
@@ -348,28 +428,25 @@ def block_forward_sparse(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConf
     runs channel skipping over a grouped conv2 (`channel.channel_block_sparse`).
     """
     D.require_cuda()
-    x = np.asarray(x)
-    _check_input(x, block)
-    n = x.shape[0]
     p = cfg.paradigm
     if p is Paradigm.CHANNEL:
         from . import channel as CH
         return CH.channel_block_sparse(x, bw, block, mask, grouped_channel_ext=grouped_channel_ext)
     db = device_block(bw, block)
-    xd = D.to_device_nhwc(x, dtype=db.dtype)
+    xd, numpy_in = _dev_in(x, block.input_shape.channels, db.dtype)
+    n = xd.shape[0]
     out = block.output_shape
     if p is Paradigm.SPATIAL:
         _check_spatial_mask(mask, block, n)
         y, *_ = db.forward(xd, "spatial", mask.granularity, coarse=_u8(mask.coarse),
                            misplace_first=_misplace_first_patch)
     elif p is Paradigm.LAYER:
-        d = np.asarray(mask.decisions)
-        if d.shape != (n,):
-            raise MaskShapeMismatch(f"layer mask {d.shape} != {(n,)}")
-        y, *_ = db.forward(xd, "layer", out.height, coarse=_u8(d))
+        if tuple(mask.decisions.shape) != (n,):
+            raise MaskShapeMismatch(f"layer mask {tuple(mask.decisions.shape)} != {(n,)}")
+        y, *_ = db.forward(xd, "layer", out.height, coarse=_u8(mask.decisions))
     else:
         y, *_ = db.forward(xd, "static")
-    return D.from_device_nhwc(y, out.channels)
+    return _dev_out(y, out.channels, numpy_in)
 
 
 def block_forward_dense_masked(x, bw: BlockWeights, block: BlockSpec, cfg: DynamicConfig, mask):
@@ -381,12 +458,10 @@ def block_forward_dense_masked(x, bw: BlockWeights, block: BlockSpec, cfg: Dynam
     """
     from . import channel as CH
     D.require_cuda()
-    x = np.asarray(x)
-    _check_input(x, block)
-    n = x.shape[0]
     p = cfg.paradigm
     db = device_block(bw, block)
-    xd = D.to_device_nhwc(x, dtype=db.dtype)
+    xd, numpy_in = _dev_in(x, block.input_shape.channels, db.dtype)
+    n = xd.shape[0]
     out = block.output_shape
     ymask = None
     chmask = None
@@ -396,19 +471,23 @@ def block_forward_dense_masked(x, bw: BlockWeights, block: BlockSpec, cfg: Dynam
         ymask = _u8(mask.coarse)
         patch = (mask.granularity, mask.granularity)
     elif p is Paradigm.CHANNEL:
-        m = np.asarray(mask.expanded)
-        if m.shape != (n, block.conv2.out_channels):
-            raise MaskShapeMismatch(f"channel mask {m.shape} != {(n, block.conv2.out_channels)}")
-        mm = np.zeros((n, db.cmid_p), np.uint8)
-        mm[:, : m.shape[1]] = m
-        chmask = _u8(mm)
+        chmask = _channel_mask_u8(mask.expanded, n, block.conv2.out_channels, db.cmid_p)
     elif p is Paradigm.LAYER:
-        d = np.asarray(mask.decisions)
-        if d.shape != (n,):
-            raise MaskShapeMismatch(f"layer mask {d.shape} != {(n,)}")
-        ymask = _u8(d)
+        if tuple(mask.decisions.shape) != (n,):
+            raise MaskShapeMismatch(f"layer mask {tuple(mask.decisions.shape)} != {(n,)}")
+        ymask = _u8(mask.decisions)
     y = CH.dense_block(db, xd, ymask=ymask, patch=patch, chmask=chmask)
-    return D.from_device_nhwc(y, out.channels)
+    return _dev_out(y, out.channels, numpy_in)
+
+
+def _channel_mask_u8(m, n: int, cm: int, cmp: int) -> torch.Tensor:
+    """(N, C_mid) keep mask (numpy or CUDA tensor) -> device uint8 [N * pad8(C_mid)]."""
+    if tuple(m.shape) != (n, cm):
+        raise MaskShapeMismatch(f"channel mask {tuple(m.shape)} != {(n, cm)}")
+    mm = torch.zeros((n, cmp), dtype=torch.uint8, device="cuda")
+    mm[:, :cm] = m.to(device="cuda", dtype=torch.uint8) if isinstance(m, torch.Tensor) else \
+        torch.from_numpy(np.ascontiguousarray(np.asarray(m), dtype=np.uint8)).cuda()
+    return mm.reshape(-1)
 
 
 # ---------------------------------------------------------------------------

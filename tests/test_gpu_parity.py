@@ -547,3 +547,82 @@ def test_regnet_grouped_channel_ext_block(stage, r):
     yd = O.block_forward_dense_masked(x, O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down), block, cfg,
                                       O.ChannelMask(coarse, coarse, 1))
     assert _rel(y, yd) <= 1e-2
+
+
+def test_conv2d_direct_matches_reference_golden():
+    """conv2d_direct (`reference.py:52-69`) through the drop-in: the reference's own
+    outputs (golden, incl. a grouped strided conv), its validation errors, and the
+    CUDA-NHWC-in / CUDA-NHWC-out form."""
+    import torch
+    R = _R()
+    from paper_2308_15949_b200.errors import ShapeMismatch
+    a = np.load(G / "convs.npz")
+    l1 = ConvLayerSpec(16, 8, 1)
+    l2 = ConvLayerSpec(8, 8, 3, 2, 2)
+    y1 = R.conv2d_direct(a["conv_x"], l1, a["bw_w1"])
+    assert _rel(y1, a["conv1_y"]) <= 5e-3  # bf16 storage
+    y2 = R.conv2d_direct(a["conv2_x"], l2, a["bw_w2"])
+    assert _rel(y2, a["conv2_y"]) <= 5e-3
+    with pytest.raises(ShapeMismatch):
+        R.conv2d_direct(a["conv_x"][:, :8], l1, a["bw_w1"])
+    with pytest.raises(ShapeMismatch):
+        R.conv2d_direct(a["conv_x"], l1, a["bw_w1"][:4])
+    from paper_2308_15949_b200 import device as D
+    xd = D.to_device_nhwc(a["conv_x"])
+    yd = R.conv2d_direct(xd, l1, a["bw_w1"])
+    assert isinstance(yd, torch.Tensor) and yd.is_cuda and tuple(yd.shape) == (2, 10, 10, 8)
+    np.testing.assert_array_equal(D.from_device_nhwc(yd, 8), y1)
+
+
+def test_conv2d_direct_fp32_mode(fp32_mode):
+    R = fp32_mode
+    a = np.load(G / "convs.npz")
+    assert _rel(R.conv2d_direct(a["conv_x"], ConvLayerSpec(16, 8, 1), a["bw_w1"]), a["conv1_y"]) <= 1e-5
+    assert _rel(R.conv2d_direct(a["conv2_x"], ConvLayerSpec(8, 8, 3, 2, 2), a["bw_w2"]), a["conv2_y"]) <= 1e-5
+
+
+def test_mirror_accepts_cuda_nhwc_tensors():
+    """The drop-in's native form: CUDA NHWC tensors in, device
+    tensors out, no host round trip; identical to the numpy NCHW form."""
+    import torch
+    R = _R()
+    from paper_2308_15949_b200 import device as D
+    from paper_2308_15949_b200.zoo import build_network
+    block = [b.block for b in build_network("resnet50").blocks if b.stage == 3 and b.index == 1][0]
+    rng = np.random.default_rng(3)
+    bw = R.make_block_weights(block, rng)
+    x = O.round_bf16(rng.standard_normal((2, 1024, 14, 14)))
+    mw = rng.standard_normal((2, 1024, 1, 1)) / 32.0
+    xd = D.to_device_nhwc(x)  # bf16 NHWC
+    m_np = R.spatial_masker_forward(x, mw, 2)
+    m_d = R.spatial_masker_forward(xd, mw, 2)
+    assert isinstance(m_d.coarse, torch.Tensor) and m_d.coarse.is_cuda
+    np.testing.assert_array_equal(m_d.coarse.cpu().numpy(), m_np.coarse)
+    cfg = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=2)
+    y_np = R.block_forward_sparse(x, bw, block, cfg, m_np)
+    y_d = R.block_forward_sparse(xd, bw, block, cfg, m_d)
+    assert isinstance(y_d, torch.Tensor) and y_d.is_cuda and y_d.dtype == torch.bfloat16
+    np.testing.assert_array_equal(D.from_device_nhwc(y_d, 1024), y_np)
+    yd_np = R.block_forward_dense_masked(x, bw, block, cfg, m_np)
+    np.testing.assert_array_equal(D.from_device_nhwc(R.block_forward_dense_masked(xd, bw, block, cfg, m_d), 1024),
+                                  yd_np)
+    lay = DynamicConfig(Paradigm.LAYER)
+    dec = np.array([True, False])
+    np.testing.assert_array_equal(
+        D.from_device_nhwc(R.block_forward_sparse(xd, bw, block, lay, R.LayerMask(torch.tensor(dec).cuda())), 1024),
+        R.block_forward_sparse(x, bw, block, lay, R.LayerMask(dec)))
+    # channel masker + channel block on device tensors
+    w1 = rng.standard_normal((16, 1024)) / 32.0
+    w2 = rng.standard_normal((512, 16)) / 4.0
+    cm_np = R.channel_masker_forward(x, (w1, w2), 1)
+    cm_d = R.channel_masker_forward(xd, (w1, w2), 1)
+    assert isinstance(cm_d.coarse, torch.Tensor)
+    dv = (np.maximum(x.mean(axis=(2, 3)) @ w1.T, 0) @ w2.T).reshape(2, -1, 2)
+    safe = np.abs(dv[..., 0] - dv[..., 1]) > 1e-4 * np.abs(dv).sum(-1)
+    assert np.array_equal(cm_d.coarse.cpu().numpy()[safe], cm_np.coarse[safe])
+    ccfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=1)
+    np.testing.assert_array_equal(D.from_device_nhwc(R.block_forward_sparse(xd, bw, block, ccfg, cm_np), 1024),
+                                  R.block_forward_sparse(x, bw, block, ccfg, cm_np))
+    from paper_2308_15949_b200.errors import ShapeMismatch
+    with pytest.raises(ShapeMismatch):
+        R.block_forward_sparse(xd[..., :512], bw, block, cfg, m_d)
