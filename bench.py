@@ -833,7 +833,8 @@ def calibrate(torch, args, net, ws, rank):
         net.calibrate(cal)
         biases = net.masker_biases()
         src = f"live on {args.calib_images} held-out images"
-    t = torch.tensor([float(b) for b in biases], dtype=torch.float64, device="cuda")
+    coll = "cpu" if os.environ.get("LAUD_BENCH_SHARE_GPU") == "1" else "cuda"
+    t = torch.tensor([float(b) for b in biases], dtype=torch.float64, device=coll)
     if ws > 1:
         torch.distributed.broadcast(t, 0)
     net.set_masker_biases(t.tolist())
@@ -843,10 +844,20 @@ def calibrate(torch, args, net, ws, rank):
 def run_gpu(args):
     import torch
     ws, rank, local = dist_env()
+    # LAUD_BENCH_SHARE_GPU=1 (smoke test of the N>1 path on a 1-GPU box): ranks
+    # share the visible GPUs and the checking collectives run on gloo/CPU.  Its
+    # times measure contention, not scaling.
+    share = os.environ.get("LAUD_BENCH_SHARE_GPU") == "1"
+    coll = "cpu" if share else "cuda"
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dev = local % torch.cuda.device_count() if share else local
+        torch.cuda.set_device(dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        local = dev
     else:
         torch.cuda.set_device(0)
     from paper_2308_15949_b200 import _lib
@@ -887,7 +898,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    per_rank_ms = [v[0] for v in gather_scalars([tot_ms], "cuda")]
+    per_rank_ms = [v[0] for v in gather_scalars([tot_ms], coll)]
     tot_ms = max(per_rank_ms)
     ms_step = tot_ms / args.steps
     value = g * args.steps / (tot_ms * 1e-3)
@@ -903,7 +914,7 @@ def run_gpu(args):
     if ws > 1:
         torch.distributed.barrier()
     e_tot = runner.run([host_img] * args.steps, host_out, before_step=flush.zero_)
-    e_tot = max(v[0] for v in gather_scalars([e_tot], "cuda"))
+    e_tot = max(v[0] for v in gather_scalars([e_tot], coll))
     e2e = {"value": g * args.steps / (e_tot * 1e-3), "unit": "images/s",
            "h2d_bytes_per_step": int(host_img.numel()) * ws, "d2h_bytes_per_step": int(nb * n_cls * 4) * ws,
            "path": "network.PipelinedRunner (public API): per step a pinned uint8 upload (copy stream, "
@@ -914,15 +925,15 @@ def run_gpu(args):
     # ---- checking (outside timing): NCCL gather of logits vs single-GPU forwards; per-rank P
     graph.replay()
     torch.cuda.synchronize()
-    local_logits = logits[:, :1000].float().clone()
+    local_logits = logits[:, :1000].float().clone().to(coll)
 
     def recompute(a, b):
         out = net.forward(torch.from_numpy(image_range(a, b)).cuda())[:, :1000].float().clone()
         torch.cuda.synchronize()
-        return out
+        return out.to(coll)
 
     logits_check = check_shards(local_logits, g, ws, rank, recompute)
-    per_rank = gather_scalars([p_local, r_local, nb], "cuda")
+    per_rank = gather_scalars([p_local, r_local, nb], coll)
 
     extra = {}
     recs = profile_launches(torch, net, images)
@@ -982,6 +993,8 @@ def run_gpu(args):
             "gpu_launches": int(launches_per_step * args.steps), "launches_per_step": int(launches_per_step),
             "clocks": clk.summary(),
         }
+        if share:
+            line["smoke_shared_gpu"] = "LAUD_BENCH_SHARE_GPU=1: ranks share one GPU; times are contention, not scaling"
         line.update(extra)
         print(json.dumps(line), flush=True)
     if ws > 1:

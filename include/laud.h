@@ -258,6 +258,12 @@ int laud_stem_im2col(const uint8_t* img, int n, int h, int w, int k, int stride,
                      const float* mean, const float* inv_std, void* cols, int cols_ld,
                      void* stream);
 int laud_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, void* stream);
+/* Fused ResNet stem: uint8 NHWC 224x224x3 images -> (normalise, 7x7/2 conv,
+ * + bias, ReLU, 3x3/2 max-pool) -> bf16 NHWC [n][56][56][64], one kernel (no
+ * im2col in HBM).  weight: bf16 [64][256], K index ky*32 + kx*4 + c (kx < 7,
+ * c < 3; other entries zero); bias fp32 [64]. */
+int laud_stem_pool(const uint8_t* img, int n, int h, int w, const float* mean, const float* inv_std,
+                   const void* weight, const float* bias, void* out, void* stream);
 int laud_global_avgpool(const void* x, int n, int hw, int c, void* y, void* stream);
 
 #ifdef __cplusplus

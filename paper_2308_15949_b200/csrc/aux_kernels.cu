@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(256) se_pool_kernel(const __nv_bfloat16* __res
   if (tid == 0) rr[n] = make_int2(r0, r1);
   const int cpp = c >> 3;
   const int groups = cpp <= (int)blockDim.x ? (int)blockDim.x / cpp : 1;
-  if (r1 > r0 && (tid < groups * cpp || cpp > (int)blockDim.x)) {
+  // deterministic: per-(row group, channel) partials, summed in group order
+  // (no float atomics: the pooled mean feeds a gate, results must not vary)
+  float* part = mean + c;  // [groups][c]
+  if (tid < groups * cpp || cpp > (int)blockDim.x) {
     for (int cc = tid % cpp; cc < cpp; cc += (cpp > (int)blockDim.x ? blockDim.x : cpp)) {
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const int ch = cc << 3;
@@ -211,12 +214,21 @@ __global__ void __launch_bounds__(256) se_pool_kernel(const __nv_bfloat16* __res
         f = unpack_bf16x2(v.z); acc[4] += f.x; acc[5] += f.y;
         f = unpack_bf16x2(v.w); acc[6] += f.x; acc[7] += f.y;
       }
+      float* dst = cpp > (int)blockDim.x ? mean : part + (size_t)(tid / cpp) * c;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) atomicAdd(&mean[ch + e], acc[e]);
+      for (int e = 0; e < 8; ++e) dst[ch + e] = acc[e];
       if (cpp <= (int)blockDim.x) break;
     }
   }
   __syncthreads();
+  if (cpp <= (int)blockDim.x) {
+    for (int i = tid; i < c; i += blockDim.x) {
+      float sum = 0.f;
+      for (int g = 0; g < groups; ++g) sum += part[(size_t)g * c + i];
+      mean[i] = sum;
+    }
+    __syncthreads();
+  }
   const float inv = r1 > r0 ? 1.f / (float)(r1 - r0) : 0.f;
   for (int i = tid; i < c; i += blockDim.x) means[(size_t)n * c + i] = mean[i] * inv;
 }
@@ -309,7 +321,8 @@ cudaError_t launch_se(void* h2, int n, int c, const int* list, const int* count,
   float* means = reinterpret_cast<float*>(scratch);
   float* gates = means + (size_t)n * c;
   int2* rr = reinterpret_cast<int2*>(gates + (((size_t)n * c + 3) & ~(size_t)3));
-  launch_k(se_pool_kernel, dim3(n), dim3(256), (size_t)c * sizeof(float), s,
+  const int se_groups = (c / 8) <= 256 ? 256 / (c / 8) : 1;
+  launch_k(se_pool_kernel, dim3(n), dim3(256), (size_t)c * (1 + se_groups) * sizeof(float), s,
            reinterpret_cast<const __nv_bfloat16*>(h2), c, list, count, cells_per_img, rows_per_cell,
            rows_per_img, means, rr);
   const size_t smem = (size_t)SE_SPB * (c + hs) * sizeof(float);
@@ -350,18 +363,40 @@ __global__ void __launch_bounds__(256) se_pool_ch_kernel(const __nv_bfloat16* __
   __syncthreads();
   const int cpr = (kc + 7) >> 3;
   const __nv_bfloat16* base = h2 + (size_t)n * sr * c;
-  for (int k = tid; k < hw * cpr; k += blockDim.x) {
-    const int r = k / cpr, ch = (k - r * cpr) << 3;
-    const uint4 v = *reinterpret_cast<const uint4*>(base + (size_t)r * c + ch);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  // deterministic: thread (row group, chunk) sums its rows in order; chunk
+  // partials of the groups are then added in group order (no float atomics)
+  const int cpc = (c + 7) >> 3;
+  const int groups = cpc <= (int)blockDim.x ? (int)blockDim.x / cpc : 1;
+  float* part = acc + c;  // [groups][c]
+  for (int cc = tid % cpc; cc < cpr && (tid < groups * cpc || cpc > (int)blockDim.x);
+       cc += (cpc > (int)blockDim.x ? blockDim.x : cpc)) {
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int ch = cc << 3;
+    for (int r = (cpc > (int)blockDim.x ? 0 : tid / cpc); r < hw; r += groups) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + (size_t)r * c + ch);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = unpack_bf16x2(w[e]);
-      if (ch + 2 * e < kc) atomicAdd(&acc[ch + 2 * e], f.x);
-      if (ch + 2 * e + 1 < kc) atomicAdd(&acc[ch + 2 * e + 1], f.y);
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = unpack_bf16x2(w[e]);
+        a[2 * e] += f.x;
+        a[2 * e + 1] += f.y;
+      }
     }
+    float* dst = cpc > (int)blockDim.x ? acc : part + (size_t)(tid / cpc) * c;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (ch + e < kc) dst[ch + e] = a[e];
+    if (cpc <= (int)blockDim.x) break;
   }
   __syncthreads();
+  if (cpc <= (int)blockDim.x) {
+    for (int i = tid; i < kc; i += blockDim.x) {
+      float sum = 0.f;
+      for (int g = 0; g < groups; ++g) sum += part[(size_t)g * c + i];
+      acc[i] = sum;
+    }
+    __syncthreads();
+  }
   const float inv = 1.f / (float)hw;
   for (int j = tid; j < kc; j += blockDim.x) means[(size_t)n * c + __ldg(sel + (size_t)n * c + j)] = acc[j] * inv;
 }
@@ -404,7 +439,8 @@ cudaError_t launch_se_channel(void* h2, int n, int c, int hw, int sr, const int*
                               void* scratch, cudaStream_t s) {
   float* means = reinterpret_cast<float*>(scratch);
   float* gates = means + (size_t)n * c;
-  launch_k(se_pool_ch_kernel, dim3(n), dim3(256), (size_t)c * sizeof(float), s,
+  const int ch_groups = ((c + 7) / 8) <= 256 ? 256 / ((c + 7) / 8) : 1;
+  launch_k(se_pool_ch_kernel, dim3(n), dim3(256), (size_t)c * (1 + ch_groups) * sizeof(float), s,
            reinterpret_cast<const __nv_bfloat16*>(h2), c, hw, sr, sel, count, means);
   const size_t smem = (size_t)SE_SPB * (c + hs) * sizeof(float);
   if (smem > 48 * 1024) {

@@ -47,6 +47,8 @@ cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, i
                                cudaStream_t s);
 cudaError_t launch_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, cudaStream_t s);
 cudaError_t launch_gap(const void* x, int n, int hw, int c, void* y, cudaStream_t s);
+cudaError_t launch_stem_pool(const uint8_t* img, int n, const float* mean, const float* inv_std,
+                             const void* wpk, const float* bias, void* out, int num_sms, cudaStream_t s);
 cudaError_t launch_se(void* h2, int n, int c, const int* list, const int* count, int cells_per_img,
                       int rows_per_cell, int rows_per_img, const float* w1, const float* b1, int hs,
                       const float* w2, const float* b2, void* scratch, cudaStream_t s);
@@ -598,7 +600,7 @@ int laud_channel_masker(const void* x, int x_f32, int ld, int n, int hw, int c, 
                         const float* bias, void* stream) {
   if (c % 8 || ld % 8 || ld < c) return fail(LAUD_ERR_SHAPE, "channels must be multiples of 8");
   if (d < 1 || g < 1 || cm != d * g || cm > cm_p) return fail(LAUD_ERR_GRANULARITY, "bad D/G");
-  if ((size_t)(c + hidden + d) * 4 > 48 * 1024) return fail(LAUD_ERR_SHAPE, "masker too wide");
+  if ((size_t)(c + hidden + d + 8 * 1024) * 4 > 100 * 1024) return fail(LAUD_ERR_SHAPE, "masker too wide");
   ProfScope ps(1, (cudaStream_t)stream);
   return cuda_check(launch_channel_masker(x, x_f32, ld, n, hw, c, w1, hidden, w2, d, g, cm, cm_p,
                                           coarse, dvals, expanded, sel, count, bias,
@@ -1144,6 +1146,18 @@ int laud_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, void* st
   if (c % 8) return fail(LAUD_ERR_SHAPE, "channels must be a multiple of 8");
   ProfScope ps(3, (cudaStream_t)stream);
   return cuda_check(launch_maxpool3s2(x, n, h, w, c, y, (cudaStream_t)stream), "maxpool", 1);
+}
+
+int laud_stem_pool(const uint8_t* img, int n, int h, int w, const float* mean, const float* inv_std,
+                   const void* weight, const float* bias, void* out, void* stream) {
+  if (!img || !mean || !inv_std || !weight || !bias || !out) return fail(LAUD_ERR_ARG, "null pointer in stem args");
+  if (h != 224 || w != 224) return fail(LAUD_ERR_SHAPE, "fused stem: 224x224 images (got %dx%d)", h, w);
+  if (n <= 0) return LAUD_OK;
+  if ((reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(LAUD_ERR_ARG, "fused stem: 16-byte aligned weights and output");
+  ProfScope ps(3, (cudaStream_t)stream);
+  return cuda_check(launch_stem_pool(img, n, mean, inv_std, weight, bias, out, num_sms(), (cudaStream_t)stream),
+                    "fused stem", 1);
 }
 
 int laud_global_avgpool(const void* x, int n, int hw, int c, void* y, void* stream) {

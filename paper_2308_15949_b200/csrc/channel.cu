@@ -53,39 +53,46 @@ __global__ void __launch_bounds__(CM_THREADS) channel_masker_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < c; i += blockDim.x) gap[i] = 0.f;
   __syncthreads();
-  // global average pool: thread owns one 8-channel chunk, strides over pixels
+  // global average pool: thread (row group, 8-channel chunk) sums its pixels in
+  // order; the groups' partials are then added in group order — deterministic
+  // (no float atomics), so decisions never vary between identical runs
   const int cpp = c >> 3;
   const T* xs = x + (size_t)n * hw * ld;
-  if ((int)blockDim.x % cpp == 0) {  // fixed chunk per thread, register accumulation
-    const int groups = blockDim.x / cpp;
-    const int chunk = tid % cpp, grp = tid / cpp;
-    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int px = grp;
-    // four independent 16-byte loads in flight per thread (the pass is HBM-bound)
-    for (; px + 3 * groups < hw; px += 4 * groups) {
-      float v0[8], v1[8], v2[8], v3[8];
-      load8<T>(xs + (size_t)px * ld + chunk * 8, v0);
-      load8<T>(xs + (size_t)(px + groups) * ld + chunk * 8, v1);
-      load8<T>(xs + (size_t)(px + 2 * groups) * ld + chunk * 8, v2);
-      load8<T>(xs + (size_t)(px + 3 * groups) * ld + chunk * 8, v3);
+  const int groups = cpp <= (int)blockDim.x ? (int)blockDim.x / cpp : 1;
+  float* part = dl + d;  // [groups][c] (launch reserves 8 * blockDim floats)
+  if (tid < groups * cpp || cpp > (int)blockDim.x) {
+    for (int chunk = tid % cpp; chunk < cpp; chunk += (cpp > (int)blockDim.x ? blockDim.x : cpp)) {
+      const int grp = cpp > (int)blockDim.x ? 0 : tid / cpp;
+      float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int px = grp;
+      // four independent 16-byte loads in flight per thread (the pass is HBM-bound)
+      for (; px + 3 * groups < hw; px += 4 * groups) {
+        float v0[8], v1[8], v2[8], v3[8];
+        load8<T>(xs + (size_t)px * ld + chunk * 8, v0);
+        load8<T>(xs + (size_t)(px + groups) * ld + chunk * 8, v1);
+        load8<T>(xs + (size_t)(px + 2 * groups) * ld + chunk * 8, v2);
+        load8<T>(xs + (size_t)(px + 3 * groups) * ld + chunk * 8, v3);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] += (v0[e] + v1[e]) + (v2[e] + v3[e]);
+        for (int e = 0; e < 8; ++e) a[e] += (v0[e] + v1[e]) + (v2[e] + v3[e]);
+      }
+      for (; px < hw; px += groups) {
+        float v[8];
+        load8<T>(xs + (size_t)px * ld + chunk * 8, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] += v[e];
+      }
+      float* dst = cpp > (int)blockDim.x ? gap : part + (size_t)grp * c;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dst[chunk * 8 + e] = a[e];
+      if (cpp <= (int)blockDim.x) break;
     }
-    for (; px < hw; px += groups) {
-      float v[8];
-      load8<T>(xs + (size_t)px * ld + chunk * 8, v);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] += v[e];
-    }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) atomicAdd(&gap[chunk * 8 + e], a[e]);
-  } else {
-    for (int q = tid; q < hw * cpp; q += blockDim.x) {
-      const int px = q / cpp, chunk = q - (q / cpp) * cpp;
-      float v[8];
-      load8<T>(xs + (size_t)px * ld + chunk * 8, v);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) atomicAdd(&gap[chunk * 8 + e], v[e]);
+  }
+  __syncthreads();
+  if (cpp <= (int)blockDim.x) {
+    for (int i = tid; i < c; i += blockDim.x) {
+      float sum = 0.f;
+      for (int g2 = 0; g2 < groups; ++g2) sum += part[(size_t)g2 * c + i];
+      gap[i] = sum;
     }
   }
   __syncthreads();
@@ -213,7 +220,14 @@ cudaError_t launch_channel_masker(const void* x, int x_f32, int ld, int n, int h
                                   const float* w1, int hd, const float* w2, int d, int g, int cm,
                                   int cm_p, uint8_t* coarse, float* dvals, uint8_t* expanded,
                                   int* sel, int* count, const float* bias, cudaStream_t s) {
-  const size_t smem = (size_t)(c + hd + d) * sizeof(float);
+  const size_t smem = (size_t)(c + hd + d + 8 * CM_THREADS) * sizeof(float);  // + GAP partials
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(channel_masker_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(channel_masker_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         100 * 1024);
+    configured = true;
+  }
   if (x_f32)
     launch_k(channel_masker_kernel<float>, dim3(n), dim3(CM_THREADS), smem, s, reinterpret_cast<const float*>(x), ld, hw, c,
                                                       w1, hd, w2, d, g, cm, cm_p, coarse, dvals,

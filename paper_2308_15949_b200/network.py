@@ -122,6 +122,14 @@ class LaudNetwork:
         wcol = wcol.reshape(st.out_channels, 1, 1, self.stem_cols)
         self.stem_w = D.pack_weight(wcol.transpose(0, 3, 1, 2), self.stem_cols, device)
         self.stem_c = D.pad8(st.out_channels)
+        # fused 7x7/2 stem + max-pool (laud_stem_pool): weights [64][ky*32 + kx*4 + c]
+        self.stem_fused = (st.kernel == 7 and st.stride == 2 and net.stem_pool and st.out_channels == 64
+                           and os.environ.get("LAUD_STEM_FUSED", "1") == "1")
+        if self.stem_fused:
+            wf = np.zeros((64, 7, 8, 4))
+            wf[:, :, :7, :3] = ws.transpose(0, 2, 3, 1)  # (co, ky, kx, c)
+            wf = np.concatenate([wf.reshape(64, 224), np.zeros((64, 32))], axis=1)
+            self.stem_wf = torch.from_numpy(wf).to(device=device, dtype=torch.bfloat16).contiguous()
         self.stem_bias = D.fvec(params["stem_b"], st.out_channels, 0.0, device)
         self.mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32, device=device)
         self.inv_std = torch.tensor([1.0 / s for s in IMAGENET_STD], dtype=torch.float32, device=device)
@@ -190,6 +198,11 @@ class LaudNetwork:
         pad = k // 2
         ho, wo = (h + 2 * pad - k) // st + 1, (w + 2 * pad - k) // st + 1
         sh = D.stream_handle(stream)
+        if self.stem_fused and h == 224 and w == 224:
+            pool = self._buf("pool", (n, 56, 56, self.stem_c))
+            _lib.call("laud_stem_pool", D.ptr(images), n, h, w, D.ptr(self.mean), D.ptr(self.inv_std),
+                      D.ptr(self.stem_wf), D.ptr(self.stem_bias), D.ptr(pool), sh)
+            return self._blocks_and_head(pool, n, stream, record)
         cols = self._buf("cols", (n * ho * wo, self.stem_cols))
         _lib.call("laud_stem_im2col", D.ptr(images), n, h, w, k, st, pad, D.ptr(self.mean),
                   D.ptr(self.inv_std), D.ptr(cols), self.stem_cols, sh)
@@ -204,6 +217,10 @@ class LaudNetwork:
             pool = self._buf("pool", (n, ph, pw, self.stem_c))
             _lib.call("laud_maxpool3s2", D.ptr(stem_out), n, ho, wo, self.stem_c, D.ptr(pool), sh)
             x = pool
+        return self._blocks_and_head(x, n, stream, record)
+
+    def _blocks_and_head(self, x, n, stream, record):
+        sh = D.stream_handle(stream)
         ping = 0
         prev_coarse = None
         for bi, slot in enumerate(self.slots):

@@ -251,3 +251,48 @@ def test_stem_im2col_matches_numpy(n, h, w, k):
             ref[..., ky, kx * 3:kx * 3 + 3] = padded[:, ky:ky + st * ho:st, kx:kx + st * wo:st]
     ref_bf = torch.from_numpy(ref.reshape(n * ho * wo, k * seg)).bfloat16()
     assert torch.equal(cols.cpu(), ref_bf)
+
+
+@pytest.mark.parametrize("n", [1, 3, 40])
+def test_fused_stem_pool_matches_unfused(n):
+    """laud_stem_pool (7x7/2 conv from uint8 images in one kernel, im2col-free
+    tcgen05 MMAs on overlapping core matrices, bias + ReLU + 3x3/2 max-pool) vs
+    the im2col + GEMM + max-pool path and a torch fp32 reference."""
+    import ctypes as C
+    from paper_2308_15949_b200 import _lib
+    from paper_2308_15949_b200.network import IMAGENET_MEAN, IMAGENET_STD
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(n)
+    img = torch.randint(0, 256, (n, 224, 224, 3), dtype=torch.uint8, generator=g).cuda()
+    w = (torch.randn(64, 3, 7, 7, generator=g) * 0.1).to(torch.bfloat16).float()
+    b = (torch.randn(64, generator=g) * 0.1).cuda()
+    mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32).cuda()
+    inv = torch.tensor([1.0 / s for s in IMAGENET_STD], dtype=torch.float32).cuda()
+    wf = torch.zeros(64, 7, 8, 4)
+    wf[:, :, :7, :3] = w.permute(0, 2, 3, 1)
+    wf = torch.cat([wf.reshape(64, 224), torch.zeros(64, 32)], 1).to(torch.bfloat16).cuda().contiguous()
+    out = torch.empty(n, 56, 56, 64, dtype=torch.bfloat16, device="cuda")
+    sh = D.stream_handle()
+    _lib.call("laud_stem_pool", D.ptr(img), n, 224, 224, D.ptr(mean), D.ptr(inv), D.ptr(wf), D.ptr(b), D.ptr(out), sh)
+    # unfused: im2col (K = 7 * 24) + engine GEMM + max-pool
+    cols_ld = 7 * 24
+    cols = torch.empty(n * 112 * 112, cols_ld, dtype=torch.bfloat16, device="cuda")
+    _lib.call("laud_stem_im2col", D.ptr(img), n, 224, 224, 7, 2, 3, D.ptr(mean), D.ptr(inv), D.ptr(cols), cols_ld, sh)
+    wc = torch.zeros(64, 7, 24)
+    wc[:, :, :21] = w.permute(0, 2, 3, 1).reshape(64, 7, 21)
+    wcol = D.pack_weight(wc.reshape(64, cols_ld, 1, 1), cols_ld)
+    conv = torch.empty(n, 112, 112, 64, dtype=torch.bfloat16, device="cuda")
+    CH.conv(act=cols, in_hw=(n * 112 * 112, 1), in_c=cols_ld, in_ld=cols_ld, weight=wcol, n_out=64, out=conv,
+            out_ld=64, out_hw=(112, 112), batch=n, a_compact=1, bias=b, relu=1)
+    ref2 = torch.empty_like(out)
+    _lib.call("laud_maxpool3s2", D.ptr(conv), n, 112, 112, 64, D.ptr(ref2), sh)
+    torch.cuda.synchronize()
+    diff = (out.float() - ref2.float()).abs()
+    assert diff.max().item() <= 0.05 * ref2.float().abs().max().item()
+    assert (diff > 0).float().mean().item() < 0.02  # accumulation-order rounding only
+    # torch fp32 reference of the same bf16-rounded inputs
+    x = ((img.float() - mean) * inv).to(torch.bfloat16).float().permute(0, 3, 1, 2)
+    y = torch.relu(torch.nn.functional.conv2d(x, w.cuda(), stride=2, padding=3) + b.view(1, -1, 1, 1))
+    y = torch.nn.functional.max_pool2d(y.to(torch.bfloat16).float(), 3, 2, 1).permute(0, 2, 3, 1)
+    err = (out.float() - y).norm() / y.norm()
+    assert err < 4e-3, float(err)

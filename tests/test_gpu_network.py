@@ -94,3 +94,24 @@ def test_pipelined_runner_matches_forward():
     assert ms > 0
     for i in range(3):
         assert torch.equal(out[i, :, :1000], ref[i])
+
+
+@pytest.mark.parametrize("arch,paradigm,plan", [("resnet101", "spatial", "4-2-2-1"),
+                                                ("regnety-1.6gf", "spatial", "4-4-2-1"),
+                                                ("resnet50", "channel", "2-2-2-2"),
+                                                ("regnety-400mf", "channel", "1-1-1-1")])
+def test_network_is_bitwise_deterministic(arch, paradigm, plan):
+    """No float atomics on any decision or pooling path (conv1-fused masker,
+    channel-masker GAP, SE pooling): two forwards of the same images give
+    identical logits, and so do two different batch compositions per image."""
+    import torch
+    from paper_2308_15949_b200.network import LaudNetwork, random_images
+    net = LaudNetwork(arch, paradigm, plan, 0.5, seed=0)
+    img = random_images(6, seed=9)
+    net.calibrate(img)
+    a = net.forward(img)[:, :1000].clone()
+    b = net.forward(img)[:, :1000].clone()
+    c = torch.cat([net.forward(img[:4])[:, :1000].clone(), net.forward(img[4:])[:, :1000].clone()])
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert torch.equal(a, c)
