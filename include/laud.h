@@ -134,6 +134,17 @@ typedef struct laud_conv_args {
   /* fp32 mode: act / weight / resid / out are fp32 (weight in the same packed
    * layout), computed with fp32 FFMA (the 1e-5 numerics path). */
   int fp32;
+  /* per-sample weights gathered in the kernel (channel skipping at large
+   * batch, needs sample_rows + chan_count): b_gather = 1 -> B rows are weight
+   * rows b_index[n][j] for output columns j < k_n (weight packed as usual);
+   * b_gather = 2 -> weight is
+   * the TRANSPOSED 1x1 kernel [K rows][n_out] and the tile's K rows are
+   * b_index[n][k], k < k_n (compact A of k_n channels).  b_rows: rows of the
+   * gathered weight tensor.  0 = packed / batched B as above. */
+  int b_gather;
+  const int* b_index;
+  int b_index_ld;
+  int b_rows;
 } laud_conv_args;
 
 int laud_conv(const laud_conv_args* a, void* stream);
@@ -236,6 +247,11 @@ typedef struct laud_block_args {
    * dense-masked schedule uses.  NULL = the reference behaviour
    * (LAUD_ERR_UNSUPPORTED for groups != 1). */
   const void* w2_dense;
+  /* channel paradigm at batch >= 8: conv3's kernel transposed, bf16
+   * [c_mid][c_out] (K rows, c_out contiguous), for the in-kernel K gather
+   * W3[:, sel] (conv2's N gather W2[sel] uses w2).  NULL = dense-masked
+   * schedule at large batch. */
+  const void* w3t;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

@@ -25,8 +25,9 @@ def conv(*, act, in_hw, in_c, in_ld, weight, n_out, out, out_ld, out_hw, batch, 
          pad=0, row_mode=ROWS_DENSE, rows_max=None, lst=None, count=None, patch=(1, 1),
          cells=(1, 1), a_compact=0, scale=None, bias=None, relu=0, out_mode=OUT_PIXEL, out_f32=0,
          resid=None, resid_ld=0, relu_inactive=None, ymask_coarse=None, ymask_channel=None,
-         misplace_first=0, groups=1, fp32=0, stream=None):
-    """One call of the implicit-GEMM engine (``laud_conv``)."""
+         misplace_first=0, groups=1, fp32=0, stream=None, **extra):
+    """One call of the implicit-GEMM engine (``laud_conv``); ``extra``: further
+    ``laud_conv_args`` fields (per-sample / gathered-weight modes), pointers as tensors."""
     a = _lib.ConvArgs(
         row_mode=row_mode, list=D.ptr(lst), count=D.ptr(count),
         rows_max=rows_max if rows_max is not None else batch * out_hw[0] * out_hw[1],
@@ -38,6 +39,8 @@ def conv(*, act, in_hw, in_c, in_ld, weight, n_out, out, out_ld, out_hw, batch, 
         resid_ld=resid_ld, relu_inactive_coarse=D.ptr(relu_inactive),
         ymask_coarse=D.ptr(ymask_coarse), ymask_channel=D.ptr(ymask_channel),
         misplace_first=misplace_first, groups=groups, fp32=fp32)
+    for k, v in extra.items():
+        setattr(a, k, D.ptr(v) if isinstance(v, torch.Tensor) else v)
     _lib.check(_lib.lib().laud_conv(C.byref(a), D.stream_handle(stream)))
 
 

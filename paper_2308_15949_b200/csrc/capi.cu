@@ -354,6 +354,19 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
   p.b_batched = a->b_batched;
   p.col_index = a->col_index;
   p.col_index_ld = a->col_index_ld;
+  p.b_gather = a->b_gather;
+  p.b_index = a->b_index;
+  p.b_index_ld = a->b_index_ld;
+  p.b_rows = a->b_rows;
+  if (a->b_gather) {
+    if (a->b_gather != B_GATHER_N && a->b_gather != B_GATHER_K) return fail(LAUD_ERR_ARG, "b_gather must be 0, 1 or 2");
+    if (!a->b_index || !a->chan_count || a->sample_rows <= 0 || a->b_batched || a->groups > 1 || a->fp32 ||
+        a->b_rows <= 0)
+      return fail(LAUD_ERR_ARG, "gathered weights need b_index, b_rows, chan_count and sample_rows (no groups / fp32)");
+    if (a->b_gather == B_GATHER_K && (a->ksize != 1 || !a->k_dyn || !a->a_compact))
+      return fail(LAUD_ERR_ARG, "K-gathered weights: 1x1 conv over compact rows with k_dyn");
+    if (a->b_gather == B_GATHER_N && !a->n_dyn) return fail(LAUD_ERR_ARG, "N-gathered weights need n_dyn");
+  }
   if (a->sample_rows % 128) return fail(LAUD_ERR_ARG, "sample_rows must be a multiple of 128");
   if ((a->n_dyn || a->k_dyn) && !a->chan_count) return fail(LAUD_ERR_ARG, "chan_count missing");
   p.misplace_first = a->misplace_first;
@@ -408,8 +421,11 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
       return cuda_check(launch_patch_conv(ma, mb, p, s, hbn, num_sms(), st), "patch conv launch", 1);
     }
   }
-  // grouped: narrow tiles keep the block-diagonal K window short
-  const int bn = p.groups > 1 ? 64 : pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
+  // grouped: narrow tiles keep the block-diagonal K window short; gathered
+  // weights: 128-wide N tiles (the per-sample kept width at r <= 0.5)
+  const int bn = p.groups > 1 ? 64
+                 : a->b_gather ? (a->n_out <= 64 ? 64 : 128)
+                               : pick_bn(a->n_out, a->ksize * a->ksize * round_up(a->in_c, 64), a->rows_max);
   const int kw = a->ksize * a->ksize * p.kpad;
   int rc;
   // A operand: [a_rows][in_c] with row stride in_ld, gathered 4 rows at a time
@@ -462,7 +478,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     return e ? atoi(e) : 1;  // short-K pairs (2) measured slower: opt-in
   }();
   const long long pair_tiles = (long long)((a->rows_max + 255) / 256) * ((a->n_out + bn - 1) / bn);
-  const bool pair_ok = pair_env && bn == 256 && p.a_tile && !a->sample_rows && !a->chan_count &&
+  const bool pair_ok = pair_env && bn == 256 && p.a_tile && !a->sample_rows && !a->chan_count && !a->b_gather &&
                        !a->b_batched && p.groups == 1 && pair_tiles >= num_sms() / 2;
   const int pair = (!pair_ok || ad) ? 0 : (kw >= 1024 ? 1 : (kw <= 512 && (pair_env & 2) ? 2 : 0));
   if (ad) {  // fused masker readers need single-CTA tiles with contiguous (TMA box) A rows
@@ -471,8 +487,16 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     p.adot_out = ad->out;
   }
   CUtensorMap m;
-  if ((rc = tensor_map_2d(a->weight, a->n_out, kw, kw, pair ? bn / 2 : bn, &m, a->b_batched ? a->batch : 0)))
+  memset(&m, 0, sizeof(m));
+  if (a->b_gather) {  // gathered rows are read with cp.async (no tensor map)
+    if (a->b_gather == B_GATHER_K && a->n_out % 64)
+      return fail(LAUD_ERR_SHAPE, "K-gathered weights: n_out must be a multiple of 64");
+    if (reinterpret_cast<uintptr_t>(a->weight) % 16) return fail(LAUD_ERR_ARG, "gathered weights: 16-byte alignment");
+    p.weight_g = a->weight;
+    p.b_ld = a->b_gather == B_GATHER_N ? kw : a->n_out;
+  } else if ((rc = tensor_map_2d(a->weight, a->n_out, kw, kw, pair ? bn / 2 : bn, &m, a->b_batched ? a->batch : 0))) {
     return rc;
+  }
   ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
   if (ps.on) {
     ps.rec.rows_per_count = a->row_mode == ROWS_PATCH ? (long long)p.patch_h * p.patch_w : 1;
@@ -673,6 +697,127 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
                          "skip copy", 0)))
       return rc;
   }
+  static const int dense_min = [] {
+    const char* e = getenv("LAUD_CH_DENSE_MIN");
+    return e ? atoi(e) : 8;
+  }();
+  // EXT schedule (opt-in, LAUD_CH_GATHER=1): per-sample weights gathered
+  // inside the conv kernels instead of a packing pass.  conv1 stays
+  // dense-masked (h1 full width, zero on the dropped channels); conv2's tiles
+  // belong to one sample and gather their B rows W2[sel] (N = k_n, K = the
+  // full masked h1 -> r F2); h2 is compact (k_n columns, sel order); conv3
+  // gathers the K rows of W3^T (MN-major B: K = k_n -> r F3) and adds into
+  // the residual.  Correct (tests) but measured slower than the dense-masked
+  // schedule at batch 256 (R101 stage-3 conv2: 381 us gathered vs 83 us
+  // dense, tools/engine_probe.py chconv2_s3): the per-(tile, k-block) weight
+  // gather (16 KiB from scattered rows, TMA gather4 or cp.async) is far below
+  // the MMA rate, and a sample's 196 rows cannot amortise it.
+  // Read per call so tests can switch it.
+  const char* ge = getenv("LAUD_CH_GATHER");
+  const int gather_env = ge ? atoi(ge) : 0;
+  const int hw2 = ho * wo, sr2g = (hw2 + 127) / 128 * 128;
+  if (gather_env && !a->fp32 && a->groups == 1 && a->w3t && dense_min > 0 && n >= dense_min &&
+      sr2g * 100 <= hw2 * 135 && a->c_out % 64 == 0) {
+    laud_conv_args c1;
+    memset(&c1, 0, sizeof(c1));
+    c1.row_mode = ROWS_DENSE;
+    c1.rows_max = n * a->h_in * a->w_in;
+    c1.batch = n;
+    c1.out_h = a->h_in;
+    c1.out_w = a->w_in;
+    c1.patch_h = c1.patch_w = c1.cells_h = c1.cells_w = 1;
+    c1.act = a->x;
+    c1.in_h = a->h_in;
+    c1.in_w = a->w_in;
+    c1.in_c = a->c_in;
+    c1.in_ld = a->x_ld;
+    c1.ksize = 1;
+    c1.stride = 1;
+    c1.weight = a->w1;
+    c1.n_out = cmp;
+    c1.scale = a->s1;
+    c1.bias = a->b1;
+    c1.relu = a->relu1;
+    c1.ymask_channel = a->ch_expanded;
+    c1.out_mode = OUT_PIXEL;
+    c1.out = a->h1;
+    c1.out_ld = cmp;
+    if ((rc = run_conv(&c1, st))) return rc;
+    laud_conv_args c2;
+    memset(&c2, 0, sizeof(c2));
+    c2.row_mode = ROWS_DENSE;
+    c2.sample_rows = sr2g;
+    c2.rows_max = n * sr2g;
+    c2.batch = n;
+    c2.out_h = ho;
+    c2.out_w = wo;
+    c2.patch_h = c2.patch_w = c2.cells_h = c2.cells_w = 1;
+    c2.act = a->h1;
+    c2.in_h = a->h_in;
+    c2.in_w = a->w_in;
+    c2.in_c = cmp;
+    c2.in_ld = cmp;
+    c2.ksize = 3;
+    c2.stride = a->stride;
+    c2.pad = 1;
+    c2.weight = a->w2;
+    c2.n_out = cmp;
+    c2.chan_count = a->ch_count;
+    c2.n_dyn = 1;
+    c2.col_index = a->ch_sel;
+    c2.col_index_ld = cmp;
+    c2.b_gather = B_GATHER_N;
+    c2.b_index = a->ch_sel;
+    c2.b_index_ld = cmp;
+    c2.b_rows = cmp;
+    c2.scale = a->s2;
+    c2.bias = a->b2;
+    c2.relu = a->relu2;
+    c2.out_mode = OUT_ROW;
+    c2.out = a->h2;
+    c2.out_ld = cmp;
+    if ((rc = run_conv(&c2, st))) return rc;
+    if (a->se_w1) {  // EXT squeeze-excitation over each sample's kept channels (compact h2)
+      if ((rc = cuda_check(launch_se_channel(a->h2, n, cmp, hw2, hw2, a->ch_sel, a->ch_count, a->se_w1,
+                                             a->se_b1, a->se_hidden, a->se_w2, a->se_b2, a->h1, st),
+                           "squeeze-excitation (channel)", 1)))
+        return rc;
+    }
+    laud_conv_args c3;
+    memset(&c3, 0, sizeof(c3));
+    c3.row_mode = ROWS_DENSE;
+    c3.sample_rows = sr2g;
+    c3.rows_max = n * sr2g;
+    c3.batch = n;
+    c3.out_h = ho;
+    c3.out_w = wo;
+    c3.patch_h = c3.patch_w = c3.cells_h = c3.cells_w = 1;
+    c3.act = a->h2;
+    c3.in_h = ho;
+    c3.in_w = wo;
+    c3.in_c = cmp;
+    c3.in_ld = cmp;
+    c3.a_compact = 1;
+    c3.ksize = 1;
+    c3.stride = 1;
+    c3.weight = a->w3t;
+    c3.n_out = a->c_out;
+    c3.chan_count = a->ch_count;
+    c3.k_dyn = 1;
+    c3.b_gather = B_GATHER_K;
+    c3.b_index = a->ch_sel;
+    c3.b_index_ld = cmp;
+    c3.b_rows = cmp;
+    c3.scale = a->s3;
+    c3.bias = a->b3;
+    c3.relu = a->relu_out;
+    c3.out_mode = OUT_PIXEL;
+    c3.out = a->out;
+    c3.out_ld = a->c_out;
+    c3.resid = a->out;
+    c3.resid_ld = a->c_out;
+    return run_conv(&c3, st);
+  }
   // Schedule.  Per-sample dynamic width (below) computes exactly the kept
   // channels but packs W1[sel], W2[sel][:, sel], W3[:, sel] for every sample —
   // at large batch that weight traffic (n * r|W|) dwarfs the activations, so
@@ -680,10 +825,6 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
   // dense-masked schedule of the same algebra (reference.py:336-339): dense
   // convs, h1 and h2 zeroed on the dropped channels in the epilogues, so conv3
   // sums only the kept ones.
-  static const int dense_min = [] {
-    const char* e = getenv("LAUD_CH_DENSE_MIN");
-    return e ? atoi(e) : 8;
-  }();
   if (a->fp32 || (dense_min > 0 && n >= dense_min)) {
     laud_conv_args c1;
     memset(&c1, 0, sizeof(c1));

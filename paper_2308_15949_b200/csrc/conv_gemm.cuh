@@ -145,7 +145,9 @@ struct Smem {
   static constexpr int BAR_OFF = VEC_OFF + VEC_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 2 * NACC;
   static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
-  static constexpr int BYTES = TMEM_SLOT_OFF + 16;
+  static constexpr int BIDX_OFF = TMEM_SLOT_OFF + 16;  // gathered-B row indices of the current tile
+  static constexpr int BIDX_INTS = BN > BK ? BN : BK;
+  static constexpr int BYTES = BIDX_OFF + BIDX_INTS * 4;
   static constexpr int ALLOC = BYTES + 1024;  // manual 1 KiB alignment
   static constexpr uint32_t TMEM_COLS = NACC * BN;
 };
@@ -185,8 +187,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   unsigned long long* const trc = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      // arrivals: A expect_tx (TMA) or 128 cp.async threads, hybrid both halves, + B
-      mbar_init(&full[s], p.a_tma ? 2 : 128 + 1);
+      // arrivals: A expect_tx (TMA) or 128 cp.async threads, + B expect_tx or 32 cp.async lanes
+      mbar_init(&full[s], (p.a_tma ? 1 : 128) + (p.b_gather != B_BOX ? 32 : 1));
       mbar_init(&empty[s], p.adot_out ? 2 : 1);  // + the fused masker readers
     }
     for (int a = 0; a < L::NACC; ++a) {
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == WARP_TMA && lane == 0) {
-    tma_prefetch_desc(&tmap_b);
+    if (p.b_gather == B_BOX) tma_prefetch_desc(&tmap_b);
     if (p.a_tma) tma_prefetch_desc(&tmap_a);
   }
   if (warp == WARP_MMA) {
@@ -456,7 +458,59 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == WARP_TMA) {
     // ------------------------------------------------------------ B producer (TMA)
-    if (lane == 0) {
+    if (p.b_gather != B_BOX) {
+      // per-sample weights gathered in-kernel (channel skipping): the warp's 32
+      // lanes cp.async the tile's 16-byte chunks into the 128B-swizzled stage
+      // (a TMA gather4 per 4 rows measured ~8x slower per byte here); indices
+      // past the sample's k_n zero-fill.  The tile's row indices sit in smem.
+      int* const bidx = reinterpret_cast<int*>(base + L::BIDX_OFF);
+      const __nv_bfloat16* const wsrc = reinterpret_cast<const __nv_bfloat16*>(p.weight_g);
+      uint32_t it = 0;
+      for (int t = t_begin; t < tiles; t += t_step) {
+        const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
+        if (ti.skip) continue;
+        const int* idx = p.b_index + (size_t)ti.sample * p.b_index_ld;
+        const bool gn = p.b_gather == B_GATHER_N;
+        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          if (gn ? kb == 0 : true) {
+            // N gather: the tile's BN rows once per tile; K gather: this k-block's 64 K rows
+            __syncwarp();
+            const int cnt = gn ? BN : BK, off = gn ? ti.n0 : kb * BK;
+            for (int j = lane; j < cnt; j += 32) bidx[j] = off + j < ti.kc ? __ldg(idx + off + j) : -1;
+            __syncwarp();
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t dst = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
+          if (gn) {
+            // K-major [BN rows][64]: row r = weight row bidx[r], 128 B at the k-block's K offset
+            const int cblk = kb / taps, tap = kb - cblk * taps;
+            const int kcoord = tap * p.kpad + cblk * BK;
+#pragma unroll 4
+            for (int i = lane; i < BN * 8; i += 32) {
+              const int r = i >> 3, c = i & 7;
+              const int row = bidx[r];
+              const __nv_bfloat16* src = wsrc + (size_t)(row < 0 ? 0 : row) * p.b_ld + kcoord + c * 8;
+              cp_async_16(dst + r * 128 + ((c ^ (r & 7)) << 4), src, row < 0 ? 0u : 16u);
+            }
+          } else {
+            // MN-major: BN/64 panels of [64 K rows][64 N] (SW128, 8 KiB each); K row k
+            // = transposed-weight row bidx[k], columns n0 + 64 pn ..
+#pragma unroll 4
+            for (int i = lane; i < BK * (BN / 8); i += 32) {
+              const int k = i / (BN / 8), cc = i - k * (BN / 8);
+              const int pn = cc >> 3, c = cc & 7;
+              const int row = bidx[k];
+              const __nv_bfloat16* src = wsrc + (size_t)(row < 0 ? 0 : row) * p.b_ld + ti.n0 + cc * 8;
+              cp_async_16(dst + pn * 8192 + k * 128 + ((c ^ (k & 7)) << 4), src, row < 0 ? 0u : 16u);
+            }
+          }
+          cp_async_mbar_arrive_noinc(&full[stage]);
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    } else if (lane == 0) {
       uint32_t it = 0;
       for (int t = t_begin; t < tiles; t += t_step) {
         const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
@@ -487,7 +541,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == WARP_MMA) {
     // ------------------------------------------------------------ MMA issuer
     // (PAIR: the leader issues M = 256 MMAs for both CTAs; the peer's warp idles)
-    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * BM : BM, BN);
+    // B_GATHER_K tiles are MN-major (instruction descriptor bit 16)
+    const uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * BM : BM, BN) | (p.b_gather == B_GATHER_K ? (1u << 16) : 0u);
+    const bool b_mn = p.b_gather == B_GATHER_K;
     uint32_t it = 0, local = 0;
     for (int t = t_begin; t < tiles && leader; t += t_step) {
       const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
@@ -514,7 +570,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               umma_bf16_pair(tmem_d, umma_sdesc_sw128(sA + k * 32), umma_sdesc_sw128(sB + k * 32), idesc,
                              (kb | k) != 0);
             else
-              umma_bf16(tmem_d, umma_sdesc_sw128(sA + k * 32), umma_sdesc_sw128(sB + k * 32), idesc,
+              umma_bf16(tmem_d, umma_sdesc_sw128(sA + k * 32),
+                        b_mn ? umma_sdesc_sw128_mn(sB + k * 2048, 8192) : umma_sdesc_sw128(sB + k * 32), idesc,
                         (kb | k) != 0);
           }
           if constexpr (PAIR)

@@ -16,6 +16,7 @@ namespace laud {
 
 enum RowMode : int { ROWS_DENSE = 0, ROWS_PATCH = 1, ROWS_PIXEL = 2 };
 enum OutMode : int { OUT_PIXEL = 0, OUT_ROW = 1 };
+enum BGather : int { B_BOX = 0, B_GATHER_N = 1, B_GATHER_K = 2 };
 
 struct ConvParams {
   // ---- rows (output pixels)
@@ -75,6 +76,17 @@ struct ConvParams {
   int b_batched;           // B is [N][n_out][K] (3D tensor map, sample coordinate)
   const int* col_index;    // [N][col_index_ld]: scale/bias index of output column c
   int col_index_ld;
+  // ---- weights gathered in-kernel per sample (channel skipping at large batch):
+  //      B_GATHER_N: B rows = weight rows b_index[sample][n0 + j] (cp.async,
+  //                  K-major [rows][taps * kpad]; j >= k_n -> zero rows);
+  //      B_GATHER_K: B = weightT rows b_index[sample][k] for the tile's 64 K
+  //                  (MN-major [K rows][n_out], 1x1 only; k >= k_n -> zero).
+  int b_gather;
+  const int* b_index;
+  int b_index_ld;
+  int b_rows;              // rows of the gathered weight tensor
+  const void* weight_g;    // gathered weights (bf16) and their row stride in elements
+  int b_ld;
   // ---- masker-conv3 fusion: mdot_out[cell(row)] += dot(bf16 output row, mdot_w)
   const float* mdot_w;
   float* mdot_out;

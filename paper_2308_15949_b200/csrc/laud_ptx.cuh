@@ -228,6 +228,17 @@ __device__ __forceinline__ uint64_t umma_sdesc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
+// MN-major, 128-byte swizzle: atoms of 8 K rows x 64 MN elements (1 KiB),
+// stacked along K (SBO = 1 KiB); 64-wide MN panels `lbo` bytes apart.
+__device__ __forceinline__ uint64_t umma_sdesc_sw128_mn(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
 // 32 lanes x 32 consecutive fp32 columns per warp (lane i <-> TMEM lane base+i).
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(

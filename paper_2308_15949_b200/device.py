@@ -276,6 +276,10 @@ class DeviceBlock:
         a.ch_coarse, a.ch_sel, a.ch_count = ptr(self._ch_coarse), ptr(self._ch_sel), ptr(self._ch_count)
         a.ch_dvals = ptr(self._ch_dvals)
         a.wpack = ptr(ws.get("wpack", _lib.lib().laud_channel_pack_bytes(n, self.cin_p, cmp, self.cout_p)))
+        if self.groups == 1 and self.dtype == torch.bfloat16:
+            if getattr(self, "w3t", None) is None:  # conv3 kernel transposed: [c_mid][c_out] (laud.h w3t)
+                self.w3t = self.w3[:, 0, :cmp].t().contiguous()
+            a.w3t = ptr(self.w3t)
         if chmask is None:
             if getattr(self, "ch_w1", None) is None:
                 raise DeviceError("no channel mask given and no channel masker weights set")

@@ -263,6 +263,31 @@ def test_channel_block_throughput_batch(n, g, stride):
     assert _rel(y[:1], skip) <= BF16_TOL
 
 
+@pytest.mark.parametrize("gather", [0, 1])
+@pytest.mark.parametrize("cin,cmid,hw,n", [(256, 64, 56, 8), (512, 128, 28, 8), (64, 64, 56, 8), (1024, 256, 14, 16)])
+def test_channel_block_gathered_weights_stages(cin, cmid, hw, n, gather, monkeypatch):
+    """Large-batch channel schedules — dense-masked (default) and the opt-in
+    in-kernel weight gathers (LAUD_CH_GATHER=1: conv2 gathers W2[sel] rows,
+    N = k_n; conv3 gathers W3^T K rows into an MN-major B tile) — at the R101
+    stage-1/2/3 geometries vs the bf16-emulating oracle; per-sample ratios 0 .. 1."""
+    monkeypatch.setenv("LAUD_CH_GATHER", str(gather))
+    R = _R()
+    blk = BlockSpec(ConvLayerSpec(cin, cmid, 1), ConvLayerSpec(cmid, cmid, 3), ConvLayerSpec(cmid, 4 * cmid, 1),
+                    TensorShape(cin, hw, hw), has_downsample=cin != 4 * cmid)
+    rng = np.random.default_rng(cin + hw)
+    bw = R.make_block_weights(blk, rng)
+    x = rng.standard_normal((n, cin, hw, hw))
+    coarse = np.zeros((n, cmid), bool)
+    for i in range(n):
+        coarse[i, rng.permutation(cmid)[: (i * cmid) // (n - 1)]] = True
+    m = R.ChannelMask(coarse, coarse, 1)
+    cfg = DynamicConfig(Paradigm.CHANNEL, channel_granularity=1)
+    y = R.block_forward_sparse(x, bw, blk, cfg, m)
+    obw = O.BlockWeights(bw.w1, bw.w2, bw.w3, bw.w_down)
+    emu = O.block_forward_sparse(x, obw, blk, cfg, O.ChannelMask(coarse, coarse, 1), emulate_bf16=True)
+    assert _rel(y, emu) <= BF16_TOL, _rel(y, emu)
+
+
 @pytest.mark.parametrize("stage,index,paradigm", [(1, 0, "spatial"), (2, 1, "spatial"), (3, 0, "spatial"),
                                                    (3, 1, "spatial"), (4, 1, "spatial"), (3, 1, "layer"),
                                                    (2, 0, "static")])

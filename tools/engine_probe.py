@@ -42,6 +42,11 @@ def shape_defs():
     d["pconv_s1"] = dict(kind="patch", n=256, h=56, c=64, s=4)
     d["pconv_s3_b1"] = dict(kind="patch", n=1, h=14, c=256, s=2)
     d["conv3_s1"] = dict(kind="conv3", m=256 * 56 * 56 // 2, n=256, k=64)
+    # channel skipping at batch 256, stage-3 geometry, k_n = 128 kept channels per sample:
+    # conv2 with in-kernel gathered W2[sel] rows (g=1) / plain W2 tiles (g=0, same shape)
+    d["chconv2_s3"] = dict(kind="chconv2", n=256, h=14, c=256, k=128, g=1)
+    d["chconv2_s3_box"] = dict(kind="chconv2", n=256, h=14, c=256, k=128, g=0)
+    d["chconv3_s3"] = dict(kind="chconv3", n=256, h=14, c=256, co=1024, k=128, g=2)
     return d
 
 
@@ -75,6 +80,38 @@ def run(name, spec, flush, reps=20):
                   rows_max=b * h * h, lst=lst, count=cnt, patch=(s, s), cells=(hc, hc))
         flops = 2.0 * m * c * 9 * c
         nbytes = 2.0 * (b * h * h * c + m * c + 9 * c * c)
+    elif spec["kind"] in ("chconv2", "chconv3"):
+        import numpy as np
+        b, h, c, kk = spec["n"], spec["h"], spec["c"], spec["k"]
+        sr = (h * h + 127) // 128 * 128
+        sel = np.stack([np.sort(np.random.default_rng(i).permutation(c)[:kk]) for i in range(b)]).astype(np.int32)
+        selp = np.zeros((b, c), np.int32)
+        selp[:, :kk] = sel
+        sel_t = torch.from_numpy(selp).cuda()
+        cnt = torch.full((b,), kk, dtype=torch.int32, device="cuda")
+        if spec["kind"] == "chconv2":
+            a = bf(b, h, h, c)
+            w = bf(c, 9, c)
+            out = torch.empty(b * h * h, c, dtype=torch.bfloat16, device="cuda")
+            ex = dict(sample_rows=sr, chan_count=cnt, n_dyn=1, col_index=sel_t, col_index_ld=c)
+            if spec["g"]:
+                ex.update(b_gather=1, b_index=sel_t, b_index_ld=c, b_rows=c)
+            kw = dict(act=a, in_hw=(h, h), in_c=c, in_ld=c, weight=w, n_out=c, out=out, out_ld=c,
+                      out_hw=(h, h), batch=b, ksize=3, pad=1, relu=1, out_mode=CH.OUT_ROW, rows_max=b * sr,
+                      bias=torch.zeros(c, device="cuda"), **ex)
+            flops = 2.0 * b * h * h * kk * 9 * c
+            nbytes = 2.0 * (b * h * h * c + b * h * h * kk + 9 * c * c)
+        else:
+            co = spec["co"]
+            a = bf(b * h * h, c)
+            w = bf(c, co)
+            out = bf(b, h, h, co)
+            ex = dict(sample_rows=sr, chan_count=cnt, k_dyn=1, b_gather=2, b_index=sel_t, b_index_ld=c, b_rows=c)
+            kw = dict(act=a, in_hw=(h, h), in_c=c, in_ld=c, weight=w, n_out=co, out=out, out_ld=co,
+                      out_hw=(h, h), batch=b, a_compact=1, resid=out, resid_ld=co, rows_max=b * sr,
+                      bias=torch.zeros(co, device="cuda"), **ex)
+            flops = 2.0 * b * h * h * kk * co
+            nbytes = 2.0 * (b * h * h * kk + 2 * b * h * h * co + c * co)
     else:
         b, h, c = spec["n"], spec["h"], spec["c"]
         a = bf(b, h, h, c)
