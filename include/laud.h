@@ -252,6 +252,11 @@ typedef struct laud_block_args {
    * W3[:, sel] (conv2's N gather W2[sel] uses w2).  NULL = dense-masked
    * schedule at large batch. */
   const void* w3t;
+  /* optional second stream: at small grids (<= 4096 mask cells) the spatial /
+   * layer masker runs there, concurrently with conv1 (both only read x), and
+   * the block's stream waits for it before the skip path and conv2 (graph
+   * capture: a fork/join).  NULL = masker on `stream` (or fused into conv1). */
+  void* aux_stream;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

@@ -60,7 +60,7 @@ class BlockArgs(C.Structure):
         ("ch_expanded", _vp), ("ch_sel", _vp), ("ch_count", _vp), ("ch_dvals", _vp),
         ("wpack", _vp), ("prev_coarse", _vp), ("dn", _vp), ("next_wdiff", _vp), ("ch_bias", _vp), ("fp32", C.c_int),
         ("conv1_dense", C.c_int), ("se_w1", _vp), ("se_b1", _vp), ("se_w2", _vp), ("se_b2", _vp),
-        ("se_hidden", C.c_int), ("cell_sums", _vp), ("w2_dense", _vp), ("w3t", _vp),
+        ("se_hidden", C.c_int), ("cell_sums", _vp), ("w2_dense", _vp), ("w3t", _vp), ("aux_stream", _vp),
     ]
 
 

@@ -278,6 +278,18 @@ int pick_bn(int n_out, int k, long long rows) {
   return 256;  // measured best for every R101 conv shape at batch 256 (tools/sweep_cfg.sh)
 }
 
+// Events of the block forward's masker fork/join (laud_block_args.aux_stream);
+// reused call after call (stream-ordered, and under graph capture each record
+// / wait pair becomes a graph edge at capture time).
+cudaEvent_t fork_event(int i) {
+  static cudaEvent_t ev[2] = {nullptr, nullptr};
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  });
+  return ev[i];
+}
+
 // fused masker dots riding on a dense 1x1 conv (ConvParams::adot_*)
 struct AdotArgs {
   const float* w;
@@ -1021,9 +1033,23 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     const char* e = getenv("LAUD_MASKER_IN_CONV1");
     return e ? atoi(e) : 1;
   }();
-  const bool fuse_masker = fuse_env && a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense &&
+  // small grids (latency-bound, e.g. batch 1): the one-launch standalone
+  // masker on the auxiliary stream, concurrent with a plain conv1 — its
+  // decisions cost no time on the block's critical path (conv1's fused
+  // readers would lengthen conv1's single-CTA K loop instead)
+  static const int fork_env = [] {
+    const char* e = getenv("LAUD_MASKER_FORK");
+    return e ? atoi(e) : 1;
+  }();
+  const bool masker_computed = (a->paradigm == LAUD_PARADIGM_SPATIAL || a->paradigm == LAUD_PARADIGM_LAYER) &&
+                               !a->given_coarse && !a->dn && a->masker_wdiff;
+  const long long mask_cells =
+      a->paradigm == LAUD_PARADIGM_LAYER ? n : (a->s > 0 ? (long long)n * (ho / a->s) * (wo / a->s) : 0);
+  const bool fork_masker = fork_env && a->aux_stream && masker_computed && mask_cells <= 4096;
+  const bool fuse_masker = fuse_env && !fork_masker && a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense &&
                            !a->given_coarse && !a->dn && !a->fp32 && a->masker_wdiff && a->cell_sums &&
                            a->x_ld == a->c_in && a->c_in % 64 == 0;
+  cudaEvent_t fork_done = nullptr;
 
   // ---------------------------------------------------------------- rows
   int pm;  // row mode for conv2/conv3
@@ -1066,6 +1092,18 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
                                               a->coarse_out, a->cell_list, a->cell_count,
                                               a->partial, a->scan, st, a->prev_coarse, a->dn),
                         "spatial masker (fused)", 2);
+      } else if (fork_masker) {
+        cudaStream_t aux = (cudaStream_t)a->aux_stream;
+        cudaEvent_t x_ready = fork_event(0);
+        fork_done = fork_event(1);
+        if ((rc = cuda_check(cudaEventRecord(x_ready, st), "fork record", 0)) ||
+            (rc = cuda_check(cudaStreamWaitEvent(aux, x_ready, 0), "fork wait", 0)))
+          return rc;
+        rc = laud_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in,
+                                 a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
+                                 a->masker_wdiff, a->masker_bias, a->coarse_out, a->cell_list,
+                                 a->cell_count, a->partial, a->scan, aux);
+        if (rc == LAUD_OK) rc = cuda_check(cudaEventRecord(fork_done, aux), "join record", 0);
       } else {
         rc = laud_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in,
                                  a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
@@ -1129,6 +1167,17 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     } else {
       return rc;
     }
+  }
+
+  if (fork_done) {
+    // conv1 runs densely on the block's stream while the forked masker
+    // decides (for a layer block, inactive samples' h1 is computed but never
+    // read); the decisions are joined before the skip path (ReLU at inactive
+    // cells) and conv2
+    c1.row_mode = ROWS_DENSE;
+    if ((rc = run_conv(&c1, st))) return rc;
+    conv1_done = true;
+    if ((rc = cuda_check(cudaStreamWaitEvent(st, fork_done, 0), "join wait", 0))) return rc;
   }
 
   // ---------------------------------------------------------------- skip path

@@ -300,7 +300,8 @@ class DeviceBlock:
                 misplace_first: bool = False, stream=None, ws: Optional[Workspace] = None,
                 chmask: Optional[torch.Tensor] = None, coarse_out: Optional[torch.Tensor] = None,
                 prev_coarse: Optional[torch.Tensor] = None, dn: Optional[torch.Tensor] = None,
-                next_wdiff: Optional[torch.Tensor] = None, conv1_dense: Optional[bool] = None):
+                next_wdiff: Optional[torch.Tensor] = None, conv1_dense: Optional[bool] = None,
+                aux_stream=None):
         """x: (N, H, W, cin_p) bf16 CUDA.  Returns (out, coarse, cell_list, cell_count)."""
         n, h, w, cl = x.shape
         if cl != self.cin_p or x.dtype != self.dtype or not x.is_contiguous():
@@ -364,5 +365,7 @@ class DeviceBlock:
                 a.w2_dense = ptr(self.w2_dense)
         if dn is not None and paradigm == "spatial":
             a.dn, a.prev_coarse, a.next_wdiff = ptr(dn), ptr(prev_coarse), ptr(next_wdiff)
+        if aux_stream is not None:  # small grids: masker forked onto it (laud.h aux_stream)
+            a.aux_stream = stream_handle(aux_stream)
         _lib.check(lib.laud_block_forward(C.byref(a), stream_handle(stream)))
         return out, coarse_buf, cell_list, counts

@@ -219,6 +219,11 @@ class LaudNetwork:
             x = pool
         return self._blocks_and_head(x, n, stream, record)
 
+    def _aux_stream(self):
+        if getattr(self, "_aux", None) is None:
+            self._aux = torch.cuda.Stream(device=self.device)
+        return self._aux
+
     def _blocks_and_head(self, x, n, stream, record):
         sh = D.stream_handle(stream)
         ping = 0
@@ -247,6 +252,8 @@ class LaudNetwork:
                     kw["dn"] = self._buf("dn", (ncell,), torch.float32)
                     kw["prev_coarse"] = prev_coarse if fused_in else None
                     kw["next_wdiff"] = nxt.db.wdiff if fused_out else None
+            if para in ("spatial", "layer"):
+                kw["aux_stream"] = self._aux_stream()  # small grids fork the masker (laud.h aux_stream)
             y, coarse, cells, counts = db.forward(x, para, slot.s if para == "spatial" else 0,
                                                   out=out, stream=stream, ws=self.ws, **kw)
             prev_coarse = kw.get("coarse_out")
