@@ -145,6 +145,12 @@ typedef struct laud_conv_args {
   const int* b_index;
   int b_index_ld;
   int b_rows;
+  /* small grids: the halo patch conv (3x3 over S x S patches) may split K over
+   * a thread-block cluster (fp32 partials reduced through distributed shared
+   * memory) when one wave of tiles leaves SMs idle — a different fp32
+   * summation order than the unsplit conv, so off by default (the mirror API
+   * keeps sparse == dense-masked bitwise); the network executor enables it. */
+  int latency_split;
 } laud_conv_args;
 
 int laud_conv(const laud_conv_args* a, void* stream);
@@ -257,6 +263,8 @@ typedef struct laud_block_args {
    * the block's stream waits for it before the skip path and conv2 (graph
    * capture: a fork/join).  NULL = masker on `stream` (or fused into conv1). */
   void* aux_stream;
+  /* allow the conv2 split-K of laud_conv_args.latency_split at small grids. */
+  int latency_split;
 } laud_block_args;
 
 /* Channel masker alone — replaces `channel_masker_forward` (reference.py:189-218):

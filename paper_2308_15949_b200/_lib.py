@@ -40,6 +40,7 @@ class ConvArgs(C.Structure):
         ("col_index", _vp), ("col_index_ld", C.c_int), ("mdot_w", _vp), ("mdot_out", _vp),
         ("misplace_first", C.c_int), ("groups", C.c_int), ("fp32", C.c_int),
         ("b_gather", C.c_int), ("b_index", _vp), ("b_index_ld", C.c_int), ("b_rows", C.c_int),
+        ("latency_split", C.c_int),
     ]
 
 
@@ -60,7 +61,7 @@ class BlockArgs(C.Structure):
         ("ch_expanded", _vp), ("ch_sel", _vp), ("ch_count", _vp), ("ch_dvals", _vp),
         ("wpack", _vp), ("prev_coarse", _vp), ("dn", _vp), ("next_wdiff", _vp), ("ch_bias", _vp), ("fp32", C.c_int),
         ("conv1_dense", C.c_int), ("se_w1", _vp), ("se_b1", _vp), ("se_w2", _vp), ("se_b2", _vp),
-        ("se_hidden", C.c_int), ("cell_sums", _vp), ("w2_dense", _vp), ("w3t", _vp), ("aux_stream", _vp),
+        ("se_hidden", C.c_int), ("cell_sums", _vp), ("w2_dense", _vp), ("w3t", _vp), ("aux_stream", _vp), ("latency_split", C.c_int),
     ]
 
 

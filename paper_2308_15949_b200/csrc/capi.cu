@@ -421,6 +421,20 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
       if ((rc = tensor_map_2d(a->act, p.a_rows, a->in_c, a->in_ld, 1, &ma)) ||
           (rc = tensor_map_2d(a->weight, a->n_out, kw, kw, hbn, &mb)))
         return rc;
+      // split-K over a cluster when one wave of tiles leaves most SMs idle
+      const long long pc_tiles = ((long long)(a->rows_max / (s * s)) + 128 / s - 1) / (128 / s) * ((a->n_out + hbn - 1) / hbn);
+      const int ncb = p.kpad / 64;
+      p.ksplit = 1;
+      static const int ks_max = [] {
+        const char* e = getenv("LAUD_KSPLIT_MAX");
+        return e ? atoi(e) : 8;
+      }();
+      if (a->latency_split)
+        for (int k = ks_max; k >= 2; k >>= 1)
+          if (ncb % k == 0 && pc_tiles * k <= num_sms()) {
+            p.ksplit = k;
+            break;
+          }
       ProfScope ps(0, st, a->count);
       if (ps.on) {
         ps.rec.rows_per_count = (long long)s * s;
@@ -1274,6 +1288,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c2.weight = a->w2;
   c2.n_out = a->c_mid;
   c2.groups = a->groups;
+  c2.latency_split = a->latency_split;
   c2.scale = a->s2;
   c2.bias = a->b2;
   c2.relu = a->relu2;

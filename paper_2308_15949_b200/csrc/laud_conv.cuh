@@ -87,6 +87,10 @@ struct ConvParams {
   int b_rows;              // rows of the gathered weight tensor
   const void* weight_g;    // gathered weights (bf16) and their row stride in elements
   int b_ld;
+  // ---- split-K over a thread-block cluster (halo patch conv, small grids):
+  //      ksplit CTAs of a cluster take disjoint channel-block ranges of one
+  //      tile; fp32 partials are reduced through distributed shared memory
+  int ksplit;
   // ---- masker-conv3 fusion: mdot_out[cell(row)] += dot(bf16 output row, mdot_w)
   const float* mdot_w;
   float* mdot_out;

@@ -77,6 +77,9 @@ struct Cfg {
   static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
   static constexpr int ALLOC = TMEM_SLOT_OFF + 16 + 1024;
   static_assert(STAGES >= 2, "shared memory: fewer than two weight stages");
+  // split-K partials [S*128 rows][PSTRIDE fp32] reuse the halo + weight stages
+  static constexpr int PSTRIDE = BN + 4;  // +16 B: conflict-free row-per-lane float4 stores
+  static_assert(S * 128 * PSTRIDE * 4 <= STG_OFF, "split-K partials must fit the halo + weight region");
   static_assert(ALLOC <= 227 * 1024, "shared memory budget");
   static_assert(EW_COLS % 16 == 0, "epilogue slice");
 };
@@ -145,6 +148,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int m_tiles = (count + P - 1) / P;
   const int tiles = m_tiles * n_tiles;
   const int ncb = p.kpad / 64;  // channel blocks
+  // split-K (small grids): the KS CTAs of a cluster share a tile, CTA ks takes
+  // channel blocks [cb0, cb1); the host launches one wave (one tile per cluster)
+  const int KS = p.ksplit > 1 ? p.ksplit : 1;
+  const int ks = KS > 1 ? (int)cluster_ctarank() : 0;
+  const int t_begin = blockIdx.x / KS, t_step = gridDim.x / KS;
+  const int cb0 = ks * ncb / KS, cb1 = (ks + 1) * ncb / KS;
 
   if (warp < NUM_PROD) {
     // ---------------------------------------------------------------- halo producers
@@ -157,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int quad = op % (P / 4);  // 4 patches p = 4*quad .. 4*quad+3
     const int cpi = p.cells_h * p.cells_w;
     uint32_t fill = 0;  // band fills so far (same sequence for every band)
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int t = t_begin; t < tiles; t += t_step) {
       const int mt = t / n_tiles;
       int pn[4], py[4], px[4];
       bool pv[4];
@@ -175,7 +184,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           px[j] = (cr - ci * p.cells_w) * S - 1 + xpos;
         }
       }
-      for (int cb = 0; cb < ncb; ++cb, ++fill) {
+      for (int cb = cb0; cb < cb1; ++cb, ++fill) {
         for (int y = 0; y < E; ++y) {
           mbar_wait(&band_empty[y], (fill & 1) ^ 1);
           const uint32_t dst = base_u32 + L::HALO_OFF + y * L::BAND_BYTES + (xpos * P + quad * 4) * 128;
@@ -198,9 +207,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- weights (B) TMA
     if (lane == 0) {
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t_begin; t < tiles; t += t_step) {
         const int n0 = (t % n_tiles) * BN;
-        for (int cb = 0; cb < ncb; ++cb)
+        for (int cb = cb0; cb < cb1; ++cb)
           for (int tap = 0; tap < 9; ++tap, ++it) {
             const int stage = it % L::STAGES;
             mbar_wait(&empty[stage], ((it / L::STAGES) & 1) ^ 1);
@@ -213,12 +222,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
     uint32_t it = 0, fill = 0, local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = t_begin; t < tiles; t += t_step, ++local) {
       const int buf = local % L::NBUF;
       mbar_wait(&acc_empty[buf], ((local / L::NBUF) & 1) ^ 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + buf * L::TILE_COLS;
-      for (int cb = 0; cb < ncb; ++cb, ++fill) {
+      for (int cb = cb0; cb < cb1; ++cb, ++fill) {
         for (int ky = 0; ky < 3; ++ky) {
           // bands first read at this ky: 0 .. S-1 at ky = 0, then ky + S - 1
           for (int y = (ky == 0 ? 0 : ky + S - 1); y <= ky + S - 1; ++y) mbar_wait(&band_full[y], fill & 1);
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                   umma_bf16(tacc + ly * BN, umma_sdesc_sw128(sa + k * 32), umma_sdesc_sw128(sb + k * 32), idesc,
-                            (cb | ky | kx | k) != 0);
+                            cb != cb0 || (ky | kx | k) != 0);
               }
               umma_commit(&empty[stage]);
               // bands whose last reader was this ky go back to the producers
@@ -270,9 +279,31 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int i = q * 32 + lane;
     const int lx = i / P, pl = i - (i / P) * P;
     uint32_t local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = t_begin; t < tiles; t += t_step, ++local) {
       const int buf = local % L::NBUF;
       const int mt = t / n_tiles;
+      if (KS > 1) {
+        // split-K: this CTA's fp32 partial -> its own smem (the halo / weight
+        // region: every MMA of the tile has completed), reduced after the
+        // cluster barrier below
+        mbar_wait(&acc_full[buf], (local / L::NBUF) & 1);
+        tc_fence_after();
+        for (int ly = 0; ly < S; ++ly) {
+          const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * L::TILE_COLS + ly * BN + col0;
+          float* prow = reinterpret_cast<float*>(base + L::HALO_OFF) + (size_t)(ly * 128 + q * 32 + lane) * L::PSTRIDE + col0;
+#pragma unroll 1
+          for (int j = 0; j < EW / CH; ++j) {
+            uint32_t r[CH];
+            tmem_ld_32x32b<CH>(tbase + j * CH, r);
+#pragma unroll
+            for (int e = 0; e < CH; e += 4)
+              *reinterpret_cast<float4*>(prow + j * CH + e) =
+                  make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), __uint_as_float(r[e + 2]),
+                              __uint_as_float(r[e + 3]));
+          }
+        }
+        continue;
+      }
       const int c_base = (t % n_tiles) * BN + col0;
       const int nch = max(0, min(EW, p.n_out - c_base));
       const int pi = mt * P + pl;
@@ -327,6 +358,47 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
+  if (KS > 1) {
+    // split-K reduction through distributed shared memory: CTA ks finishes rows
+    // [ks, ks + 1) * S*128/KS of the tile's (ly, row) space, summing the KS
+    // partials in rank order (deterministic), then scale / bias / ReLU -> bf16
+    cluster_sync();  // every CTA's partials written and visible cluster-wide
+    if (t_begin < tiles) {
+      const int t = t_begin;
+      const int mt = t / n_tiles, n0 = (t % n_tiles) * BN;
+      constexpr int RR = S * 128;
+      const int rpc = RR / KS;
+      constexpr int C4 = BN / 4;
+      const uint32_t part = base_u32 + L::HALO_OFF;
+      __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
+      for (int idx = threadIdx.x; idx < rpc * C4; idx += THREADS) {
+        const int lr = ks * rpc + idx / C4, c4 = idx % C4;
+        const int ly = lr / 128, row = lr % 128;
+        const int lx = row / P, pl = row - lx * P;
+        const int pi = mt * P + pl;
+        const int c = n0 + c4 * 4;
+        if (pi >= count || c >= p.n_out) continue;
+        const uint32_t off = (uint32_t)(((ly * 128 + row) * L::PSTRIDE + c4 * 4) * 4);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < KS; ++r) {
+          float4 v;
+          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "r"(mapa_shared(part + off, r)) : "memory");
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        float o[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          o[e] = fmaf(o[e], vsc[c + e], vbi[c + e]);
+          if (p.relu) o[e] = fmaxf(o[e], 0.f);
+        }
+        const long long dst = (long long)pi * s2 + ly * S + lx;
+        *reinterpret_cast<uint2*>(outp + dst * p.out_ld + c) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
+      }
+    }
+    cluster_sync();  // peers done reading this CTA's partials
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == WARP_MMA) {
@@ -348,6 +420,23 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParam
   }
   const int s2 = S * S;
   const long long tiles = ((long long)(p.rows_max / s2) + L::P - 1) / L::P * ((p.n_out + BN - 1) / BN);
+  if (p.ksplit > 1) {  // one wave of clusters, one tile each (host-checked)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(tiles * p.ksplit), 1, 1);
+    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.dynamicSmemBytes = L::ALLOC;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.ksplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  }
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
   return launch_k(kern, dim3(grid), dim3(THREADS), L::ALLOC, stream, ta, tb, p);

@@ -301,7 +301,7 @@ class DeviceBlock:
                 chmask: Optional[torch.Tensor] = None, coarse_out: Optional[torch.Tensor] = None,
                 prev_coarse: Optional[torch.Tensor] = None, dn: Optional[torch.Tensor] = None,
                 next_wdiff: Optional[torch.Tensor] = None, conv1_dense: Optional[bool] = None,
-                aux_stream=None):
+                aux_stream=None, latency_split: bool = False):
         """x: (N, H, W, cin_p) bf16 CUDA.  Returns (out, coarse, cell_list, cell_count)."""
         n, h, w, cl = x.shape
         if cl != self.cin_p or x.dtype != self.dtype or not x.is_contiguous():
@@ -367,5 +367,6 @@ class DeviceBlock:
             a.dn, a.prev_coarse, a.next_wdiff = ptr(dn), ptr(prev_coarse), ptr(next_wdiff)
         if aux_stream is not None:  # small grids: masker forked onto it (laud.h aux_stream)
             a.aux_stream = stream_handle(aux_stream)
+        a.latency_split = int(latency_split)  # small grids: conv2 split-K over a cluster
         _lib.check(lib.laud_block_forward(C.byref(a), stream_handle(stream)))
         return out, coarse_buf, cell_list, counts

@@ -166,6 +166,9 @@ class LaudNetwork:
         # masker-conv3 fusion: block i+1 reuses block i's conv3 output dots when
         # both run on the same grid with the same S and i+1 has no downsample
         self.fuse_masker = False  # measured: the conv3 dot costs more than the masker saves
+        # small grids: conv2 may split K over a thread-block cluster (laud.h
+        # latency_split; a different fp32 summation order, within the logit gates)
+        self.latency_split = os.environ.get("LAUD_LATENCY_SPLIT", "1") != "0"
         for i, slot in enumerate(self.slots):
             prev = self.slots[i - 1] if i > 0 else None
             b = slot.db.block
@@ -254,6 +257,7 @@ class LaudNetwork:
                     kw["next_wdiff"] = nxt.db.wdiff if fused_out else None
             if para in ("spatial", "layer"):
                 kw["aux_stream"] = self._aux_stream()  # small grids fork the masker (laud.h aux_stream)
+                kw["latency_split"] = self.latency_split
             y, coarse, cells, counts = db.forward(x, para, slot.s if para == "spatial" else 0,
                                                   out=out, stream=stream, ws=self.ws, **kw)
             prev_coarse = kw.get("coarse_out")

@@ -90,11 +90,14 @@ def test_patch_rows_gather_scatter():
 
 @pytest.mark.parametrize("s,cin,cout,n,h,density", [
     (2, 256, 256, 8, 14, 0.5), (2, 128, 128, 4, 28, 0.5), (4, 64, 64, 4, 56, 0.5), (2, 64, 64, 3, 16, 0.3),
-    (4, 128, 128, 2, 28, 0.7), (2, 256, 256, 64, 14, 0.5), (2, 40, 24, 2, 8, 1.0), (4, 64, 64, 1, 8, 0.0)])
-def test_patch_conv_halo_smem(s, cin, cout, n, h, density):
+    (4, 128, 128, 2, 28, 0.7), (2, 256, 256, 64, 14, 0.5), (2, 40, 24, 2, 8, 1.0), (4, 64, 64, 1, 8, 0.0),
+    (2, 256, 256, 1, 14, 0.5), (2, 512, 256, 2, 14, 0.6), (4, 256, 64, 1, 56, 0.5)])
+@pytest.mark.parametrize("split", [0, 1])
+def test_patch_conv_halo_smem(s, cin, cout, n, h, density, split):
     """3x3 patch conv over active S x S cells (the halo-in-shared-memory kernel for
     S = 2 / 4, stride 1): ragged patch counts (not a multiple of the tile's patch
-    count), image-border cells (zero halo), several N tiles, scale/bias/ReLU."""
+    count), image-border cells (zero halo), several N tiles, scale/bias/ReLU; with
+    latency_split the small grids split K over a cluster (DSMEM reduction)."""
     CH, D = _engine()
     g = torch.Generator().manual_seed(s * 1000 + cin + n)
     x = torch.randn(n, h, h, cin, generator=g).cuda().to(torch.bfloat16)
@@ -110,7 +113,7 @@ def test_patch_conv_halo_smem(s, cin, cout, n, h, density):
     CH.conv(act=x, in_hw=(h, h), in_c=cin, in_ld=cin, weight=D.pack_weight(w, cin), n_out=cout, out=rows,
             out_ld=cout, out_hw=(h, h), batch=n, ksize=3, pad=1, row_mode=CH.ROWS_PATCH,
             rows_max=n * h * h, lst=lst, count=cnt, patch=(s, s), cells=(hc, hc),
-            out_mode=CH.OUT_ROW, scale=sc.cuda(), bias=bi.cuda(), relu=1)
+            out_mode=CH.OUT_ROW, scale=sc.cuda(), bias=bi.cuda(), relu=1, latency_split=split)
     torch.cuda.synchronize()
     if len(cells) == 0:
         assert (rows.float() == 7.0).all()
