@@ -94,8 +94,9 @@ def main():
                             cz[i, rng.permutation(cells)[:k]] = 1
                         coarse = torch.from_numpy(cz.reshape(-1)).cuda()
                         for dense1 in ((False, True) if s <= 2 else (False,)):
+                            # latency_split as the network executor runs it (laud.h)
                             us = timed(lambda: db.forward(x, "spatial", s, coarse=coarse, out=out_t, ws=ws,
-                                                          conv1_dense=dense1), flush)
+                                                          conv1_dense=dense1, latency_split=True), flush)
                             add("spatial", us, S=s, r=k / cells, conv1_dense=dense1)
                 cm = blk.conv2.out_channels
                 for r in ratios:
@@ -111,7 +112,8 @@ def main():
                     d[rng.permutation(n)[:kl]] = 1
                     lm = torch.from_numpy(d).cuda()
                     if n > 1 or kl in (0, 1):
-                        add("layer", timed(lambda: db.forward(x, "layer", coarse=lm, out=out_t, ws=ws), flush),
+                        add("layer", timed(lambda: db.forward(x, "layer", coarse=lm, out=out_t, ws=ws,
+                                                              latency_split=True), flush),
                             r=kl / n)
                 print(arch, bp["stage"], bp["index"], n, len(rows), flush=True)
     with open(out, "w") as f:
