@@ -692,7 +692,9 @@ def block_sweep_b1_vs_cpu(torch, args, flush, reps_cpu=3):
             else:
                 cz = _exact_masks(rng, 1, cells, r)[0]
                 coarse = torch.from_numpy(cz).cuda()
-                fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp)  # noqa: E731
+                # the network executor's schedule: dense conv1, small-grid split-K
+                fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp,  # noqa: E731
+                                        conv1_dense=True, latency_split=True)
                 c3 = cz.reshape(1, o.height // s, o.width // s).astype(bool)
                 cfg = DynamicConfig(Paradigm.SPATIAL, spatial_granularity=s)
                 om = O.SpatialMask(c3, O.upsample_coarse(c3, s), s)
@@ -783,7 +785,9 @@ def block_sweep(torch, args, flush, pk):
             else:
                 cz = _exact_masks(rng, n, cells, r)
                 coarse = torch.from_numpy(cz.reshape(-1)).cuda()
-                fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp)  # noqa: E731
+                # the network executor's schedule: dense conv1, small-grid split-K
+                fn = lambda: db.forward(xx, "spatial", s, coarse=coarse, out=xx, ws=wsp,  # noqa: E731
+                                        conv1_dense=True, latency_split=True)
                 a = RF.block_algorithmic(blk, "spatial", n, coarse=cz.reshape(n, o.height // s, o.width // s), s=s)
             g, _ = capture(torch, fn, 2)
             tot, _ = timed_graph(torch, g, 10, flush, torch.cuda.current_stream())
