@@ -126,7 +126,7 @@ def main():
         "by_paradigm": by_para,
         "optimizer": {"iterations": int(res.nit), "final_msle_fit_rows": float(res.fun)},
     }
-    (ROOT / "profiles" / "r01_predictor_fit.json").write_text(json.dumps(report, indent=1) + "\n")
+    (ROOT / "profiles" / f"{Path(sys.argv[1]).name.split('_')[0]}_predictor_fit.json").write_text(json.dumps(report, indent=1) + "\n")
     print(json.dumps(report["all_rows"]), json.dumps(report["held_out"]))
 
 

@@ -84,7 +84,7 @@ def main():
     (ROOT / "paper_2308_15949_b200" / "data").mkdir(exist_ok=True)
     (ROOT / "paper_2308_15949_b200" / "data" / "b200_predictor.json").write_text(
         json.dumps({"params": params, "source": sys.argv[1]}, indent=1) + "\n")
-    (ROOT / "profiles" / "r01_native_predictor_fit.json").write_text(json.dumps(report, indent=1) + "\n")
+    (ROOT / "profiles" / f"{Path(sys.argv[1]).name.split('_')[0]}_native_predictor_fit.json").write_text(json.dumps(report, indent=1) + "\n")
     print(json.dumps({k: report[k] for k in ("fit_rows", "held_out", "by_paradigm_held_out")}, indent=1))
 
 
