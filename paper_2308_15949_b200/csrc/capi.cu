@@ -402,17 +402,17 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
   // Patch conv2 with the halo in shared memory (patch_conv.cu): stride-1 3x3
   // over S = 2 / 4 patches, compact output rows, plain affine epilogue
   static const int halo_env = [] {
-    const char* e = getenv("LAUD_HALO");
-    return e ? atoi(e) : 1;
+    const char* e = getenv("LAUD_HALO");  // bit 0: halo conv2, bit 1: also grouped conv2
+    return e ? atoi(e) : 3;
   }();
   if (halo_env && !ad && a->row_mode == ROWS_PATCH && a->ksize == 3 && a->stride == 1 && a->pad == 1 &&
-      p.groups == 1 && !a->a_compact && !a->sample_rows && !a->chan_count && !a->b_batched &&
+      (p.groups == 1 || (halo_env & 2)) && !a->a_compact && !a->sample_rows && !a->chan_count && !a->b_batched &&
       a->out_mode == OUT_ROW && !a->resid && !a->ymask_coarse && !a->ymask_channel && !a->mdot_w &&
       !a->relu_inactive_coarse && !a->out_f32 && !a->col_index && !a->misplace_first &&
       a->patch_h == a->patch_w && a->in_h == a->out_h && a->in_w == a->out_w && a->n_out <= 512 &&
       (reinterpret_cast<uintptr_t>(a->act) % 16) == 0 && (long long)a->batch * a->in_h * a->in_w < (1ll << 31) - 1) {
     const int s = a->patch_h;
-    const int hbn = s == 4 ? 64 : (a->n_out % 128 == 0 ? 128 : 64);
+    const int hbn = (s == 4 || p.groups > 1) ? 64 : (a->n_out % 128 == 0 ? 128 : 64);
     if (patch_conv_supported(s, hbn)) {
       p.a_rows = a->batch * a->in_h * a->in_w;
       int rc;
@@ -429,7 +429,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
         const char* e = getenv("LAUD_KSPLIT_MAX");
         return e ? atoi(e) : 8;
       }();
-      if (a->latency_split)
+      if (a->latency_split && p.groups == 1)
         for (int k = ks_max; k >= 2; k >>= 1)
           if (ncb % k == 0 && pc_tiles * k <= num_sms()) {
             p.ksplit = k;

@@ -153,7 +153,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int KS = p.ksplit > 1 ? p.ksplit : 1;
   const int ks = KS > 1 ? (int)cluster_ctarank() : 0;
   const int t_begin = blockIdx.x / KS, t_step = gridDim.x / KS;
-  const int cb0 = ks * ncb / KS, cb1 = (ks + 1) * ncb / KS;
+  // channel blocks of tile t for this CTA: all of them, or (grouped conv) only
+  // those holding the input channels of the groups the tile's N range spans
+  // (the block-diagonal weights are zero elsewhere); split-K takes a slice
+  auto cb_range = [&](int t, int& b0, int& b1) {
+    int lo = 0, hi = ncb;
+    if (p.groups > 1) {
+      const int n0 = (t % n_tiles) * BN;
+      const int g0 = n0 / p.gw_out;
+      const int g1 = min(p.groups, (min(n0 + BN, p.n_out) + p.gw_out - 1) / p.gw_out);
+      lo = (g0 * p.gw_in) / 64;
+      hi = (g1 * p.gw_in + 63) / 64;
+    }
+    b0 = lo + ks * (hi - lo) / KS;
+    b1 = lo + (ks + 1) * (hi - lo) / KS;
+  };
 
   if (warp < NUM_PROD) {
     // ---------------------------------------------------------------- halo producers
@@ -184,6 +198,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           px[j] = (cr - ci * p.cells_w) * S - 1 + xpos;
         }
       }
+      int cb0, cb1;
+      cb_range(t, cb0, cb1);
       for (int cb = cb0; cb < cb1; ++cb, ++fill) {
         for (int y = 0; y < E; ++y) {
           mbar_wait(&band_empty[y], (fill & 1) ^ 1);
@@ -209,6 +225,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t it = 0;
       for (int t = t_begin; t < tiles; t += t_step) {
         const int n0 = (t % n_tiles) * BN;
+        int cb0, cb1;
+        cb_range(t, cb0, cb1);
         for (int cb = cb0; cb < cb1; ++cb)
           for (int tap = 0; tap < 9; ++tap, ++it) {
             const int stage = it % L::STAGES;
@@ -227,6 +245,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&acc_empty[buf], ((local / L::NBUF) & 1) ^ 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + buf * L::TILE_COLS;
+      int cb0, cb1;
+      cb_range(t, cb0, cb1);
       for (int cb = cb0; cb < cb1; ++cb, ++fill) {
         for (int ky = 0; ky < 3; ++ky) {
           // bands first read at this ky: 0 .. S-1 at ky = 0, then ky + S - 1

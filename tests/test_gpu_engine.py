@@ -139,6 +139,38 @@ def test_compaction_matches_argwhere():
         assert plan.patch_count == int(coarse.sum())
 
 
+@pytest.mark.parametrize("c,groups,s,n,h,density", [
+    (48, 2, 4, 4, 56, 0.5), (120, 5, 4, 2, 28, 0.5), (336, 14, 2, 8, 14, 0.5), (336, 14, 2, 1, 14, 1.0),
+    (120, 5, 2, 3, 28, 0.3)])
+def test_grouped_patch_conv_halo(c, groups, s, n, h, density):
+    """Grouped 3x3 conv (RegNet conv2, block-diagonal weights) over active S x S
+    patches on the halo kernel: each N tile loads only the channel blocks of its
+    groups; vs torch's grouped conv at the active cells."""
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(c + groups + s)
+    x = torch.randn(n, h, h, c, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(c, c // groups, 3, 3, generator=g) / np.sqrt(9 * c // groups)).to(torch.bfloat16).float()
+    hc = h // s
+    rng = np.random.default_rng(n + h + c)
+    cells = np.flatnonzero(rng.random(n * hc * hc) < density).astype(np.int32)
+    lst = torch.from_numpy(np.concatenate([cells, np.zeros(4, np.int32)])).cuda()
+    cnt = torch.tensor([len(cells)], dtype=torch.int32, device="cuda")
+    rows = torch.empty((len(cells) * s * s, c), dtype=torch.bfloat16, device="cuda")
+    CH.conv(act=x, in_hw=(h, h), in_c=c, in_ld=c, weight=D.pack_weight(w, c, groups=groups), n_out=c, out=rows,
+            out_ld=c, out_hw=(h, h), batch=n, ksize=3, pad=1, row_mode=CH.ROWS_PATCH, rows_max=n * h * h,
+            lst=lst, count=cnt, patch=(s, s), cells=(hc, hc), out_mode=CH.OUT_ROW, groups=groups)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.cuda(), padding=1,
+                                     groups=groups).permute(0, 2, 3, 1)
+    idx = torch.from_numpy(cells.astype(np.int64))
+    ni, r = idx // (hc * hc), idx % (hc * hc)
+    ci, cj = r // hc, r % hc
+    exp = torch.stack([ref[a, b * s:(b + 1) * s, q * s:(q + 1) * s].reshape(s * s, c)
+                       for a, b, q in zip(ni.tolist(), ci.tolist(), cj.tolist())]).reshape(-1, c)
+    err = (rows.float() - exp).norm() / exp.norm()
+    assert err < 6e-3, float(err)
+
+
 @pytest.mark.parametrize("c,groups,stride,n,h", [
     (48, 2, 1, 2, 8), (120, 5, 2, 2, 14), (336, 14, 1, 1, 14), (888, 37, 2, 1, 14), (64, 8, 1, 2, 9)])
 def test_grouped_conv_matches_torch(c, groups, stride, n, h):
