@@ -440,7 +440,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
         ps.rec.rows_per_count = (long long)s * s;
         ps.rec.rows_max = a->rows_max;
         ps.rec.n_out = a->n_out;
-        ps.rec.k_alg = 9LL * a->in_c;
+        ps.rec.k_alg = 9LL * a->in_c / p.groups;  // grouped: C_in / groups per output
         ps.rec.taps = 9;
         ps.rec.resid = 0;
       }

@@ -14,10 +14,13 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   c.num_sms = num_sms;
   c.stream = stream;
   // EP_PLAIN*: bf16 out, no per-channel scale / coarse mask / masker-dot, bias
-  // vector fits the smem cache (12 * BN floats), every warp slice full
+  // vector fits the smem cache (12 * BN floats)
+  // (a partial last N tile is fine — its extra columns are never stored —
+  // except under the per-sample channel mask, read per column)
+  const int npad = n_tiles * bn;
   c.ep_plain = !p.out_f32 && !p.scale && !p.col_index && !p.ymask_coarse && !p.mdot_w &&
-               p.n_out <= 12 * bn && p.n_out % bn == 0 &&
-               (!p.adot_out || p.n_out + p.kpad <= 12 * bn);  // + masker weights in smem
+               npad <= 12 * bn && (p.n_out % bn == 0 || !p.ymask_channel) &&
+               (!p.adot_out || npad + p.kpad <= 12 * bn);  // + masker weights in smem
   c.relu_all = p.relu && !p.relu_inactive_coarse;
   c.am = p.a_tile ? (p.adot_out ? AM_TILE_DOT : AM_TILE) : p.a_box ? AM_BOX : p.a_tma ? AM_G4 : AM_ANY;
   if (pair) {

@@ -126,10 +126,12 @@ struct Smem {
   static constexpr int B_STAGE_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's B rows
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
-  // narrow tiles (BN <= 128, two staging buffers): the epilogue warps form two
-  // groups that finish alternate tiles concurrently (each group its own
+  // narrow tiles (BN <= 128, NSTG staging buffers): the epilogue warps form
+  // NSTG groups that finish consecutive tiles concurrently (each group its own
   // staging buffer and TMEM accumulators), so per-tile epilogue latency overlaps
-  static constexpr int EG = (BN <= 128 && NSTG == 2 && !PAIR) ? 2 : 1;
+  // (BN = 64: four groups of 4 warps, one per staging buffer — small-K convs
+  // are bound by the per-tile epilogue latency, so more tiles finish at once)
+  static constexpr int EG = (BN <= 128 && NSTG >= 2 && !PAIR) ? NSTG : 1;
   static constexpr int NACC = 2 * EG;  // TMEM accumulators in flight
   static constexpr int EW_COLS0 = BN / (NUM_EPI_WARPS / EG / 4);
   // staging rows: 16-byte chunks XOR-swizzled by row when a warp's slice is 8
@@ -631,11 +633,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool plain = kPlain || (staged && !has_scale && !p.ymask_coarse && !p.mdot_w);
     // the whole bias vector lives in smem for the kernel when it fits (the
     // per-warp vector slices are the fallback for scale / masker-dot / lists)
-    const bool cached = kPlain || (!has_scale && !p.mdot_w && p.n_out <= L::VEC_BYTES / 4);
+    const bool cached = kPlain || (!has_scale && !p.mdot_w && (p.n_out + BN - 1) / BN * BN <= L::VEC_BYTES / 4);
     float* const bias_cache = reinterpret_cast<float*>(base + L::VEC_OFF);
     if (cached) {
-      for (int i = threadIdx.x - FIRST_EPI * 32; i < p.n_out; i += NUM_EPI_WARPS * 32)
-        bias_cache[i] = p.bias ? __ldg(p.bias + i) : 0.f;
+      // padded to whole tiles: the plain path reads full warp slices (columns
+      // past n_out are computed but never stored)
+      const int npad = (p.n_out + BN - 1) / BN * BN;
+      for (int i = threadIdx.x - FIRST_EPI * 32; i < npad; i += NUM_EPI_WARPS * 32)
+        bias_cache[i] = (p.bias && i < p.n_out) ? __ldg(p.bias + i) : 0.f;
       asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
     }
 
@@ -724,10 +729,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     uint32_t local = 0;
     int t = next_valid(t_begin);
-    if (grp > 0 && t < tiles) {  // group g starts at the CTA's g-th tile
-      t = next_valid(t + t_step);
-      local = 1;
-    }
+    for (int g = 0; g < grp && t < tiles; ++g) t = next_valid(t + t_step);  // group g starts at the g-th tile
+    local = grp;
     RowInfo cur;
     if (t < tiles) {
       cur = row_info(t, row_raw(t));
@@ -754,7 +757,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       // next tile's rows and vectors: issue the global loads now, use them later
       int tn = next_valid(t + t_step);  // this group's next tile: EG tiles on
-      if (L::EG > 1 && tn < tiles) tn = next_valid(tn + t_step);
+      for (int g = 1; g < L::EG && tn < tiles; ++g) tn = next_valid(tn + t_step);
       RowInfo nxt = cur;
       VecPre vpn;
       int raw_n = 0;

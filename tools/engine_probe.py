@@ -42,6 +42,10 @@ def shape_defs():
     d["pconv_s1"] = dict(kind="patch", n=256, h=56, c=64, s=4)
     d["pconv_s3_b1"] = dict(kind="patch", n=1, h=14, c=256, s=2)
     d["conv3_s1"] = dict(kind="conv3", m=256 * 56 * 56 // 2, n=256, k=64)
+    # RegNetY-1.6GF at batch 1024: the 112x112 stage-1 b0 conv1 (32 -> 48) and a
+    # stage-3 1x1 (336 -> 336) — small-K / small-N streaming convs
+    d["rg_s1_conv1"] = dict(kind="gemm", m=1024 * 112 * 112, n=48, k=32)
+    d["rg_s3_1x1"] = dict(kind="gemm", m=1024 * 196, n=336, k=336)
     # channel skipping at batch 256, stage-3 geometry, k_n = 128 kept channels per sample:
     # conv2 with in-kernel gathered W2[sel] rows (g=1) / plain W2 tiles (g=0, same shape)
     d["chconv2_s3"] = dict(kind="chconv2", n=256, h=14, c=256, k=128, g=1)
