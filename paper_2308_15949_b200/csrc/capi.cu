@@ -1062,7 +1062,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   const bool fork_masker = fork_env && a->aux_stream && masker_computed && mask_cells <= 4096;
   const bool fuse_masker = fuse_env && !fork_masker && a->paradigm == LAUD_PARADIGM_SPATIAL && a->conv1_dense &&
                            !a->given_coarse && !a->dn && !a->fp32 && a->masker_wdiff && a->cell_sums &&
-                           a->x_ld == a->c_in && a->c_in % 64 == 0;
+                           a->x_ld == a->c_in;  // K tail past c_in: zero-filled A, zero weights
   cudaEvent_t fork_done = nullptr;
 
   // ---------------------------------------------------------------- rows

@@ -52,22 +52,30 @@ def check_decisions(x64, masker_w, block, s, bias, got_coarse, tag=""):
     return ties
 
 
-@pytest.mark.parametrize("stage,index,s,n", [(1, 0, 4, 8), (1, 1, 4, 8), (2, 0, 2, 16), (2, 1, 2, 16),
-                                             (3, 0, 2, 32), (3, 1, 2, 32), (4, 0, 1, 32), (4, 1, 1, 32),
-                                             (3, 1, 2, 128)])
-def test_conv1_fused_masker_matches_oracle(stage, index, s, n):
+@pytest.mark.parametrize("arch,stage,index,s,n", [
+    ("resnet101", 1, 0, 4, 8), ("resnet101", 1, 1, 4, 8), ("resnet101", 2, 0, 2, 16), ("resnet101", 2, 1, 2, 16),
+    ("resnet101", 3, 0, 2, 32), ("resnet101", 3, 1, 2, 32), ("resnet101", 4, 0, 1, 32), ("resnet101", 4, 1, 1, 32),
+    ("resnet101", 3, 1, 2, 128),
+    # RegNetY-1.6GF: input widths 32 / 48 / 120 / 336 (not multiples of 64: zero-padded K tails)
+    ("regnety-1.6gf", 1, 0, 4, 8), ("regnety-1.6gf", 2, 1, 4, 16), ("regnety-1.6gf", 3, 1, 2, 32),
+    ("regnety-1.6gf", 4, 1, 1, 32)])
+def test_conv1_fused_masker_matches_oracle(arch, stage, index, s, n):
     """R101 blocks (S = 4/2/1, strided b0 blocks, a CTA-pair-sized conv1 at n=128):
     the conv1-fused masker's decisions and cell list vs the fp64 oracle on the
     same bf16 input; masks bit-identical across two runs."""
     import torch
     from paper_2308_15949_b200 import device as D
-    bp, db = _block("resnet101", stage, index)
+    bp, db = _block(arch, stage, index)
     blk = bp["block"]
     h = blk.input_shape.height
     torch.manual_seed(stage * 100 + index)
     x = torch.randn(n, h, h, db.cin_p, device="cuda").relu_().bfloat16()
     o = blk.output_shape
     nc = n * (o.height // s) * (o.width // s)
+    x64 = _nchw64(x)
+    if arch != "resnet101":  # a bias that splits this block's cells (the fixed 0.37 suits the R101 blocks)
+        dbar, _ = O.masker_margin(x64, bp["masker_w"], blk, s)
+        db.masker_bias = float(-np.median(dbar) + 1e-3)
     masks, lists = [], []
     for _ in range(2):
         ws = D.Workspace()
@@ -79,7 +87,6 @@ def test_conv1_fused_masker_matches_oracle(stage, index, s, n):
     assert np.array_equal(masks[0], masks[1]), "decisions differ between identical runs"
     assert np.array_equal(lists[0], lists[1])
     assert 0.0 < masks[0].mean() < 1.0
-    x64 = _nchw64(x)
     check_decisions(x64, bp["masker_w"], blk, s, db.masker_bias, masks[0], f"s{stage}b{index}")
     np.testing.assert_array_equal(lists[0], np.flatnonzero(masks[0]))
 
