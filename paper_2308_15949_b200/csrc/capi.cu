@@ -412,7 +412,13 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
       a->patch_h == a->patch_w && a->in_h == a->out_h && a->in_w == a->out_w && a->n_out <= 512 &&
       (reinterpret_cast<uintptr_t>(a->act) % 16) == 0 && (long long)a->batch * a->in_h * a->in_w < (1ll << 31) - 1) {
     const int s = a->patch_h;
-    const int hbn = (s == 4 || p.groups > 1) ? 64 : (a->n_out % 128 == 0 ? 128 : 64);
+    static const int gbn_env = [] {  // N tile of the grouped halo conv (tools: A/B)
+      const char* e = getenv("LAUD_PC_GBN");
+      return e ? atoi(e) : 128;
+    }();
+    // grouped: 128-wide N tiles (fewer re-loads of a channel block's halo by the
+    // N tiles whose groups straddle it; measured 18.3 -> 17.7 ms on RegNetY b1024)
+    const int hbn = p.groups > 1 ? gbn_env : (s == 4 ? 64 : (a->n_out % 128 == 0 ? 128 : 64));
     if (patch_conv_supported(s, hbn)) {
       p.a_rows = a->batch * a->in_h * a->in_w;
       int rc;

@@ -79,7 +79,7 @@ struct Cfg {
   static_assert(STAGES >= 2, "shared memory: fewer than two weight stages");
   // split-K partials [S*128 rows][PSTRIDE fp32] reuse the halo + weight stages
   static constexpr int PSTRIDE = BN + 4;  // +16 B: conflict-free row-per-lane float4 stores
-  static_assert(S * 128 * PSTRIDE * 4 <= STG_OFF, "split-K partials must fit the halo + weight region");
+  static constexpr bool SPLIT_OK = S * 128 * PSTRIDE * 4 <= STG_OFF;  // else split-K is not offered
   static_assert(ALLOC <= 227 * 1024, "shared memory budget");
   static_assert(EW_COLS % 16 == 0, "epilogue slice");
 };
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int ncb = p.kpad / 64;  // channel blocks
   // split-K (small grids): the KS CTAs of a cluster share a tile, CTA ks takes
   // channel blocks [cb0, cb1); the host launches one wave (one tile per cluster)
-  const int KS = p.ksplit > 1 ? p.ksplit : 1;
+  const int KS = (L::SPLIT_OK && p.ksplit > 1) ? p.ksplit : 1;
   const int ks = KS > 1 ? (int)cluster_ctarank() : 0;
   const int t_begin = blockIdx.x / KS, t_step = gridDim.x / KS;
   // channel blocks of tile t for this CTA: all of them, or (grouped conv) only
@@ -440,7 +440,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParam
   }
   const int s2 = S * S;
   const long long tiles = ((long long)(p.rows_max / s2) + L::P - 1) / L::P * ((p.n_out + BN - 1) / BN);
-  if (p.ksplit > 1) {  // one wave of clusters, one tile each (host-checked)
+  if (p.ksplit > 1 && L::SPLIT_OK) {  // one wave of clusters, one tile each (host-checked)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(tiles * p.ksplit), 1, 1);
     cfg.blockDim = dim3(THREADS, 1, 1);
@@ -466,7 +466,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParam
 
 // Host dispatch (capi.cu): S in {2, 4}, stride 1, 3x3, n_out <= 512.
 bool patch_conv_supported(int s, int bn) {
-  return (s == 2 && (bn == 128 || bn == 64)) || (s == 4 && bn == 64);
+  return (s == 2 && (bn == 128 || bn == 64)) || (s == 4 && (bn == 64 || bn == 128));
 }
 
 cudaError_t launch_patch_conv(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p, int s, int bn,
@@ -474,6 +474,7 @@ cudaError_t launch_patch_conv(const CUtensorMap& ta, const CUtensorMap& tb, cons
   if (s == 2 && bn == 128) return pc::launch<2, 128>(ta, tb, p, num_sms, stream);
   if (s == 2 && bn == 64) return pc::launch<2, 64>(ta, tb, p, num_sms, stream);
   if (s == 4 && bn == 64) return pc::launch<4, 64>(ta, tb, p, num_sms, stream);
+  if (s == 4 && bn == 128) return pc::launch<4, 128>(ta, tb, p, num_sms, stream);
   return cudaErrorInvalidValue;
 }
 
