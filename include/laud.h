@@ -293,6 +293,11 @@ int laud_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, void* st
  * c < 3; other entries zero); bias fp32 [64]. */
 int laud_stem_pool(const uint8_t* img, int n, int h, int w, const float* mean, const float* inv_std,
                    const void* weight, const float* bias, void* out, void* stream);
+/* Fused RegNet stem: uint8 NHWC 224x224x3 images -> (normalise, 3x3/2 conv,
+ * + bias, ReLU) -> bf16 NHWC [n][112][112][32], one kernel (no im2col).
+ * weight: bf16 [32][3][16], K index kx*4 + c (kx < 3, c < 3; others zero). */
+int laud_stem3(const uint8_t* img, int n, int h, int w, const float* mean, const float* inv_std,
+               const void* weight, const float* bias, void* out, void* stream);
 int laud_global_avgpool(const void* x, int n, int hw, int c, void* y, void* stream);
 
 #ifdef __cplusplus

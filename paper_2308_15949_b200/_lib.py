@@ -93,6 +93,7 @@ _SIGS = {
     "laud_stem_im2col": (C.c_int, [_vp] + [C.c_int] * 6 + [_vp, _vp, _vp, C.c_int, _vp]),
     "laud_maxpool3s2": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "laud_stem_pool": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "laud_stem3": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "laud_global_avgpool": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp]),
 }
 

@@ -47,6 +47,8 @@ cudaError_t launch_stem_im2col(const uint8_t* img, int n, int h, int w, int k, i
                                cudaStream_t s);
 cudaError_t launch_maxpool3s2(const void* x, int n, int h, int w, int c, void* y, cudaStream_t s);
 cudaError_t launch_gap(const void* x, int n, int hw, int c, void* y, cudaStream_t s);
+cudaError_t launch_stem3(const uint8_t* img, int n, const float* mean, const float* inv_std, const void* wpk,
+                         const float* bias, void* out, int num_sms, cudaStream_t s);
 cudaError_t launch_stem_pool(const uint8_t* img, int n, const float* mean, const float* inv_std,
                              const void* wpk, const float* bias, void* out, int num_sms, cudaStream_t s);
 cudaError_t launch_se(void* h2, int n, int c, const int* list, const int* count, int cells_per_img,
@@ -1369,6 +1371,18 @@ int laud_stem_pool(const uint8_t* img, int n, int h, int w, const float* mean, c
   ProfScope ps(3, (cudaStream_t)stream);
   return cuda_check(launch_stem_pool(img, n, mean, inv_std, weight, bias, out, num_sms(), (cudaStream_t)stream),
                     "fused stem", 1);
+}
+
+int laud_stem3(const uint8_t* img, int n, int h, int w, const float* mean, const float* inv_std,
+               const void* weight, const float* bias, void* out, void* stream) {
+  if (!img || !mean || !inv_std || !weight || !bias || !out) return fail(LAUD_ERR_ARG, "null pointer in stem args");
+  if (h != 224 || w != 224) return fail(LAUD_ERR_SHAPE, "fused 3x3 stem: 224x224 images (got %dx%d)", h, w);
+  if (n <= 0) return LAUD_OK;
+  if ((reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(LAUD_ERR_ARG, "fused 3x3 stem: 16-byte aligned weights and output");
+  ProfScope ps(3, (cudaStream_t)stream);
+  return cuda_check(launch_stem3(img, n, mean, inv_std, weight, bias, out, num_sms(), (cudaStream_t)stream),
+                    "fused 3x3 stem", 1);
 }
 
 int laud_global_avgpool(const void* x, int n, int hw, int c, void* y, void* stream) {

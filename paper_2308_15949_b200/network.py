@@ -130,6 +130,13 @@ class LaudNetwork:
             wf[:, :, :7, :3] = ws.transpose(0, 2, 3, 1)  # (co, ky, kx, c)
             wf = np.concatenate([wf.reshape(64, 224), np.zeros((64, 32))], axis=1)
             self.stem_wf = torch.from_numpy(wf).to(device=device, dtype=torch.bfloat16).contiguous()
+        # fused 3x3/2 stem without pool (RegNetY, laud_stem3): weights [32][ky][kx*4 + c]
+        self.stem3_fused = (st.kernel == 3 and st.stride == 2 and not net.stem_pool and st.out_channels == 32
+                            and os.environ.get("LAUD_STEM_FUSED", "1") == "1")
+        if self.stem3_fused:
+            w3 = np.zeros((32, 3, 4, 4))
+            w3[:, :, :3, :3] = ws.transpose(0, 2, 3, 1)  # (co, ky, kx, c)
+            self.stem_wf3 = torch.from_numpy(w3.reshape(32, 48)).to(device=device, dtype=torch.bfloat16).contiguous()
         self.stem_bias = D.fvec(params["stem_b"], st.out_channels, 0.0, device)
         self.mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32, device=device)
         self.inv_std = torch.tensor([1.0 / s for s in IMAGENET_STD], dtype=torch.float32, device=device)
@@ -206,6 +213,11 @@ class LaudNetwork:
             _lib.call("laud_stem_pool", D.ptr(images), n, h, w, D.ptr(self.mean), D.ptr(self.inv_std),
                       D.ptr(self.stem_wf), D.ptr(self.stem_bias), D.ptr(pool), sh)
             return self._blocks_and_head(pool, n, stream, record)
+        if self.stem3_fused and h == 224 and w == 224:
+            stem_out = self._buf("stem", (n, 112, 112, self.stem_c))
+            _lib.call("laud_stem3", D.ptr(images), n, h, w, D.ptr(self.mean), D.ptr(self.inv_std),
+                      D.ptr(self.stem_wf3), D.ptr(self.stem_bias), D.ptr(stem_out), sh)
+            return self._blocks_and_head(stem_out, n, stream, record)
         cols = self._buf("cols", (n * ho * wo, self.stem_cols))
         _lib.call("laud_stem_im2col", D.ptr(images), n, h, w, k, st, pad, D.ptr(self.mean),
                   D.ptr(self.inv_std), D.ptr(cols), self.stem_cols, sh)

@@ -331,3 +331,32 @@ def test_fused_stem_pool_matches_unfused(n):
     y = torch.nn.functional.max_pool2d(y.to(torch.bfloat16).float(), 3, 2, 1).permute(0, 2, 3, 1)
     err = (out.float() - y).norm() / y.norm()
     assert err < 4e-3, float(err)
+
+
+@pytest.mark.parametrize("n", [1, 3, 37])
+def test_fused_stem3_matches_torch(n):
+    """laud_stem3 (RegNet stem: 3x3/2 conv from uint8 images + bias + ReLU, one
+    kernel, im2col-free tcgen05 MMAs on overlapping core matrices) vs a torch fp32
+    reference of the same bf16-rounded normalised inputs and bf16 weights."""
+    from paper_2308_15949_b200 import _lib
+    from paper_2308_15949_b200.network import IMAGENET_MEAN, IMAGENET_STD
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(100 + n)
+    img = torch.randint(0, 256, (n, 224, 224, 3), dtype=torch.uint8, generator=g).cuda()
+    w = (torch.randn(32, 3, 3, 3, generator=g) * 0.2).to(torch.bfloat16).float()
+    b = (torch.randn(32, generator=g) * 0.1).cuda()
+    mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32).cuda()
+    inv = torch.tensor([1.0 / s for s in IMAGENET_STD], dtype=torch.float32).cuda()
+    wf = torch.zeros(32, 3, 4, 4)
+    wf[:, :, :3, :3] = w.permute(0, 2, 3, 1)
+    wf = wf.reshape(32, 48).to(torch.bfloat16).cuda().contiguous()
+    out = torch.empty(n, 112, 112, 32, dtype=torch.bfloat16, device="cuda")
+    _lib.call("laud_stem3", D.ptr(img), n, 224, 224, D.ptr(mean), D.ptr(inv), D.ptr(wf), D.ptr(b), D.ptr(out),
+              D.stream_handle())
+    torch.cuda.synchronize()
+    x = ((img.float() - mean) * inv).to(torch.bfloat16).float().permute(0, 3, 1, 2)
+    y = torch.relu(torch.nn.functional.conv2d(x, w.cuda(), stride=2, padding=1) + b.view(1, -1, 1, 1))
+    y = y.permute(0, 2, 3, 1)
+    err = (out.float() - y).norm() / y.norm()
+    assert err < 4e-3, float(err)
+    assert (out.float() - y).abs().max().item() < 0.05 * y.abs().max().item()
