@@ -277,6 +277,10 @@ int pick_bn(int n_out, int k, long long rows) {
   if (small_env && mt * ((n_out + 63) / 64) <= num_sms()) return 64;
   if (small_env && mt * ((n_out + 127) / 128) <= num_sms()) return 128;
   if (n_out <= 128) return 128;
+  // widths that 256-wide tiles pad badly (RegNet 336: 512 computed columns vs
+  // 384 with 128-wide tiles) take 128-wide tiles
+  const int pad256 = (n_out + 255) / 256 * 256, pad128 = (n_out + 127) / 128 * 128;
+  if ((pad256 - pad128) * 10 > n_out) return 128;
   return 256;  // measured best for every R101 conv shape at batch 256 (tools/sweep_cfg.sh)
 }
 
