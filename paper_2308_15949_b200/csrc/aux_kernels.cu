@@ -143,16 +143,17 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int hw, int c,
 }
 
 // EXT squeeze-excitation on conv2's compact output rows h2 [rows][c] (bf16,
-// in place), two launches:
+// in place), four launches:
 //  se_pool_kernel (one CTA per sample n): its rows [r0, r1) — its active
 //    patches (patch list sorted by cell, `cells_per_img` cells per image,
 //    `rows_per_cell` rows each; found by a block-wide k-ary search) or, with
 //    list == nullptr, its dense pixel block — averaged into means[n][c]; the
 //    row range goes to rr[n].
-//  se_fc_scale_kernel (one CTA per SE_SPB samples): gate = sigmoid(W2 relu(W1
-//    mean + b1) + b2) with each weight row read once for SE_SPB samples, then
-//    h2 *= gate over those samples' rows (bf16 RNE) — the oracle EXT
-//    (`laud_oracle._se_scale`).
+//  se_fc1_kernel / se_fc2_kernel (SE_SPB samples x an output chunk per CTA):
+//    gate = sigmoid(W2 relu(W1 mean + b1) + b2), each weight row read once per
+//    SE_SPB samples;
+//  se_scale_kernel: h2 *= gate over each sample's rows (bf16 RNE) — the oracle
+//    EXT (`laud_oracle._se_scale`).
 constexpr int SE_SPB = 16;
 
 __global__ void __launch_bounds__(256) se_pool_kernel(const __nv_bfloat16* __restrict__ h2, int c,
@@ -233,57 +234,82 @@ __global__ void __launch_bounds__(256) se_pool_kernel(const __nv_bfloat16* __res
   for (int i = tid; i < c; i += blockDim.x) means[(size_t)n * c + i] = mean[i] * inv;
 }
 
-__global__ void __launch_bounds__(256) se_fc_kernel(int n, int c, const float* __restrict__ means,
-                                                    const float* __restrict__ w1,
-                                                    const float* __restrict__ b1, int hs,
-                                                    const float* __restrict__ w2,
-                                                    const float* __restrict__ b2, float* __restrict__ gates) {
+// The SE FC layers as two launches with grids over (sample groups x output
+// chunks), so the GPU fills at batch 1024 (one CTA per 16 samples left 64 CTAs
+// on 148 SMs): fc1 = relu(W1 mean + b1) -> hidden [n][hs], fc2 = sigmoid(W2
+// hidden + b2) -> gates [n][c].  Per output, the FMAs run in the order of the
+// oracle EXT's reductions (sequential over the input index).
+__global__ void __launch_bounds__(256) se_fc1_kernel(int n, int c, const float* __restrict__ means,
+                                                     const float* __restrict__ w1, const float* __restrict__ b1,
+                                                     int hs, float* __restrict__ hidden) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ float sm[];
-  float* mean = sm;                  // [SE_SPB][c]
-  float* hid = mean + SE_SPB * c;    // [SE_SPB][hs]
+  extern __shared__ float mean[];  // [SE_SPB][c]
   const int s0 = blockIdx.x * SE_SPB;
   const int ns = min(SE_SPB, n - s0);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < SE_SPB * c; i += blockDim.x)
-    mean[i] = i / c < ns ? means[(size_t)s0 * c + i] : 0.f;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < SE_SPB * c; i += blockDim.x) mean[i] = i / c < ns ? means[(size_t)s0 * c + i] : 0.f;
   __syncthreads();
-  // thread per output unit for all SE_SPB samples of the CTA: every weight is
-  // loaded once per CTA and feeds SE_SPB FMAs (means / hidden in smem)
-  for (int jj = tid; jj < hs; jj += blockDim.x) {  // hidden = relu(W1 mean + b1)
-    float a[SE_SPB];
-#pragma unroll
-    for (int q = 0; q < SE_SPB; ++q) a[q] = 0.f;
-    const float4* wr = reinterpret_cast<const float4*>(w1 + (size_t)jj * c);
-#pragma unroll 2
-    for (int i = 0; i < c / 4; ++i) {
-      const float4 wv = __ldg(wr + i);
-#pragma unroll
-      for (int q = 0; q < SE_SPB; ++q) {
-        const float4 mv = reinterpret_cast<const float4*>(mean + q * c)[i];
-        a[q] = fmaf(wv.x, mv.x, fmaf(wv.y, mv.y, fmaf(wv.z, mv.z, fmaf(wv.w, mv.w, a[q]))));
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < SE_SPB; ++q) hid[q * hs + jj] = fmaxf(a[q] + b1[jj], 0.f);
-  }
-  __syncthreads();
-  for (int ii = tid; ii < c; ii += blockDim.x) {  // gate = sigmoid(W2 hidden + b2)
-    float a[SE_SPB];
-#pragma unroll
-    for (int q = 0; q < SE_SPB; ++q) a[q] = 0.f;
-    const float* wr = w2 + (size_t)ii * hs;
+  const int u = blockIdx.y * 32 + (tid & 31);  // hidden unit
+  const int q0 = (tid >> 5) * 2;               // two samples per thread
+  if (u >= hs) return;
+  float a0 = 0.f, a1 = 0.f;
+  const float4* wr = reinterpret_cast<const float4*>(w1 + (size_t)u * c);
 #pragma unroll 4
-    for (int jj = 0; jj < hs; ++jj) {
-      const float wv = __ldg(wr + jj);
-#pragma unroll
-      for (int q = 0; q < SE_SPB; ++q) a[q] = fmaf(wv, hid[q * hs + jj], a[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < SE_SPB; ++q)
-      if (q < ns) gates[(size_t)(s0 + q) * c + ii] = 1.f / (1.f + __expf(-(a[q] + b2[ii])));
+  for (int i = 0; i < c / 4; ++i) {
+    const float4 wv = __ldg(wr + i);
+    const float4 m0 = reinterpret_cast<const float4*>(mean + q0 * c)[i];
+    const float4 m1 = reinterpret_cast<const float4*>(mean + (q0 + 1) * c)[i];
+    a0 = fmaf(wv.x, m0.x, fmaf(wv.y, m0.y, fmaf(wv.z, m0.z, fmaf(wv.w, m0.w, a0))));
+    a1 = fmaf(wv.x, m1.x, fmaf(wv.y, m1.y, fmaf(wv.z, m1.z, fmaf(wv.w, m1.w, a1))));
   }
+  if (q0 < ns) hidden[(size_t)(s0 + q0) * hs + u] = fmaxf(a0 + b1[u], 0.f);
+  if (q0 + 1 < ns) hidden[(size_t)(s0 + q0 + 1) * hs + u] = fmaxf(a1 + b1[u], 0.f);
+}
+
+__global__ void __launch_bounds__(256) se_fc2_kernel(int n, int c, const float* __restrict__ hidden,
+                                                     const float* __restrict__ w2, const float* __restrict__ b2,
+                                                     int hs, float* __restrict__ gates) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float hid[];  // [SE_SPB][hs]
+  const int s0 = blockIdx.x * SE_SPB;
+  const int ns = min(SE_SPB, n - s0);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < SE_SPB * hs; i += blockDim.x) hid[i] = i / hs < ns ? hidden[(size_t)s0 * hs + i] : 0.f;
+  __syncthreads();
+  const int o = blockIdx.y * 128 + (tid & 127);  // output channel
+  const int q0 = (tid >> 7) * (SE_SPB / 2);      // half of the samples per thread
+  if (o >= c) return;
+  float a[SE_SPB / 2];
+#pragma unroll
+  for (int q = 0; q < SE_SPB / 2; ++q) a[q] = 0.f;
+  const float* wr = w2 + (size_t)o * hs;
+#pragma unroll 4
+  for (int jj = 0; jj < hs; ++jj) {
+    const float wv = __ldg(wr + jj);
+#pragma unroll
+    for (int q = 0; q < SE_SPB / 2; ++q) a[q] = fmaf(wv, hid[(q0 + q) * hs + jj], a[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < SE_SPB / 2; ++q)
+    if (q0 + q < ns) gates[(size_t)(s0 + q0 + q) * c + o] = 1.f / (1.f + __expf(-(a[q] + b2[o])));
+}
+
+static cudaError_t launch_se_fc(int n, int c, const float* means, const float* w1, const float* b1, int hs,
+                                const float* w2, const float* b2, float* hidden, float* gates, cudaStream_t s) {
+  const size_t sm1 = (size_t)SE_SPB * c * sizeof(float);
+  static size_t configured = 0;
+  if (sm1 > 48 * 1024 && sm1 > configured) {
+    cudaError_t e = cudaFuncSetAttribute(se_fc1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    if (e != cudaSuccess) return e;
+    configured = sm1;
+  }
+  const int sg = (n + SE_SPB - 1) / SE_SPB;
+  launch_k(se_fc1_kernel, dim3(sg, (hs + 31) / 32), dim3(256), sm1, s, n, c, means, w1, b1, hs, hidden);
+  launch_k(se_fc2_kernel, dim3(sg, (c + 127) / 128), dim3(256), (size_t)SE_SPB * hs * sizeof(float), s, n, c,
+           (const float*)hidden, w2, b2, hs, gates);
+  return cudaSuccess;
 }
 
 // h2 *= gate[sample of the row], elementwise over all rows (16-byte chunks)
@@ -325,15 +351,9 @@ cudaError_t launch_se(void* h2, int n, int c, const int* list, const int* count,
   launch_k(se_pool_kernel, dim3(n), dim3(256), (size_t)c * (1 + se_groups) * sizeof(float), s,
            reinterpret_cast<const __nv_bfloat16*>(h2), c, list, count, cells_per_img, rows_per_cell,
            rows_per_img, means, rr);
-  const size_t smem = (size_t)SE_SPB * (c + hs) * sizeof(float);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(se_fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  launch_k(se_fc_kernel, dim3((n + SE_SPB - 1) / SE_SPB), dim3(256), smem, s, n, c, means, w1, b1, hs, w2,
-           b2, gates);
+  float* hidden = reinterpret_cast<float*>(rr + n + 2);
+  cudaError_t e = launch_se_fc(n, c, means, w1, b1, hs, w2, b2, hidden, gates, s);
+  if (e != cudaSuccess) return e;
   const int rows_max = list ? n * cells_per_img * rows_per_cell : n * rows_per_img;
   const long long work = (long long)rows_max * (c / 8);
   const int blocks = (int)((work + 255) / 256 < 148 * 16 ? (work + 255) / 256 : 148 * 16);
@@ -442,13 +462,9 @@ cudaError_t launch_se_channel(void* h2, int n, int c, int hw, int sr, const int*
   const int ch_groups = ((c + 7) / 8) <= 256 ? 256 / ((c + 7) / 8) : 1;
   launch_k(se_pool_ch_kernel, dim3(n), dim3(256), (size_t)c * (1 + ch_groups) * sizeof(float), s,
            reinterpret_cast<const __nv_bfloat16*>(h2), c, hw, sr, sel, count, means);
-  const size_t smem = (size_t)SE_SPB * (c + hs) * sizeof(float);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(se_fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  launch_k(se_fc_kernel, dim3((n + SE_SPB - 1) / SE_SPB), dim3(256), smem, s, n, c, means, w1, b1, hs, w2,
-           b2, gates);
+  float* hidden = gates + (((size_t)n * c + 3) & ~(size_t)3);
+  cudaError_t e = launch_se_fc(n, c, means, w1, b1, hs, w2, b2, hidden, gates, s);
+  if (e != cudaSuccess) return e;
   const long long work = (long long)n * hw * (c / 8);
   const int blocks = (int)((work + 255) / 256 < 148 * 16 ? (work + 255) / 256 : 148 * 16);
   launch_k(se_scale_ch_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s,
