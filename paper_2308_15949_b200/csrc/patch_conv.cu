@@ -158,6 +158,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   // (the block-diagonal weights are zero elsewhere); split-K takes a slice
   auto cb_range = [&](int t, int& b0, int& b1) {
     int lo = 0, hi = ncb;
+    if (p.groups == 1 && KS == 1) {  // the common case: every channel block
+      b0 = 0;
+      b1 = ncb;
+      return;
+    }
     if (p.groups > 1) {
       const int n0 = (t % n_tiles) * BN;
       const int g0 = n0 / p.gw_out;
