@@ -1,5 +1,10 @@
 """Small spatial / channel / layer / static block forwards for compute-sanitizer
-(memcheck, racecheck, synccheck): python tools/sanitize_block.py"""
+(memcheck, racecheck, synccheck): python tools/sanitize_block.py
+
+Round 2 adds: the small-grid cluster split-K of the halo conv2 (latency_split),
+the masker forked onto a second stream, the grouped halo conv2 (RegNet), the
+gathered-weight channel schedule (LAUD_CH_GATHER=1), both fused stems and the
+split SE FC kernels."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -24,6 +29,8 @@ def main():
         x = torch.randn(n, h, h, db.cin_p, device="cuda").relu_().bfloat16()
         for dense in (False, True):
             db.forward(x.clone(), "spatial", s, conv1_dense=dense)
+        aux = torch.cuda.Stream()
+        db.forward(x[:1].clone(), "spatial", s, conv1_dense=True, aux_stream=aux, latency_split=True)
         db.forward(x.clone(), "static")
         db.forward(x.clone(), "layer", coarse=torch.tensor([1, 0], dtype=torch.uint8, device="cuda"))
         db.enable_grouped_channel()  # EXT for grouped conv2 (no-op otherwise)
@@ -35,8 +42,20 @@ def main():
         cm8 = torch.zeros(n8 * db.cmid_p, dtype=torch.uint8, device="cuda")
         cm8[::3] = 1
         db.forward(x8, "channel", chmask=cm8)
+        if blk.conv2.groups == 1:
+            os.environ["LAUD_CH_GATHER"] = "1"  # gathered-weight schedule (read per call)
+            db.forward(x8, "channel", chmask=cm8)
+            os.environ["LAUD_CH_GATHER"] = "0"
         torch.cuda.synchronize()
         print("ok", arch, stage, index, flush=True)
+    # fused stems (ResNet 7x7/2 + pool, RegNet 3x3/2) through the network glue
+    from paper_2308_15949_b200.network import LaudNetwork
+    for arch in ("resnet50", "regnety-1.6gf"):
+        net = LaudNetwork(arch, "spatial", "4-4-2-1", 0.5, seed=0)
+        img = torch.randint(0, 256, (2, 224, 224, 3), dtype=torch.uint8, device="cuda")
+        net.forward(img)
+        torch.cuda.synchronize()
+        print("ok network", arch, flush=True)
 
 
 if __name__ == "__main__":
