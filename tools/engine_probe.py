@@ -41,6 +41,12 @@ def shape_defs():
     d["pconv_s2"] = dict(kind="patch", n=256, h=28, c=128, s=2)
     d["pconv_s1"] = dict(kind="patch", n=256, h=56, c=64, s=4)
     d["pconv_s3_b1"] = dict(kind="patch", n=1, h=14, c=256, s=2)
+    # every cell active: the halo kernel as a dense 3x3 conv (vs conv2_s1 / conv2_s2 / conv2_s3)
+    d["pconv_s1_all"] = dict(kind="patch", n=256, h=56, c=64, s=4, density=1.0)
+    d["pconv_s1_all_s2"] = dict(kind="patch", n=256, h=56, c=64, s=2, density=1.0)
+    d["pconv_s2_all"] = dict(kind="patch", n=256, h=28, c=128, s=2, density=1.0)
+    d["pconv_s2_all_s4"] = dict(kind="patch", n=256, h=28, c=128, s=4, density=1.0)
+    d["pconv_s3_all"] = dict(kind="patch", n=256, h=14, c=256, s=2, density=1.0)
     d["conv3_s1"] = dict(kind="conv3", m=256 * 56 * 56 // 2, n=256, k=64)
     # RegNetY-1.6GF at batch 1024: the 112x112 stage-1 b0 conv1 (32 -> 48) and a
     # stage-3 1x1 (336 -> 336) — small-K / small-N streaming convs
@@ -74,7 +80,8 @@ def run(name, spec, flush, reps=20):
         a = bf(b, h, h, c)
         w = bf(c, 9, c)
         hc = h // s
-        cells = np.sort(np.random.default_rng(0).permutation(b * hc * hc)[: b * hc * hc // 2]).astype(np.int32)
+        keep = int(round(spec.get("density", 0.5) * b * hc * hc))
+        cells = np.sort(np.random.default_rng(0).permutation(b * hc * hc)[:keep]).astype(np.int32)
         lst = torch.from_numpy(cells).cuda()
         cnt = torch.tensor([len(cells)], dtype=torch.int32, device="cuda")
         m = len(cells) * s * s
