@@ -296,6 +296,32 @@ cudaEvent_t fork_event(int i) {
   return ev[i];
 }
 
+// Device list 0, 1, ..., items-1 (every cell of a grid active), built once per
+// length outside graph capture and cached; nullptr when it would have to be
+// allocated during a capture (the caller then keeps its dense schedule).
+const int* identity_list(int items, cudaStream_t st) {
+  static std::mutex mu;
+  static std::unordered_map<long long, int*> lists;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const long long key = ((long long)dev << 40) | (long long)items;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = lists.find(key);
+  if (it != lists.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  std::vector<int> h(items);
+  for (int i = 0; i < items; ++i) h[i] = i;
+  int* d = nullptr;
+  if (cudaMalloc(&d, (size_t)items * sizeof(int)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), (size_t)items * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  lists[key] = d;
+  return d;
+}
+
 // fused masker dots riding on a dense 1x1 conv (ConvParams::adot_*)
 struct AdotArgs {
   const float* w;
@@ -1146,6 +1172,30 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   } else {
     return fail(LAUD_ERR_ARG, "unknown paradigm %d", a->paradigm);
   }
+  // Static blocks run conv2 on the halo kernel too (every S x S cell active:
+  // an identity cell list), measured faster than the gathered-row dense conv2
+  // at every R101 stage (tools/engine_probe.py conv2_s* vs pconv_s*_all); the
+  // K order is the same, so the outputs are bitwise those of the dense path.
+  int pm2 = pm;  // row mode of conv2 / conv3
+  {
+    static const int sh_env = [] {
+      const char* e = getenv("LAUD_STATIC_HALO");
+      return e ? atoi(e) : 1;
+    }();
+    const int sh = a->c_mid <= 64 ? 4 : 2;
+    if (sh_env && pm == ROWS_DENSE && !a->fp32 && a->stride == 1 && ho % sh == 0 && wo % sh == 0 &&
+        a->c_mid <= 512 && a->c_mid % 8 == 0) {
+      const int* iota = identity_list(n * (ho / sh) * (wo / sh), st);
+      if (iota) {
+        pm2 = ROWS_PATCH;
+        ph = pw = sh;
+        ch = ho / sh;
+        cw = wo / sh;
+        cells = iota;
+        cells_n = nullptr;
+      }
+    }
+  }
 
   // ---------------------------------------------------------------- conv1
   laud_conv_args c1;
@@ -1278,7 +1328,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   laud_conv_args c2;
   memset(&c2, 0, sizeof(c2));
   c2.fp32 = a->fp32;
-  c2.row_mode = pm;
+  c2.row_mode = pm2;
   c2.list = cells;
   c2.count = cells_n;
   c2.rows_max = n * ho * wo;
