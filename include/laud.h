@@ -151,6 +151,10 @@ typedef struct laud_conv_args {
    * summation order than the unsplit conv, so off by default (the mirror API
    * keeps sparse == dense-masked bitwise); the network executor enables it. */
   int latency_split;
+  /* > 1 (ROWS_PATCH): each list entry e stands for the list_expand cells
+   * e*k .. e*k+k-1 (k = list_expand) and the device count scales by k — a
+   * layer block's active-sample list read as its samples' S x S cells. */
+  int list_expand;
 } laud_conv_args;
 
 int laud_conv(const laud_conv_args* a, void* stream);

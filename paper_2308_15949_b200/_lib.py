@@ -40,7 +40,7 @@ class ConvArgs(C.Structure):
         ("col_index", _vp), ("col_index_ld", C.c_int), ("mdot_w", _vp), ("mdot_out", _vp),
         ("misplace_first", C.c_int), ("groups", C.c_int), ("fp32", C.c_int),
         ("b_gather", C.c_int), ("b_index", _vp), ("b_index_ld", C.c_int), ("b_rows", C.c_int),
-        ("latency_split", C.c_int),
+        ("latency_split", C.c_int), ("list_expand", C.c_int),
     ]
 
 

@@ -398,6 +398,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
   p.b_batched = a->b_batched;
   p.col_index = a->col_index;
   p.col_index_ld = a->col_index_ld;
+  p.list_expand = a->row_mode == ROWS_PATCH && a->list_expand > 1 ? a->list_expand : 0;
   p.b_gather = a->b_gather;
   p.b_index = a->b_index;
   p.b_index_ld = a->b_index_ld;
@@ -1351,6 +1352,22 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c2.n_out = a->c_mid;
   c2.groups = a->groups;
   c2.latency_split = a->latency_split;
+  // layer blocks (stride 1): conv2 / conv3 over the active samples' S x S
+  // cells (the sample list expanded in the kernels) so conv2 runs on the halo
+  // kernel instead of whole-image gathered rows; same K order, same result
+  static const int lh_env = [] {
+    const char* e = getenv("LAUD_LAYER_HALO");
+    return e ? atoi(e) : 1;
+  }();
+  if (lh_env && a->paradigm == LAUD_PARADIGM_LAYER && a->stride == 1 && !a->fp32) {
+    const int sl = a->c_mid <= 64 ? 4 : 2;
+    if (ho % sl == 0 && wo % sl == 0) {
+      c2.patch_h = c2.patch_w = sl;
+      c2.cells_h = ho / sl;
+      c2.cells_w = wo / sl;
+      c2.list_expand = (ho / sl) * (wo / sl);
+    }
+  }
   c2.scale = a->s2;
   c2.bias = a->b2;
   c2.relu = a->relu2;

@@ -54,7 +54,8 @@ __device__ __forceinline__ int row_fetch(const ConvParams& p, int m) {
     idx = m;
     lim = p.rows_max - 1;
   }
-  return __ldg(p.list + min(idx, lim));  // unconditional: consumed later
+  idx = min(idx, lim);  // unconditional: consumed later
+  return p.row_mode == ROWS_PATCH ? list_cell(p, idx) : __ldg(p.list + idx);
 }
 __device__ __forceinline__ bool map_row_raw(const ConvParams& p, int m, int nvalid, int raw, RowPos& o,
                                             bool& first_patch) {
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int bn_ = p.batch, by = 0, bx = 0;  // invalid patch -> image index past the end (zeros)
         const int pi = ti.m0 / s2 + tid;
         if (tid < ppt && pi * s2 < nvalid) {
-          const int cell = __ldg(p.list + pi);
+          const int cell = list_cell(p, pi);
           bn_ = cell / cpi;
           const int cr = cell - bn_ * cpi;
           const int ci = cr / p.cells_w, cj = cr - (cr / p.cells_w) * p.cells_w;

@@ -22,6 +22,8 @@ struct ConvParams {
   // ---- rows (output pixels)
   int row_mode;          // RowMode
   const int* list;       // patch list (cell index) or pixel list (pixel index)
+  int list_expand;       // > 1: each list entry e stands for cells e*k .. e*k+k-1 (k = list_expand;
+                         // layer blocks: a sample list read as its S x S cells), count scales by k
   const int* count;      // device count of list entries; nullptr -> use rows_max
   int rows_max;          // upper bound on rows (grid sizing)
   int batch;             // N

@@ -11,9 +11,19 @@ struct RowPos {
   int pix;  // linear output pixel (n*out_h + y)*out_w + x
 };
 
+// cell of patch-list position idx (list_expand: an entry covers list_expand cells)
+__device__ __forceinline__ int list_cell(const ConvParams& p, int idx) {
+  if (p.list_expand > 1) {
+    const int e = idx / p.list_expand;
+    return __ldg(p.list + e) * p.list_expand + (idx - e * p.list_expand);
+  }
+  return __ldg(p.list + idx);
+}
+
 __device__ __forceinline__ int rows_valid(const ConvParams& p) {
   if (p.row_mode == ROWS_DENSE || p.count == nullptr) return p.rows_max;
   int c = __ldg(p.count);
+  if (p.list_expand > 1) c *= p.list_expand;
   long long r = (p.row_mode == ROWS_PATCH) ? (long long)c * p.patch_h * p.patch_w : (long long)c;
   return r < p.rows_max ? (int)r : p.rows_max;
 }
@@ -28,7 +38,7 @@ __device__ __forceinline__ bool map_row(const ConvParams& p, int m, int nvalid, 
     int s2 = p.patch_h * p.patch_w;
     int pi = m / s2;
     int l = m - pi * s2;
-    int cell = __ldg(p.list + pi);
+    int cell = list_cell(p, pi);
     int cpi = p.cells_h * p.cells_w;
     o.n = cell / cpi;
     int c = cell - o.n * cpi;

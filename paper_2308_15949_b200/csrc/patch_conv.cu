@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int s2 = S * S;
-  const int count = p.count ? min(__ldg(p.count), p.rows_max / s2) : p.rows_max / s2;  // active patches
+  const int count = p.count ? min(__ldg(p.count) * max(p.list_expand, 1), p.rows_max / s2)
+                            : p.rows_max / s2;  // active patches
   const int n_tiles = (p.n_out + BN - 1) / BN;
   const int m_tiles = (count + P - 1) / P;
   const int tiles = m_tiles * n_tiles;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         pv[j] = issuer && pi < count;
         pn[j] = 0, py[j] = 0, px[j] = 0;
         if (pv[j]) {
-          const int cell = __ldg(p.list + pi);
+          const int cell = list_cell(p, pi);
           pn[j] = cell / cpi;
           const int cr = cell - pn[j] * cpi;
           const int ci = cr / p.cells_w;
