@@ -440,7 +440,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
   }();
   if (halo_env && !ad && a->row_mode == ROWS_PATCH && a->ksize == 3 && a->stride == 1 && a->pad == 1 &&
       (p.groups == 1 || (halo_env & 2)) && !a->a_compact && !a->sample_rows && !a->chan_count && !a->b_batched &&
-      a->out_mode == OUT_ROW && !a->resid && !a->ymask_coarse && !a->ymask_channel && !a->mdot_w &&
+      a->out_mode == OUT_ROW && !a->resid && !a->ymask_coarse && !a->mdot_w &&
       !a->relu_inactive_coarse && !a->out_f32 && !a->col_index && !a->misplace_first &&
       a->patch_h == a->patch_w && a->in_h == a->out_h && a->in_w == a->out_w && a->n_out <= 512 &&
       (reinterpret_cast<uintptr_t>(a->act) % 16) == 0 && (long long)a->batch * a->in_h * a->in_w < (1ll << 31) - 1) {
@@ -934,6 +934,22 @@ static int channel_forward(const laud_block_args* a, cudaStream_t st) {
     c2.relu = a->relu2;
     c2.out_mode = OUT_ROW;
     c2.out = a->h2;
+    // conv2 (stride 1) on the halo kernel over an identity cell list, the channel
+    // mask in its epilogue; conv3 reads h2 in the same patch order
+    if (!a->fp32 && a->stride == 1) {
+      const int sc = cmp <= 64 ? 4 : 2;
+      if (ho % sc == 0 && wo % sc == 0 && cmp <= 512) {
+        const int* iota = identity_list(n * (ho / sc) * (wo / sc), st);
+        if (iota) {
+          c2.row_mode = ROWS_PATCH;
+          c2.list = iota;
+          c2.count = nullptr;
+          c2.patch_h = c2.patch_w = sc;
+          c2.cells_h = ho / sc;
+          c2.cells_w = wo / sc;
+        }
+      }
+    }
     if ((rc = run_conv(&c2, st))) return rc;
     if (a->se_w1) {  // EXT SE on the dense-masked h2 (dropped channels pool to zero)
       if ((rc = cuda_check(launch_se(a->h2, n, cmp, nullptr, nullptr, 1, 1, ho * wo, a->se_w1, a->se_b1,

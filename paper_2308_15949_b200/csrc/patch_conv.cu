@@ -334,6 +334,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int nch = max(0, min(EW, p.n_out - c_base));
       const int pi = mt * P + pl;
       const bool valid = pi < count;
+      // dense-masked channel schedule: this row's sample keeps / drops each channel
+      const uint8_t* cmask = (p.ymask_channel && valid)
+                                 ? p.ymask_channel + (size_t)(list_cell(p, pi) / (p.cells_h * p.cells_w)) * p.n_out
+                                 : nullptr;
       mbar_wait(&acc_full[buf], (local / L::NBUF) & 1);
       tc_fence_after();
       for (int ly = 0; ly < S; ++ly) {
@@ -347,10 +351,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int g = 0; g < CH / 8; ++g) {
             const int cl = j * CH + g * 8;
             float v[8];
+            uint2 mk = make_uint2(0xffffffffu, 0xffffffffu);
+            if (cmask && c_base + cl < p.n_out) mk = __ldg(reinterpret_cast<const uint2*>(cmask + c_base + cl));
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int c = c_base + cl + e;
               v[e] = fmaf(__uint_as_float(r[g * 8 + e]), vsc[c], vbi[c]);
+              if (!(((e < 4 ? (mk.x >> (8 * e)) : (mk.y >> (8 * (e - 4)))) & 0xff))) v[e] = 0.f;
               if (p.relu) v[e] = fmaxf(v[e], 0.f);
             }
             uint4 w;
