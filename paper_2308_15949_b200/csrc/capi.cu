@@ -451,7 +451,11 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     }();
     // grouped: 128-wide N tiles (fewer re-loads of a channel block's halo by the
     // N tiles whose groups straddle it; measured 18.3 -> 17.7 ms on RegNetY b1024)
-    const int hbn = p.groups > 1 ? gbn_env : (s == 4 ? 64 : (a->n_out % 128 == 0 ? 128 : 64));
+    static const int pbn_env = [] {  // N tile of the ungrouped S = 2 halo conv (tools: A/B)
+      const char* e = getenv("LAUD_PC_BN");
+      return e ? atoi(e) : 128;
+    }();
+    const int hbn = p.groups > 1 ? gbn_env : (s == 4 ? 64 : (a->n_out % 128 == 0 ? pbn_env : 64));
     if (patch_conv_supported(s, hbn)) {
       p.a_rows = a->batch * a->in_h * a->in_w;
       int rc;
