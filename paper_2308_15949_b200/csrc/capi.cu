@@ -478,6 +478,12 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
             p.ksplit = k;
             break;
           }
+      // larger grids: split only the last partial wave's tiles over 2-CTA clusters
+      static const int tail_env = [] {
+        const char* e = getenv("LAUD_TAIL_SPLIT");
+        return e ? atoi(e) : 1;
+      }();
+      p.tail_split = (tail_env && a->latency_split && p.groups == 1 && p.ksplit == 1 && ncb % 2 == 0) ? 1 : 0;
       ProfScope ps(0, st, a->count);
       if (ps.on) {
         ps.rec.rows_per_count = (long long)s * s;

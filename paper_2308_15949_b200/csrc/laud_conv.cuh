@@ -93,6 +93,7 @@ struct ConvParams {
   //      ksplit CTAs of a cluster take disjoint channel-block ranges of one
   //      tile; fp32 partials are reduced through distributed shared memory
   int ksplit;
+  int tail_split;          // halo conv, large grids: the last partial wave's tiles split over 2-CTA clusters
   // ---- masker-conv3 fusion: mdot_out[cell(row)] += dot(bf16 output row, mdot_w)
   const float* mdot_w;
   float* mdot_out;

@@ -149,21 +149,50 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int m_tiles = (count + P - 1) / P;
   const int tiles = m_tiles * n_tiles;
   const int ncb = p.kpad / 64;  // channel blocks
-  // split-K (small grids): the KS CTAs of a cluster share a tile, CTA ks takes
-  // channel blocks [cb0, cb1); the host launches one wave (one tile per cluster)
+  // Work schedule.  Items are (tile, part): a part item is a split-K slice of a
+  // tile shared by the CTAs of a cluster (fp32 partials reduced through DSMEM
+  // after the role loops).
+  //  * small grids (ksplit = KS > 1): every tile split KS ways, one wave;
+  //  * tail split (clusters of 2): whole tiles round-robin over the CTAs for
+  //    the complete waves, then the last partial wave's tiles (at most one per
+  //    cluster) split over the cluster's 2 CTAs — the tail costs half a tile
+  //    instead of a whole one (e.g. 196 tiles on 148 SMs: 1.5 instead of 2);
+  //  * otherwise whole tiles round-robin.
   const int KS = (L::SPLIT_OK && p.ksplit > 1) ? p.ksplit : 1;
-  const int ks = KS > 1 ? (int)cluster_ctarank() : 0;
+  const bool tail = L::SPLIT_OK && KS == 1 && p.tail_split;
+  const int ks = (KS > 1 || tail) ? (int)cluster_ctarank() : 0;
+  const int NP = KS > 1 ? KS : 2;  // parts of a split tile
   const int t_begin = blockIdx.x / KS, t_step = gridDim.x / KS;
-  // channel blocks of tile t for this CTA: all of them, or (grouped conv) only
-  // those holding the input channels of the groups the tile's N range spans
-  // (the block-diagonal weights are zero elsewhere); split-K takes a slice
-  auto cb_range = [&](int t, int& b0, int& b1) {
-    int lo = 0, hi = ncb;
-    if (p.groups == 1 && KS == 1) {  // the common case: every channel block
-      b0 = 0;
-      b1 = ncb;
-      return;
+  int F = tiles, split_t = -1;
+  if (tail) {
+    const int n_cta = gridDim.x, rounds = tiles / n_cta, R = tiles - rounds * n_cta;
+    if (R > 0 && R <= n_cta / 2) {
+      F = rounds * n_cta;
+      split_t = (int)blockIdx.x / 2 < R ? F + (int)blockIdx.x / 2 : -1;
     }
+  }
+  const int nfull = F > (int)blockIdx.x ? (F - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto work = [&](int k, int& t, bool& part) -> bool {
+    if (KS > 1) {
+      t = t_begin + k * t_step;
+      part = true;
+      return t < tiles;
+    }
+    if (k < nfull) {
+      t = blockIdx.x + k * gridDim.x;
+      part = false;
+      return true;
+    }
+    t = split_t;
+    part = true;
+    return k == nfull && split_t >= 0;
+  };
+  // channel blocks of item (t, part) for this CTA: all of them, or (grouped
+  // conv) only those holding the input channels of the groups the tile's N
+  // range spans (the block-diagonal weights are zero elsewhere); a part item
+  // takes this CTA's slice
+  auto cb_range = [&](int t, bool part, int& b0, int& b1) {
+    int lo = 0, hi = ncb;
     if (p.groups > 1) {
       const int n0 = (t % n_tiles) * BN;
       const int g0 = n0 / p.gw_out;
@@ -171,8 +200,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       lo = (g0 * p.gw_in) / 64;
       hi = (g1 * p.gw_in + 63) / 64;
     }
-    b0 = lo + ks * (hi - lo) / KS;
-    b1 = lo + (ks + 1) * (hi - lo) / KS;
+    if (!part) {
+      b0 = lo;
+      b1 = hi;
+      return;
+    }
+    b0 = lo + ks * (hi - lo) / NP;
+    b1 = lo + (ks + 1) * (hi - lo) / NP;
   };
 
   if (warp < NUM_PROD) {
@@ -186,7 +220,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int quad = op % (P / 4);  // 4 patches p = 4*quad .. 4*quad+3
     const int cpi = p.cells_h * p.cells_w;
     uint32_t fill = 0;  // band fills so far (same sequence for every band)
-    for (int t = t_begin; t < tiles; t += t_step) {
+    int t;
+    bool part;
+    for (int k = 0; work(k, t, part); ++k) {
       const int mt = t / n_tiles;
       int pn[4], py[4], px[4];
       bool pv[4];
@@ -205,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       int cb0, cb1;
-      cb_range(t, cb0, cb1);
+      cb_range(t, part, cb0, cb1);
       for (int cb = cb0; cb < cb1; ++cb, ++fill) {
         for (int y = 0; y < E; ++y) {
           mbar_wait(&band_empty[y], (fill & 1) ^ 1);
@@ -229,10 +265,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- weights (B) TMA
     if (lane == 0) {
       uint32_t it = 0;
-      for (int t = t_begin; t < tiles; t += t_step) {
+      int t;
+      bool part;
+      for (int k = 0; work(k, t, part); ++k) {
         const int n0 = (t % n_tiles) * BN;
         int cb0, cb1;
-        cb_range(t, cb0, cb1);
+        cb_range(t, part, cb0, cb1);
         for (int cb = cb0; cb < cb1; ++cb)
           for (int tap = 0; tap < 9; ++tap, ++it) {
             const int stage = it % L::STAGES;
@@ -246,13 +284,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
     uint32_t it = 0, fill = 0, local = 0;
-    for (int t = t_begin; t < tiles; t += t_step, ++local) {
+    int t;
+    bool part;
+    for (int k = 0; work(k, t, part); ++k, ++local) {
       const int buf = local % L::NBUF;
       mbar_wait(&acc_empty[buf], ((local / L::NBUF) & 1) ^ 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + buf * L::TILE_COLS;
       int cb0, cb1;
-      cb_range(t, cb0, cb1);
+      cb_range(t, part, cb0, cb1);
       for (int cb = cb0; cb < cb1; ++cb, ++fill) {
         for (int ky = 0; ky < 3; ++ky) {
           // bands first read at this ky: 0 .. S-1 at ky = 0, then ky + S - 1
@@ -305,10 +345,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int i = q * 32 + lane;
     const int lx = i / P, pl = i - (i / P) * P;
     uint32_t local = 0;
-    for (int t = t_begin; t < tiles; t += t_step, ++local) {
+    int t;
+    bool part;
+    for (int k = 0; work(k, t, part); ++k, ++local) {
       const int buf = local % L::NBUF;
       const int mt = t / n_tiles;
-      if (KS > 1) {
+      if (part) {
         // split-K: this CTA's fp32 partial -> its own smem (the halo / weight
         // region: every MMA of the tile has completed), reduced after the
         // cluster barrier below
@@ -391,18 +433,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
-  if (KS > 1) {
+  if (KS > 1 || tail) {
     // split-K reduction through distributed shared memory: CTA ks finishes rows
-    // [ks, ks + 1) * S*128/KS of the tile's (ly, row) space, summing the KS
+    // [ks, ks + 1) * S*128/NP of its part tile's (ly, row) space, summing the NP
     // partials in rank order (deterministic), then scale / bias / ReLU -> bf16
     cluster_sync();  // every CTA's partials written and visible cluster-wide
-    if (t_begin < tiles) {
-      const int t = t_begin;
-      const int mt = t / n_tiles, n0 = (t % n_tiles) * BN;
+    const int tr = KS > 1 ? (t_begin < tiles ? t_begin : -1) : split_t;
+    if (tr >= 0) {
+      const int mt = tr / n_tiles, n0 = (tr % n_tiles) * BN;
       constexpr int RR = S * 128;
-      const int rpc = RR / KS;
+      const int rpc = RR / NP;
       constexpr int C4 = BN / 4;
-      const uint32_t part = base_u32 + L::HALO_OFF;
+      const uint32_t partb = base_u32 + L::HALO_OFF;
       __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
       for (int idx = threadIdx.x; idx < rpc * C4; idx += THREADS) {
         const int lr = ks * rpc + idx / C4, c4 = idx % C4;
@@ -413,17 +455,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (pi >= count || c >= p.n_out) continue;
         const uint32_t off = (uint32_t)(((ly * 128 + row) * L::PSTRIDE + c4 * 4) * 4);
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int r = 0; r < KS; ++r) {
+        for (int r = 0; r < NP; ++r) {
           float4 v;
           asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                       : "r"(mapa_shared(part + off, r)) : "memory");
+                       : "r"(mapa_shared(partb + off, r)) : "memory");
           acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
         float o[4] = {acc.x, acc.y, acc.z, acc.w};
+        uint32_t mk = 0xffffffffu;
+        if (p.ymask_channel)
+          mk = __ldg(reinterpret_cast<const uint32_t*>(
+              p.ymask_channel + (size_t)(list_cell(p, pi) / (p.cells_h * p.cells_w)) * p.n_out + c));
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           o[e] = fmaf(o[e], vsc[c + e], vbi[c + e]);
+          if (!((mk >> (8 * e)) & 0xff)) o[e] = 0.f;
           if (p.relu) o[e] = fmaxf(o[e], 0.f);
         }
         const long long dst = (long long)pi * s2 + ly * S + lx;
@@ -453,15 +500,18 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParam
   }
   const int s2 = S * S;
   const long long tiles = ((long long)(p.rows_max / s2) + L::P - 1) / L::P * ((p.n_out + BN - 1) / BN);
-  if (p.ksplit > 1 && L::SPLIT_OK) {  // one wave of clusters, one tile each (host-checked)
+  if ((p.ksplit > 1 || p.tail_split) && L::SPLIT_OK) {  // clusters (host-checked)
+    // ksplit: one wave of clusters, one tile each; tail split: a persistent grid
+    // of 2-CTA clusters
+    const long long g = p.ksplit > 1 ? tiles * p.ksplit : (tiles < num_sms ? tiles : num_sms) / 2 * 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(tiles * p.ksplit), 1, 1);
+    cfg.gridDim = dim3((unsigned)(g > 2 ? g : 2), 1, 1);
     cfg.blockDim = dim3(THREADS, 1, 1);
     cfg.dynamicSmemBytes = L::ALLOC;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.ksplit;
+    attr[0].val.clusterDim.x = p.ksplit > 1 ? p.ksplit : 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;

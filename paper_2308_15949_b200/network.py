@@ -269,7 +269,8 @@ class LaudNetwork:
                     kw["next_wdiff"] = nxt.db.wdiff if fused_out else None
             if para in ("spatial", "layer"):
                 kw["aux_stream"] = self._aux_stream()  # small grids fork the masker (laud.h aux_stream)
-                kw["latency_split"] = self.latency_split
+            if para in ("spatial", "layer", "static"):
+                kw["latency_split"] = self.latency_split  # conv2 split-K: small grids / last partial wave
             y, coarse, cells, counts = db.forward(x, para, slot.s if para == "spatial" else 0,
                                                   out=out, stream=stream, ws=self.ws, **kw)
             prev_coarse = kw.get("coarse_out")

@@ -91,13 +91,15 @@ def test_patch_rows_gather_scatter():
 @pytest.mark.parametrize("s,cin,cout,n,h,density", [
     (2, 256, 256, 8, 14, 0.5), (2, 128, 128, 4, 28, 0.5), (4, 64, 64, 4, 56, 0.5), (2, 64, 64, 3, 16, 0.3),
     (4, 128, 128, 2, 28, 0.7), (2, 256, 256, 64, 14, 0.5), (2, 40, 24, 2, 8, 1.0), (4, 64, 64, 1, 8, 0.0),
-    (2, 256, 256, 1, 14, 0.5), (2, 512, 256, 2, 14, 0.6), (4, 256, 64, 1, 56, 0.5)])
+    (2, 256, 256, 1, 14, 0.5), (2, 512, 256, 2, 14, 0.6), (4, 256, 64, 1, 56, 0.5),
+    (2, 256, 256, 256, 14, 0.5), (2, 256, 256, 300, 14, 0.7), (2, 128, 128, 200, 28, 0.5)])
 @pytest.mark.parametrize("split", [0, 1])
 def test_patch_conv_halo_smem(s, cin, cout, n, h, density, split):
     """3x3 patch conv over active S x S cells (the halo-in-shared-memory kernel for
     S = 2 / 4, stride 1): ragged patch counts (not a multiple of the tile's patch
     count), image-border cells (zero halo), several N tiles, scale/bias/ReLU; with
-    latency_split the small grids split K over a cluster (DSMEM reduction)."""
+    latency_split the small grids split K over a cluster (DSMEM reduction) and large
+    grids split the last partial wave's tiles over 2-CTA clusters (batch 200-300)."""
     CH, D = _engine()
     g = torch.Generator().manual_seed(s * 1000 + cin + n)
     x = torch.randn(n, h, h, cin, generator=g).cuda().to(torch.bfloat16)
