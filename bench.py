@@ -458,10 +458,13 @@ def profile_launches(torch, net, images):
     return list(recs[:n])
 
 
-def conv_roofline(recs, pk, pk_kind):
+def conv_roofline(recs, pk, pk_kind, channel_ratio=None):
     """Roofline of the dominant conv-engine launch shape (largest total time in
     the step): achieved = algorithmic FLOPs (or bytes, whichever bounds it) per
-    launch / average CUDA-event duration of those launches."""
+    launch / average CUDA-event duration of those launches.  Channel paradigm
+    (``channel_ratio`` = mean kept ratio r): the dense-masked launches compute
+    every MAC, but only the kept channels' work is credited — r for a 1x1 conv
+    (conv1 / conv3), r^2 for the 3x3 conv2 (W2[sel][:, sel]), bytes scaled by r."""
     convs = [r for r in recs if r.tag == 0]
     maskers = [r for r in recs if r.tag == 1]
     all_ms = sum(r.ms for r in recs)
@@ -470,6 +473,12 @@ def conv_roofline(recs, pk, pk_kind):
         groups.setdefault((r.rows, r.n_out, r.k, r.taps, r.resid), []).append((i, r))
     key, grp = max(groups.items(), key=lambda kv: sum(x.ms for _, x in kv[1]))
     flops, nbytes = _alg(grp[0][1])
+    credit = "rows x n_out x K (K = taps x C_in / groups), actual active rows"
+    if channel_ratio is not None:
+        r = float(channel_ratio)
+        flops *= r * r if grp[0][1].taps > 1 else r
+        nbytes *= r
+        credit = "channel: kept-channel work only (r F1, r^2 F2, r F3; bytes x r)"
     avg_ms = sum(x.ms for _, x in grp) / len(grp)
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     peak_b = pk["hbm_gbs"]
@@ -487,7 +496,7 @@ def conv_roofline(recs, pk, pk_kind):
         "bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
         "frac": round(ach / peak, 4), "traffic": None,
         "peak_source": f"{pk_kind} MEASURED_PEAKS.json ({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})",
-        "alg_flops_per_launch": flops, "alg_bytes_per_launch": nbytes,
+        "alg_flops_per_launch": flops, "alg_bytes_per_launch": nbytes, "credit": credit,
         "avg_launch_us": round(avg_ms * 1e3, 2),
         "share_of_profiled_step": round(sum(x.ms for _, x in grp) / all_ms, 3) if all_ms else None,
         "launch_ordinals": [i for i, _ in grp],  # positions among the conv launches (traffic pass)
@@ -941,7 +950,8 @@ def run_gpu(args):
 
     extra = {}
     recs = profile_launches(torch, net, images)
-    roof = conv_roofline(recs, pk, pk_kind)
+    roof = conv_roofline(recs, pk, pk_kind,
+                         channel_ratio=r_local if args.paradigm == "channel" else None)
     if rank == 0 and ws == 1 and not args.no_traffic:
         tr = traffic_pass(args, roof)
         if tr:
