@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // arrivals: A expect_tx (TMA) or 128 cp.async threads, + B expect_tx or 32 cp.async lanes
-      mbar_init(&full[s], (p.a_tma ? 1 : 128) + (p.b_gather != B_BOX ? 32 : 1));
+      // (fused masker: one thread issues A and B together, warps 0-3 all read)
+      mbar_init(&full[s], (AM == AM_TILE_DOT && p.adot_out) ? 1 : (p.a_tma ? 1 : 128) + (p.b_gather != B_BOX ? 32 : 1));
       mbar_init(&empty[s], p.adot_out ? 2 : 1);  // + the fused masker readers
     }
     for (int a = 0; a < L::NACC; ++a) {
@@ -245,18 +246,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr bool kDot = AM == AM_TILE_DOT || AM == AM_ANY;
     constexpr bool kBox = AM == AM_BOX || AM == AM_ANY;
     constexpr bool kG4 = AM == AM_G4 || AM == AM_ANY;
-    if (kDot && p.a_tile && p.adot_out && warp >= 1) {
-      // fused masker readers (warps 1-3): every A stage, once landed, is also
-      // read here — dot of each row with the masker weights W0 - W1
-      // (`reference.py:244-253`) — and released with a second arrive
-      const int mt = tid - 32;  // 0 .. 95: rows mt and mt + 96 (< 128)
-      const int ra = mt, rb = mt + 96;
+    // AM_TILE_DOT: the B-producer thread issues the A boxes too and warps 0-3
+    // (128 threads, one row each) are all masker readers
+    constexpr int NRD = AM == AM_TILE_DOT ? 128 : 96;
+    if (kDot && p.a_tile && p.adot_out && (AM == AM_TILE_DOT || warp >= 1)) {
+      // fused masker readers: every A stage, once landed, is also read here —
+      // dot of each row with the masker weights W0 - W1 (`reference.py:244-253`)
+      // — and released with a second arrive
+      const int mt = AM == AM_TILE_DOT ? tid : tid - 32;  // rows mt (and mt + 96 with 96 readers)
+      const int ra = mt, rb = mt + NRD;
       // plain-epilogue kernels only use the bias part of the vector region: the
       // masker weights live at its top for the whole kernel (host checks the fit)
       float* const wsm = reinterpret_cast<float*>(base + L::VEC_OFF + L::VEC_BYTES) - p.kpad;
       if constexpr (EP != EP_ANY) {
-        for (int i = mt; i < p.kpad; i += 96) wsm[i] = __ldg(p.adot_w + i);
-        asm volatile("bar.sync 3, 96;" ::: "memory");
+        for (int i = mt; i < p.kpad; i += NRD) wsm[i] = __ldg(p.adot_w + i);
+        asm volatile("bar.sync 3, %0;" ::"n"(NRD) : "memory");
       }
       for (int t = t_begin; t < tiles; t += t_step) {
         const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
@@ -273,8 +277,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               va[c] = *reinterpret_cast<const uint4*>(sA + ra * 128 + ((c ^ (ra & 7)) << 4));
-              vb[c] = rb < BM ? *reinterpret_cast<const uint4*>(sA + rb * 128 + ((c ^ (rb & 7)) << 4))
-                              : make_uint4(0u, 0u, 0u, 0u);
+              vb[c] = (NRD < BM && rb < BM) ? *reinterpret_cast<const uint4*>(sA + rb * 128 + ((c ^ (rb & 7)) << 4))
+                                            : make_uint4(0u, 0u, 0u, 0u);
             }
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -292,13 +296,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               f = unpack_bf16x2(va[c].y); aa[k] = fmaf(f.x, w0.z, aa[k]); aa[k] = fmaf(f.y, w0.w, aa[k]);
               f = unpack_bf16x2(va[c].z); aa[k] = fmaf(f.x, w1.x, aa[k]); aa[k] = fmaf(f.y, w1.y, aa[k]);
               f = unpack_bf16x2(va[c].w); aa[k] = fmaf(f.x, w1.z, aa[k]); aa[k] = fmaf(f.y, w1.w, aa[k]);
-              f = unpack_bf16x2(vb[c].x); ab[k] = fmaf(f.x, w0.x, ab[k]); ab[k] = fmaf(f.y, w0.y, ab[k]);
-              f = unpack_bf16x2(vb[c].y); ab[k] = fmaf(f.x, w0.z, ab[k]); ab[k] = fmaf(f.y, w0.w, ab[k]);
-              f = unpack_bf16x2(vb[c].z); ab[k] = fmaf(f.x, w1.x, ab[k]); ab[k] = fmaf(f.y, w1.y, ab[k]);
-              f = unpack_bf16x2(vb[c].w); ab[k] = fmaf(f.x, w1.z, ab[k]); ab[k] = fmaf(f.y, w1.w, ab[k]);
+              if constexpr (NRD < BM) {
+                f = unpack_bf16x2(vb[c].x); ab[k] = fmaf(f.x, w0.x, ab[k]); ab[k] = fmaf(f.y, w0.y, ab[k]);
+                f = unpack_bf16x2(vb[c].y); ab[k] = fmaf(f.x, w0.z, ab[k]); ab[k] = fmaf(f.y, w0.w, ab[k]);
+                f = unpack_bf16x2(vb[c].z); ab[k] = fmaf(f.x, w1.x, ab[k]); ab[k] = fmaf(f.y, w1.y, ab[k]);
+                f = unpack_bf16x2(vb[c].w); ab[k] = fmaf(f.x, w1.z, ab[k]); ab[k] = fmaf(f.y, w1.w, ab[k]);
+              }
             }
           }
-          asm volatile("bar.sync 3, 96;" ::: "memory");
+          asm volatile("bar.sync 3, %0;" ::"n"(NRD) : "memory");
           if (mt == 0) mbar_arrive(&empty[stage]);
         }
         const float acc_a = (aa[0] + aa[1]) + (aa[2] + aa[3]);
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // row-major order, so decisions are deterministic run to run
         if (dots) {
           if (ti.m0 + ra < nvalid) p.adot_out[ti.m0 + ra] = acc_a;
-          if (rb < BM && ti.m0 + rb < nvalid) p.adot_out[ti.m0 + rb] = acc_b;
+          if (NRD < BM && rb < BM && ti.m0 + rb < nvalid) p.adot_out[ti.m0 + rb] = acc_b;
         }
       }
     } else if (kTile && p.a_tile) {
@@ -527,10 +533,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (leader) mbar_arrive(&full[stage]);
             continue;
           }
-          if (leader) mbar_arrive_expect_tx(&full[stage], XMUL * L::B_STAGE_BYTES);
           const int cblk = kb / taps, tap = kb - cblk * taps;
           const int kcoord = tap * p.kpad + ti.c_lo + cblk * BK;  // per-tap stride kpad
           const uint32_t dst = base_u32 + L::B_OFF + stage * L::B_STAGE_BYTES;
+          if (AM == AM_TILE_DOT && p.adot_out) {
+            // fused masker: this thread issues the stage's A box too (warps 0-3 read it)
+            mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + L::B_STAGE_BYTES);
+            tma_load_2d(base_u32 + L::A_OFF + stage * A_STAGE_BYTES, &tmap_a, &full[stage], ti.c_lo + kb * BK,
+                        ti.m0);
+          } else if (leader) {
+            mbar_arrive_expect_tx(&full[stage], XMUL * L::B_STAGE_BYTES);
+          }
           if constexpr (PAIR) {  // this CTA's half of the tile's B rows
             tma_load_2d_pair(dst, &tmap_b, full_tx(stage), kcoord, ti.n0 + rank * (BN / 2));
           } else if (p.b_batched) {
