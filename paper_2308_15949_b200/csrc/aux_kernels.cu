@@ -150,8 +150,8 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int hw, int c,
 //    list == nullptr, its dense pixel block — averaged into means[n][c]; the
 //    row range goes to rr[n].
 //  se_fc1_kernel / se_fc2_kernel (SE_SPB samples x an output chunk per CTA):
-//    gate = sigmoid(W2 relu(W1 mean + b1) + b2), each weight row read once per
-//    SE_SPB samples;
+//    gate = sigmoid(W2 relu(W1 mean + b1) + b2), each weight row read once
+//    (coalesced) per SE_SPB samples;
 //  se_scale_kernel: h2 *= gate over each sample's rows (bf16 RNE) — the oracle
 //    EXT (`laud_oracle._se_scale`).
 constexpr int SE_SPB = 16;
@@ -235,65 +235,178 @@ __global__ void __launch_bounds__(256) se_pool_kernel(const __nv_bfloat16* __res
 }
 
 // The SE FC layers as two launches with grids over (sample groups x output
-// chunks), so the GPU fills at batch 1024 (one CTA per 16 samples left 64 CTAs
-// on 148 SMs): fc1 = relu(W1 mean + b1) -> hidden [n][hs], fc2 = sigmoid(W2
-// hidden + b2) -> gates [n][c].  Per output, the FMAs run in the order of the
-// oracle EXT's reductions (sequential over the input index).
+// chunks), so the GPU fills at batch 1024: fc1 = relu(W1 mean + b1) -> hidden
+// [n][hs], fc2 = sigmoid(W2 hidden + b2) -> gates [n][c].  One warp per SE_UB
+// output units and SE_SPB samples: the lanes stride over the input index, so each
+// weight row is read coalesced once per sample group and each shared-memory
+// operand feeds SE_UB FMAs; a unit's 16 per-lane partial sums are then reduced by
+// recursive halving (16 shuffles), after which lane l holds sample l / 2's sum.
+__device__ __forceinline__ float se_reduce16(float (&a)[SE_SPB], int lane) {
+  static_assert(SE_SPB == 16, "se_reduce16: 16 samples per warp");
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const bool up = lane & 16;
+    const float send = up ? a[k] : a[k + 8];
+    a[k] = (up ? a[k + 8] : a[k]) + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool up = lane & 8;
+    const float send = up ? a[k] : a[k + 4];
+    a[k] = (up ? a[k + 4] : a[k]) + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool up = lane & 4;
+    const float send = up ? a[k] : a[k + 2];
+    a[k] = (up ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool up = lane & 2;
+    const float send = up ? a[0] : a[1];
+    a[0] = (up ? a[1] : a[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return a[0] + __shfl_xor_sync(0xffffffffu, a[0], 1);
+}
+
+// dst[0, total) <- src[0, valid), zeros past it: B loads per thread in
+// flight before the shared-memory stores (a load -> store loop serialises on
+// the global latency, ~20 round trips per thread at C = 336)
+template <typename T, int B = 16>
+__device__ __forceinline__ void se_stage(T* dst, const T* __restrict__ src, int valid, int total, int tid) {
+  for (int base = tid; base < total; base += 256 * B) {
+    T v[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int i = base + 256 * k;
+      v[k] = i < valid ? __ldg(src + i) : T{};
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int i = base + 256 * k;
+      if (i < total) dst[i] = v[k];
+    }
+  }
+}
+
+constexpr int SE_FC1_UNITS = 32;  // hidden units per CTA (8 warps x 4)
+constexpr int SE_FC2_UNITS = 64;  // output channels per CTA (8 warps x 2 passes x 4)
+constexpr int SE_UB = 4;          // units per warp pass: each shared-memory read feeds SE_UB FMAs
+
 __global__ void __launch_bounds__(256) se_fc1_kernel(int n, int c, const float* __restrict__ means,
                                                      const float* __restrict__ w1, const float* __restrict__ b1,
                                                      int hs, float* __restrict__ hidden) {
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ float mean[];  // [SE_SPB][c]
   const int s0 = blockIdx.x * SE_SPB;
   const int ns = min(SE_SPB, n - s0);
-  const int tid = threadIdx.x;
-  for (int i = tid; i < SE_SPB * c; i += blockDim.x) mean[i] = i / c < ns ? means[(size_t)s0 * c + i] : 0.f;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c4 = c >> 2;
+  const int u0 = blockIdx.y * SE_FC1_UNITS + warp * SE_UB;
+  constexpr int T = 2;  // float4 weight loads per lane and unit in flight
+  float4 wv[SE_UB][T];
+  auto load_w = [&](int i0) {
+#pragma unroll
+    for (int k = 0; k < SE_UB; ++k)
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int i = i0 + lane + 32 * t;
+        wv[k][t] = (i < c4 && u0 + k < hs) ? __ldg(reinterpret_cast<const float4*>(w1 + (size_t)(u0 + k) * c) + i)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  };
+  load_w(0);  // weights are constants: in flight before the dependency wait
+  pdl_wait();
+  pdl_trigger();
+  se_stage(reinterpret_cast<float4*>(mean), reinterpret_cast<const float4*>(means + (size_t)s0 * c), ns * c / 4,
+           SE_SPB * c / 4, tid);
   __syncthreads();
-  const int u = blockIdx.y * 32 + (tid & 31);  // hidden unit
-  const int q0 = (tid >> 5) * 2;               // two samples per thread
-  if (u >= hs) return;
-  float a0 = 0.f, a1 = 0.f;
-  const float4* wr = reinterpret_cast<const float4*>(w1 + (size_t)u * c);
-#pragma unroll 4
-  for (int i = 0; i < c / 4; ++i) {
-    const float4 wv = __ldg(wr + i);
-    const float4 m0 = reinterpret_cast<const float4*>(mean + q0 * c)[i];
-    const float4 m1 = reinterpret_cast<const float4*>(mean + (q0 + 1) * c)[i];
-    a0 = fmaf(wv.x, m0.x, fmaf(wv.y, m0.y, fmaf(wv.z, m0.z, fmaf(wv.w, m0.w, a0))));
-    a1 = fmaf(wv.x, m1.x, fmaf(wv.y, m1.y, fmaf(wv.z, m1.z, fmaf(wv.w, m1.w, a1))));
+  if (u0 >= hs) return;
+  float a[SE_UB][SE_SPB];
+#pragma unroll
+  for (int k = 0; k < SE_UB; ++k)
+#pragma unroll
+    for (int q = 0; q < SE_SPB; ++q) a[k][q] = 0.f;
+  for (int i0 = 0; i0 < c4; i0 += 32 * T) {
+    if (i0 > 0) load_w(i0);
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int i = i0 + lane + 32 * t;
+      if (i < c4) {
+#pragma unroll
+        for (int q = 0; q < SE_SPB; ++q) {
+          const float4 m = reinterpret_cast<const float4*>(mean + q * c)[i];
+#pragma unroll
+          for (int k = 0; k < SE_UB; ++k)
+            a[k][q] = fmaf(wv[k][t].x, m.x, fmaf(wv[k][t].y, m.y, fmaf(wv[k][t].z, m.z, fmaf(wv[k][t].w, m.w, a[k][q]))));
+        }
+      }
+    }
   }
-  if (q0 < ns) hidden[(size_t)(s0 + q0) * hs + u] = fmaxf(a0 + b1[u], 0.f);
-  if (q0 + 1 < ns) hidden[(size_t)(s0 + q0 + 1) * hs + u] = fmaxf(a1 + b1[u], 0.f);
+  const int q = lane >> 1;
+#pragma unroll
+  for (int k = 0; k < SE_UB; ++k) {
+    const float v = se_reduce16(a[k], lane);
+    const int u = u0 + k;
+    if (u < hs && !(lane & 1) && q < ns) hidden[(size_t)(s0 + q) * hs + u] = fmaxf(v + b1[u], 0.f);
+  }
 }
 
 __global__ void __launch_bounds__(256) se_fc2_kernel(int n, int c, const float* __restrict__ hidden,
                                                      const float* __restrict__ w2, const float* __restrict__ b2,
                                                      int hs, float* __restrict__ gates) {
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ float hid[];  // [SE_SPB][hs]
   const int s0 = blockIdx.x * SE_SPB;
   const int ns = min(SE_SPB, n - s0);
-  const int tid = threadIdx.x;
-  for (int i = tid; i < SE_SPB * hs; i += blockDim.x) hid[i] = i / hs < ns ? hidden[(size_t)s0 * hs + i] : 0.f;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int T = 4;  // weight loads per lane and output in flight
+  constexpr int PASSES = SE_FC2_UNITS / (8 * SE_UB);
+  const int q = lane >> 1;
+  float wv[SE_UB][T];
+  auto load_w = [&](int o0, int j0) {
+#pragma unroll
+    for (int k = 0; k < SE_UB; ++k)
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int j = j0 + lane + 32 * t;
+        wv[k][t] = (j < hs && o0 + k < c) ? __ldg(w2 + (size_t)(o0 + k) * hs + j) : 0.f;
+      }
+  };
+  const int obase = blockIdx.y * SE_FC2_UNITS + warp * PASSES * SE_UB;
+  load_w(obase, 0);  // weights are constants: in flight before the dependency wait
+  pdl_wait();
+  pdl_trigger();
+  se_stage(hid, hidden + (size_t)s0 * hs, ns * hs, SE_SPB * hs, tid);
   __syncthreads();
-  const int o = blockIdx.y * 128 + (tid & 127);  // output channel
-  const int q0 = (tid >> 7) * (SE_SPB / 2);      // half of the samples per thread
-  if (o >= c) return;
-  float a[SE_SPB / 2];
+  for (int pass = 0; pass < PASSES; ++pass) {
+    const int o0 = obase + pass * SE_UB;
+    if (o0 >= c) break;
+    float a[SE_UB][SE_SPB];
 #pragma unroll
-  for (int q = 0; q < SE_SPB / 2; ++q) a[q] = 0.f;
-  const float* wr = w2 + (size_t)o * hs;
-#pragma unroll 4
-  for (int jj = 0; jj < hs; ++jj) {
-    const float wv = __ldg(wr + jj);
+    for (int k = 0; k < SE_UB; ++k)
 #pragma unroll
-    for (int q = 0; q < SE_SPB / 2; ++q) a[q] = fmaf(wv, hid[(q0 + q) * hs + jj], a[q]);
+      for (int qq = 0; qq < SE_SPB; ++qq) a[k][qq] = 0.f;
+    for (int j0 = 0; j0 < hs; j0 += 32 * T) {
+      if (pass > 0 || j0 > 0) load_w(o0, j0);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int j = j0 + lane + 32 * t;
+        if (j < hs) {
+#pragma unroll
+          for (int qq = 0; qq < SE_SPB; ++qq) {
+            const float h = hid[qq * hs + j];
+#pragma unroll
+            for (int k = 0; k < SE_UB; ++k) a[k][qq] = fmaf(wv[k][t], h, a[k][qq]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < SE_UB; ++k) {
+      const float v = se_reduce16(a[k], lane);
+      const int o = o0 + k;
+      if (o < c && !(lane & 1) && q < ns) gates[(size_t)(s0 + q) * c + o] = 1.f / (1.f + __expf(-(v + b2[o])));
+    }
   }
-#pragma unroll
-  for (int q = 0; q < SE_SPB / 2; ++q)
-    if (q0 + q < ns) gates[(size_t)(s0 + q0 + q) * c + o] = 1.f / (1.f + __expf(-(a[q] + b2[o])));
 }
 
 static cudaError_t launch_se_fc(int n, int c, const float* means, const float* w1, const float* b1, int hs,
@@ -306,8 +419,10 @@ static cudaError_t launch_se_fc(int n, int c, const float* means, const float* w
     configured = sm1;
   }
   const int sg = (n + SE_SPB - 1) / SE_SPB;
-  launch_k(se_fc1_kernel, dim3(sg, (hs + 31) / 32), dim3(256), sm1, s, n, c, means, w1, b1, hs, hidden);
-  launch_k(se_fc2_kernel, dim3(sg, (c + 127) / 128), dim3(256), (size_t)SE_SPB * hs * sizeof(float), s, n, c,
+  launch_k(se_fc1_kernel, dim3(sg, (hs + SE_FC1_UNITS - 1) / SE_FC1_UNITS), dim3(256), sm1, s, n, c, means, w1,
+           b1, hs, hidden);
+  launch_k(se_fc2_kernel, dim3(sg, (c + SE_FC2_UNITS - 1) / SE_FC2_UNITS), dim3(256),
+           (size_t)SE_SPB * hs * sizeof(float), s, n, c,
            (const float*)hidden, w2, b2, hs, gates);
   return cudaSuccess;
 }
