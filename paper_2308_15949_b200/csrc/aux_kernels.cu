@@ -290,7 +290,7 @@ __device__ __forceinline__ void se_stage(T* dst, const T* __restrict__ src, int 
 }
 
 constexpr int SE_FC1_UNITS = 32;  // hidden units per CTA (8 warps x 4)
-constexpr int SE_FC2_UNITS = 64;  // output channels per CTA (8 warps x 2 passes x 4)
+constexpr int SE_FC2_UNITS = 32;  // output channels per CTA (8 warps x 4)
 constexpr int SE_UB = 4;          // units per warp pass: each shared-memory read feeds SE_UB FMAs
 
 __global__ void __launch_bounds__(256) se_fc1_kernel(int n, int c, const float* __restrict__ means,
@@ -315,6 +315,9 @@ __global__ void __launch_bounds__(256) se_fc1_kernel(int n, int c, const float* 
       }
   };
   load_w(0);  // weights are constants: in flight before the dependency wait
+  float bias[SE_UB];
+#pragma unroll
+  for (int k = 0; k < SE_UB; ++k) bias[k] = u0 + k < hs ? __ldg(b1 + u0 + k) : 0.f;
   pdl_wait();
   pdl_trigger();
   se_stage(reinterpret_cast<float4*>(mean), reinterpret_cast<const float4*>(means + (size_t)s0 * c), ns * c / 4,
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(256) se_fc1_kernel(int n, int c, const float* 
   for (int k = 0; k < SE_UB; ++k) {
     const float v = se_reduce16(a[k], lane);
     const int u = u0 + k;
-    if (u < hs && !(lane & 1) && q < ns) hidden[(size_t)(s0 + q) * hs + u] = fmaxf(v + b1[u], 0.f);
+    if (u < hs && !(lane & 1) && q < ns) hidden[(size_t)(s0 + q) * hs + u] = fmaxf(v + bias[k], 0.f);
   }
 }
 
@@ -361,50 +364,65 @@ __global__ void __launch_bounds__(256) se_fc2_kernel(int n, int c, const float* 
   constexpr int T = 4;  // weight loads per lane and output in flight
   constexpr int PASSES = SE_FC2_UNITS / (8 * SE_UB);
   const int q = lane >> 1;
-  float wv[SE_UB][T];
-  auto load_w = [&](int o0, int j0) {
+  // (pass, column chunk) steps, software-pipelined: the next step's weights
+  // are loaded while this step's FMAs run
+  const int jsteps = (hs + 32 * T - 1) / (32 * T);
+  const int obase = blockIdx.y * SE_FC2_UNITS + warp * PASSES * SE_UB;
+  const int nsteps = min(PASSES, (c - obase + SE_UB - 1) / SE_UB) * jsteps;
+  float wn[SE_UB][T], bn[SE_UB];
+  auto load_w = [&](int step) {
+    const int o0 = obase + (step / jsteps) * SE_UB, j0 = (step % jsteps) * 32 * T;
 #pragma unroll
-    for (int k = 0; k < SE_UB; ++k)
+    for (int k = 0; k < SE_UB; ++k) {
 #pragma unroll
       for (int t = 0; t < T; ++t) {
         const int j = j0 + lane + 32 * t;
-        wv[k][t] = (j < hs && o0 + k < c) ? __ldg(w2 + (size_t)(o0 + k) * hs + j) : 0.f;
+        wn[k][t] = (j < hs && o0 + k < c) ? __ldg(w2 + (size_t)(o0 + k) * hs + j) : 0.f;
       }
+      bn[k] = o0 + k < c ? __ldg(b2 + o0 + k) : 0.f;
+    }
   };
-  const int obase = blockIdx.y * SE_FC2_UNITS + warp * PASSES * SE_UB;
-  load_w(obase, 0);  // weights are constants: in flight before the dependency wait
+  if (nsteps > 0) load_w(0);  // weights are constants: in flight before the dependency wait
   pdl_wait();
   pdl_trigger();
   se_stage(hid, hidden + (size_t)s0 * hs, ns * hs, SE_SPB * hs, tid);
   __syncthreads();
-  for (int pass = 0; pass < PASSES; ++pass) {
-    const int o0 = obase + pass * SE_UB;
-    if (o0 >= c) break;
-    float a[SE_UB][SE_SPB];
+  float a[SE_UB][SE_SPB];
+  for (int step = 0; step < nsteps; ++step) {
+    const int js = step % jsteps, o0 = obase + (step / jsteps) * SE_UB, j0 = js * 32 * T;
+    float wv[SE_UB][T], bv[SE_UB];
 #pragma unroll
-    for (int k = 0; k < SE_UB; ++k)
+    for (int k = 0; k < SE_UB; ++k) {
+      bv[k] = bn[k];
 #pragma unroll
-      for (int qq = 0; qq < SE_SPB; ++qq) a[k][qq] = 0.f;
-    for (int j0 = 0; j0 < hs; j0 += 32 * T) {
-      if (pass > 0 || j0 > 0) load_w(o0, j0);
+      for (int t = 0; t < T; ++t) wv[k][t] = wn[k][t];
+    }
+    if (step + 1 < nsteps) load_w(step + 1);
+    if (js == 0) {
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        const int j = j0 + lane + 32 * t;
-        if (j < hs) {
+      for (int k = 0; k < SE_UB; ++k)
 #pragma unroll
-          for (int qq = 0; qq < SE_SPB; ++qq) {
-            const float h = hid[qq * hs + j];
+        for (int qq = 0; qq < SE_SPB; ++qq) a[k][qq] = 0.f;
+    }
 #pragma unroll
-            for (int k = 0; k < SE_UB; ++k) a[k][qq] = fmaf(wv[k][t], h, a[k][qq]);
-          }
+    for (int t = 0; t < T; ++t) {
+      const int j = j0 + lane + 32 * t;
+      if (j < hs) {
+#pragma unroll
+        for (int qq = 0; qq < SE_SPB; ++qq) {
+          const float h = hid[qq * hs + j];
+#pragma unroll
+          for (int k = 0; k < SE_UB; ++k) a[k][qq] = fmaf(wv[k][t], h, a[k][qq]);
         }
       }
     }
+    if (js == jsteps - 1) {
 #pragma unroll
-    for (int k = 0; k < SE_UB; ++k) {
-      const float v = se_reduce16(a[k], lane);
-      const int o = o0 + k;
-      if (o < c && !(lane & 1) && q < ns) gates[(size_t)(s0 + q) * c + o] = 1.f / (1.f + __expf(-(v + b2[o])));
+      for (int k = 0; k < SE_UB; ++k) {
+        const float v = se_reduce16(a[k], lane);
+        const int o = o0 + k;
+        if (o < c && !(lane & 1) && q < ns) gates[(size_t)(s0 + q) * c + o] = 1.f / (1.f + __expf(-(v + bv[k])));
+      }
     }
   }
 }
