@@ -19,7 +19,7 @@
 #include "laud_conv.cuh"
 
 namespace laud {
-cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn,
+cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const CUtensorMap& tmap_o, int bn,
                              const ConvParams& p, int num_sms, cudaStream_t stream, int pair);
 cudaError_t launch_conv_f32(const ConvParams& p, cudaStream_t stream);
 bool patch_conv_supported(int s, int bn);
@@ -572,6 +572,22 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
   } else if ((rc = tensor_map_2d(a->weight, a->n_out, kw, kw, pair ? bn / 2 : bn, &m, a->b_batched ? a->batch : 0))) {
     return rc;
   }
+  // TMA-store epilogue (plain epilogues only; the kernel ignores it otherwise):
+  // dense rows as 32-row boxes, scattered S x S patches (S >= 2) as pixel boxes
+  CUtensorMap mo;
+  memset(&mo, 0, sizeof(mo));
+  static const int tma_out_env = [] {
+    const char* e = getenv("LAUD_TMA_OUT");
+    return e ? atoi(e) : 1;
+  }();
+  const bool out_ok = tma_out_env && !a->out_f32 && !a->col_index && (reinterpret_cast<uintptr_t>(a->out) & 15) == 0;
+  if (out_ok && a->row_mode == ROWS_DENSE && a->out_mode == OUT_ROW && !a->sample_rows && !a->count) {
+    if (tensor_map_2d(a->out, a->rows_max, a->n_out, a->out_ld, 32, &mo) == LAUD_OK) p.tma_out = 1;
+  } else if (out_ok && a->row_mode == ROWS_PATCH && a->out_mode == OUT_PIXEL && a->patch_h == a->patch_w &&
+             a->patch_h >= 2 && a->patch_h <= 4) {
+    if (tensor_map_patch(a->out, a->batch, a->out_h, a->out_w, a->n_out, a->out_ld, a->patch_h, 1, &mo) == LAUD_OK)
+      p.tma_out = 2;
+  }
   ProfScope ps(0, st, a->row_mode != ROWS_DENSE ? a->count : nullptr);
   if (ps.on) {
     ps.rec.rows_per_count = a->row_mode == ROWS_PATCH ? (long long)p.patch_h * p.patch_w : 1;
@@ -581,7 +597,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     ps.rec.taps = a->ksize * a->ksize;
     ps.rec.resid = a->resid != nullptr;
   }
-  return cuda_check(launch_conv_gemm(ma, m, bn, p, num_sms(), st, pair), "conv_gemm launch", 1);
+  return cuda_check(launch_conv_gemm(ma, m, mo, bn, p, num_sms(), st, pair), "conv_gemm launch", 1);
 }
 
 }  // namespace

@@ -4,12 +4,13 @@
 
 namespace laud {
 
-cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, int bn, const ConvParams& p, int num_sms,
-                             cudaStream_t stream, int pair) {
+cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const CUtensorMap& tmap_o, int bn,
+                             const ConvParams& p, int num_sms, cudaStream_t stream, int pair) {
   const int n_tiles = (p.n_out + bn - 1) / bn;
   ConvLaunch c;
   c.tmap_a = &tmap_a;
   c.tmap_b = &tmap;
+  c.tmap_o = &tmap_o;
   c.p = &p;
   c.num_sms = num_sms;
   c.stream = stream;

@@ -166,7 +166,7 @@ enum EpMode { EP_PLAIN = 0, EP_ANY = 1, EP_PLAIN_RES = 2, EP_PLAIN_RELU = 4, EP_
 template <int BN, int STAGES, int NSTG, bool PAIR, int AM, int EP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                     const ConvParams p) {
+                     const __grid_constant__ CUtensorMap tmap_o, const ConvParams p) {
   using L = Smem<BN, STAGES, NSTG, PAIR>;
   // PAIR: a cluster of 2 CTAs on one TPC runs M = 256 tiles with
   // tcgen05.mma.cta_group::2 issued by the leader (rank 0); each CTA loads
@@ -629,9 +629,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // one staging buffer per group; with one group and two buffers the next
     // tile's residual is prefetched into the other buffer
     constexpr bool kDoubleStage = NSTG == 2 && L::EG == 1;
-    const int stg_off0 = L::STG_OFF + grp * L::STG_BUF + q * 32 * L::STG_ROW + col0 * 2;
+    // swizzled staging is slice-major: each warp column slice owns BM rows of
+    // 128 B (chunk c of row r at c ^ (r & 7): the TMA SWIZZLE_128B layout, so a
+    // slice's rows can leave by TMA store boxes); unswizzled: row-major rows
+    constexpr int SROW = L::STG_SWZ ? EW_COLS * 2 : L::STG_ROW;
+    const int stg_off0 = L::STG_OFF + grp * L::STG_BUF +
+                         (L::STG_SWZ ? (col0 / EW_COLS) * BM * SROW + q * 32 * SROW : q * 32 * SROW + col0 * 2);
     // byte offset of 16-byte chunk c of slice row r (relative to stg_off0)
-    auto soff = [](int r, int c) { return r * L::STG_ROW + ((L::STG_SWZ ? (c ^ (r & 7)) : c) << 4); };
+    auto soff = [](int r, int c) { return r * SROW + ((L::STG_SWZ ? (c ^ (r & 7)) : c) << 4); };
     float* const vsc = reinterpret_cast<float*>(base + L::VEC_OFF) + ew * 3 * EW_COLS;
     float* const vbi_w = vsc + EW_COLS;
     float* const vnw = vbi_w + EW_COLS;  // next block's masker weights (masker-conv3 fusion)
@@ -644,6 +649,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool has_scale = p.scale != nullptr || p.col_index != nullptr;
     // the common epilogues (bias [+ residual] [+ ReLU]) take a branch-free path
     constexpr bool kPlain = EP != EP_ANY;  // host: plain && cached && full slices
+    const bool tma_out = kPlain && L::STG_SWZ && p.tma_out != 0;
     const bool plain = kPlain || (staged && !has_scale && !p.ymask_coarse && !p.mdot_w);
     // the whole bias vector lives in smem for the kernel when it fits (the
     // per-warp vector slices are the fallback for scale / masker-dot / lists)
@@ -684,6 +690,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       return ri;
     };
     auto prefetch = [&](int t, const RowInfo& ri, int buf) {
+      if (tma_out) {  // the buffer's previous TMA store must have read its rows
+        bulk_wait_read<0>();
+        __syncwarp();
+      }
+      if (p.dbg & 64) {  // ablation: no residual loads
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        return;
+      }
       const int c_base = (t % n_tiles) * BN + col0;
       const int vchunks = max(0, min(EW_COLS, p.n_out - c_base)) >> 3;
       const uint32_t sbase = base_u32 + stg_off0 + buf * L::STG_BUF;
@@ -785,6 +799,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (trc && ew == 0 && lane == 0 && local < 1024) trc[TRACE_EPI + 4 * local] = global_ns();
       tc_fence_after();
       if (pre) asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if (tma_out) bulk_wait_read<0>();  // staging rows of an earlier TMA store are free
       __syncwarp();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col0;
       auto slot_of = [&](int cl) { return reinterpret_cast<uint4*>(stg + soff(lane, cl >> 3)); };
@@ -959,7 +974,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // with two staging buffers the next residual streams in now
         if (pre && kDoubleStage) prefetch(tn, nxt, (local + 1) & 1);
       }
-      if (staged && vchunks > 0 && !(p.dbg & 2)) {
+      if (tma_out && vchunks > 0 && !(p.dbg & 2)) {
+        // the warp's 32 staged rows leave as TMA boxes: one 32-row box (dense
+        // rows) or one S x S pixel box per active patch (scattered patches)
+        fence_proxy_async_smem();
+        __syncwarp();
+        const uint32_t sl = base_u32 + stg_off0 + buf * L::STG_BUF;
+        if (p.tma_out == 1) {
+          if (lane == 0) tma_store_2d(&tmap_o, sl, c_base, (t / n_tiles) * MT + rank * BM + q * 32);
+        } else if (cur.valid && lane % (p.patch_h * p.patch_w) == 0) {
+          int y = cur.rp.y;
+          if (p.misplace_first && cur.fp) y = (y + p.patch_h) % p.out_h;
+          tma_store_4d(&tmap_o, sl + lane * SROW, c_base, cur.rp.x, y, cur.rp.n);
+        }
+        bulk_commit();
+      } else if (staged && vchunks > 0 && !(p.dbg & 2)) {
         // row-major sweep of the staged 32 x EW_COLS slice: each instruction
         // writes 32 / CPR whole row segments
         constexpr int RPI = 32 / CPR;  // rows per warp instruction
@@ -981,6 +1010,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       cur = nxt;
       t = tn;
     }
+    if (tma_out) bulk_wait_all();  // stores done before the CTA's shared memory goes away
   }
 
   tc_fence_before();
@@ -1002,7 +1032,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ---------------------------------------------------------------------------
 
 template <int BN, int STAGES, int NSTG, bool PAIR = false, int AM = AM_ANY, int EP = EP_ANY>
-static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const ConvParams& p, int tiles_max,
+static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap, const CUtensorMap& tmap_o,
+                             const ConvParams& p, int tiles_max,
                              int num_sms, cudaStream_t stream) {
   using L = Smem<BN, STAGES, NSTG, PAIR>;
   static_assert(L::ALLOC <= 227 * 1024, "shared memory budget");
@@ -1037,9 +1068,9 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kern, tmap_a, tmap, p);
+    return cudaLaunchKernelEx(&cfg, kern, tmap_a, tmap, tmap_o, p);
   } else {
-    return launch_k(kern, dim3(grid), dim3(NUM_THREADS), L::ALLOC, stream, tmap_a, tmap, p);
+    return launch_k(kern, dim3(grid), dim3(NUM_THREADS), L::ALLOC, stream, tmap_a, tmap, tmap_o, p);
   }
 }
 
@@ -1048,6 +1079,7 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
 struct ConvLaunch {
   const CUtensorMap* tmap_a;
   const CUtensorMap* tmap_b;
+  const CUtensorMap* tmap_o;  // output rows for the TMA-store epilogue (ConvParams::tma_out)
   const ConvParams* p;
   int tiles_max, num_sms, am;
   bool ep_plain, relu_all;
@@ -1055,12 +1087,12 @@ struct ConvLaunch {
 };
 
 #define LAUD_LB(B, S, N, A)                                                                                     \
-  (!c.ep_plain ? launch_bn<B, S, N, false, A, EP_ANY>(*c.tmap_a, *c.tmap_b, *c.p, c.tiles_max, c.num_sms, c.stream) \
+  (!c.ep_plain ? launch_bn<B, S, N, false, A, EP_ANY>(*c.tmap_a, *c.tmap_b, *c.tmap_o, *c.p, c.tiles_max, c.num_sms, c.stream) \
    : c.p->resid                                                                                                 \
-       ? (c.relu_all ? launch_bn<B, S, N, false, A, EP_PLAIN_RES_RELU>(*c.tmap_a, *c.tmap_b, *c.p, c.tiles_max, c.num_sms, c.stream) \
-                     : launch_bn<B, S, N, false, A, EP_PLAIN_RES>(*c.tmap_a, *c.tmap_b, *c.p, c.tiles_max, c.num_sms, c.stream))   \
-       : (c.relu_all ? launch_bn<B, S, N, false, A, EP_PLAIN_RELU>(*c.tmap_a, *c.tmap_b, *c.p, c.tiles_max, c.num_sms, c.stream)     \
-                     : launch_bn<B, S, N, false, A, EP_PLAIN>(*c.tmap_a, *c.tmap_b, *c.p, c.tiles_max, c.num_sms, c.stream)))
+       ? (c.relu_all ? launch_bn<B, S, N, false, A, EP_PLAIN_RES_RELU>(*c.tmap_a, *c.tmap_b, *c.tmap_o, *c.p, c.tiles_max, c.num_sms, c.stream) \
+                     : launch_bn<B, S, N, false, A, EP_PLAIN_RES>(*c.tmap_a, *c.tmap_b, *c.tmap_o, *c.p, c.tiles_max, c.num_sms, c.stream))   \
+       : (c.relu_all ? launch_bn<B, S, N, false, A, EP_PLAIN_RELU>(*c.tmap_a, *c.tmap_b, *c.tmap_o, *c.p, c.tiles_max, c.num_sms, c.stream)     \
+                     : launch_bn<B, S, N, false, A, EP_PLAIN>(*c.tmap_a, *c.tmap_b, *c.tmap_o, *c.p, c.tiles_max, c.num_sms, c.stream)))
 #define LAUD_BN_DISPATCH(B, S, N)                             \
   switch (c.am) {                                             \
     case AM_TILE: return LAUD_LB(B, S, N, AM_TILE);           \

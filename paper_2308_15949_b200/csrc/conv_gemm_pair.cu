@@ -8,11 +8,11 @@ cudaError_t launch_conv_pair(const ConvLaunch& c, int pair) {
   const ConvParams& p = *c.p;
   if (!p.a_tile || p.adot_out) return cudaErrorInvalidValue;  // pairs: TMA-box A rows, no masker readers
   if (pair == 2)
-    return !c.ep_plain ? launch_bn<256, 2, 2, true, AM_TILE, EP_ANY>(*c.tmap_a, *c.tmap_b, p, c.tiles_max, c.num_sms, c.stream)
-           : p.resid   ? launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN_RES>(*c.tmap_a, *c.tmap_b, p, c.tiles_max, c.num_sms, c.stream)
-                       : launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN>(*c.tmap_a, *c.tmap_b, p, c.tiles_max, c.num_sms, c.stream);
-  return !c.ep_plain ? launch_bn<256, 4, 1, true, AM_TILE, EP_ANY>(*c.tmap_a, *c.tmap_b, p, c.tiles_max, c.num_sms, c.stream)
-         : p.resid   ? launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN_RES>(*c.tmap_a, *c.tmap_b, p, c.tiles_max, c.num_sms, c.stream)
-                     : launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN>(*c.tmap_a, *c.tmap_b, p, c.tiles_max, c.num_sms, c.stream);
+    return !c.ep_plain ? launch_bn<256, 2, 2, true, AM_TILE, EP_ANY>(*c.tmap_a, *c.tmap_b, *c.tmap_o, p, c.tiles_max, c.num_sms, c.stream)
+           : p.resid   ? launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN_RES>(*c.tmap_a, *c.tmap_b, *c.tmap_o, p, c.tiles_max, c.num_sms, c.stream)
+                       : launch_bn<256, 2, 2, true, AM_TILE, EP_PLAIN>(*c.tmap_a, *c.tmap_b, *c.tmap_o, p, c.tiles_max, c.num_sms, c.stream);
+  return !c.ep_plain ? launch_bn<256, 4, 1, true, AM_TILE, EP_ANY>(*c.tmap_a, *c.tmap_b, *c.tmap_o, p, c.tiles_max, c.num_sms, c.stream)
+         : p.resid   ? launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN_RES>(*c.tmap_a, *c.tmap_b, *c.tmap_o, p, c.tiles_max, c.num_sms, c.stream)
+                     : launch_bn<256, 4, 1, true, AM_TILE, EP_PLAIN>(*c.tmap_a, *c.tmap_b, *c.tmap_o, p, c.tiles_max, c.num_sms, c.stream);
 }
 }  // namespace laud

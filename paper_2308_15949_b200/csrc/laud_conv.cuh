@@ -44,6 +44,7 @@ struct ConvParams {
   // (= per dense input pixel) into adot_out[row]; the decision pass sums the
   // cell windows in a fixed order
   const float* adot_w;
+  int tma_out;  // kPlain epilogues: 1 = dense rows stored as 32-row TMA boxes, 2 = S x S patch boxes (4D)
   float* adot_out;
   int a_rows;            // rows of the A tensor map (also the out-of-bounds marker)
   int ksize, stride, pad;
