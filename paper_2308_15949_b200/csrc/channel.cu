@@ -102,7 +102,19 @@ __global__ void __launch_bounds__(CM_THREADS) channel_masker_kernel(
   // hidden = relu(W1 gap): one warp per hidden unit
   for (int j = warp; j < hd; j += blockDim.x / 32) {
     float s = 0.f;
-    for (int i = lane; i < c; i += 32) s = fmaf(w1[(size_t)j * c + i], gap[i], s);
+    for (int i0 = 0; i0 < c; i0 += 32 * 8) {  // eight weight loads per lane in flight, FMAs in i order
+      float wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + lane + 32 * u;
+        wv[u] = i < c ? __ldg(w1 + (size_t)j * c + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + lane + 32 * u;
+        if (i < c) s = fmaf(wv[u], gap[i], s);
+      }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) hid[j] = fmaxf(s, 0.f);
@@ -111,9 +123,21 @@ __global__ void __launch_bounds__(CM_THREADS) channel_masker_kernel(
   // logit pair dd = (W2[2dd] h, W2[2dd+1] h); keep iff l0 >= l1
   for (int dd = tid; dd < d; dd += blockDim.x) {
     float l0 = 0.f, l1 = 0.f;
-    for (int j = 0; j < hd; ++j) {
-      l0 = fmaf(w2[(size_t)(2 * dd) * hd + j], hid[j], l0);
-      l1 = fmaf(w2[(size_t)(2 * dd + 1) * hd + j], hid[j], l1);
+    for (int j0 = 0; j0 < hd; j0 += 8) {  // the two rows' loads batched, FMAs in j order
+      float u0[8], u1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u;
+        u0[u] = j < hd ? __ldg(w2 + (size_t)(2 * dd) * hd + j) : 0.f;
+        u1[u] = j < hd ? __ldg(w2 + (size_t)(2 * dd + 1) * hd + j) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u < hd) {
+          l0 = fmaf(u0[u], hid[j0 + u], l0);
+          l1 = fmaf(u1[u], hid[j0 + u], l1);
+        }
+      }
     }
     const float diff = l0 - l1 + (bias ? bias[dd] : 0.f);  // EXT bias (calibration)
     dl[dd] = diff;
