@@ -48,6 +48,8 @@ def shape_defs():
     d["pconv_s2_all_s4"] = dict(kind="patch", n=256, h=28, c=128, s=4, density=1.0)
     d["pconv_s3_all"] = dict(kind="patch", n=256, h=14, c=256, s=2, density=1.0)
     d["conv3_s1"] = dict(kind="conv3", m=256 * 56 * 56 // 2, n=256, k=64)
+    # stage-1 b0 downsample (64 -> 256 over every pixel): a pure output stream
+    d["ds_s1"] = dict(kind="gemm", m=256 * 56 * 56, n=256, k=64)
     # RegNetY-1.6GF at batch 1024: the 112x112 stage-1 b0 conv1 (32 -> 48) and a
     # stage-3 1x1 (336 -> 336) — small-K / small-N streaming convs
     d["rg_s1_conv1"] = dict(kind="gemm", m=1024 * 112 * 112, n=48, k=32)
