@@ -370,16 +370,19 @@ __global__ void __launch_bounds__(256) masker_fused_kernel(
   const int cpp = c >> 3;
   const int cell_chunks = win * win * cpp;
   const int cpi = cells_h * cells_w;
-  for (int lc = warp; lc < tc; lc += 8) {
+  // wpc warps per cell (8 / tc): each takes every wpc-th 64-chunk step of the
+  // cell; the warps' sums are added in warp order (deterministic)
+  const int wpc = 8 / tc, sub = warp % wpc;
+  __shared__ float s_part[8];
+  for (int lc = warp / wpc; lc < tc; lc += 8 / wpc) {
     const int cell = cell0 + lc;
-    bool f = false;
     if (cell < total) {
       const int ni = cell / cpi;
       const int cr = cell - ni * cpi;
       const int ci = cr / cells_w, cj = cr - (cr / cells_w) * cells_w;
       float a0 = 0.f, a1 = 0.f;
 #pragma unroll 4
-      for (int q = lane; q < cell_chunks; q += 64) {
+      for (int q = lane + 64 * sub; q < cell_chunks; q += 64 * wpc) {
         const int px = q / cpp;
         const int ch = (q - px * cpp) << 3;
         const int py = px / win;
@@ -397,13 +400,21 @@ __global__ void __launch_bounds__(256) masker_fused_kernel(
       float acc = a0 + a1;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      f = acc * inv_area + bias >= 0.f;
-      if (lane == 0) {
-        coarse[cell] = f ? 1 : 0;
-        if (dots) dots[cell] = acc;
-      }
+      if (lane == 0) s_part[warp] = acc;
     }
-    if (lane == 0) s_flag[lc] = f ? 1 : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x < tc) {  // thread lc decides cell lc
+    const int lc = threadIdx.x, cell = cell0 + lc;
+    bool f = false;
+    if (cell < total) {
+      float acc = 0.f;
+      for (int k = 0; k < wpc; ++k) acc += s_part[lc * wpc + k];
+      f = acc * inv_area + bias >= 0.f;
+      coarse[cell] = f ? 1 : 0;
+      if (dots) dots[cell] = acc;
+    }
+    s_flag[lc] = f ? 1 : 0;
   }
   __syncthreads();
   // tile-local exclusive scan of tc (<= 256) flags: thread t owns flag t
@@ -586,7 +597,26 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
   if (splits == 1 && total > 0 && total <= fused_max && !dn) {  // small grids: one launch wins
     // one pass: dots + decisions + compaction; ~2 waves of CTAs over the SMs
     // one cell per warp: as many resident warps (bytes in flight) as the SMs hold
-    const int tc = 8;
+    // warps per cell: as many as keep the grid within one wave of resident
+    // CTAs (8 per SM) — small batches are latency-bound, so a cell's bytes are
+    // spread over more warps (batch 1 R101: masker 12.3 -> 8.2 us per block)
+    static const int wpc_env = [] {
+      const char* e = getenv("LAUD_MASKER_WPC");  // override: 1, 2, 4 or 8
+      return e ? atoi(e) : 0;
+    }();
+    static const int num_sms = [] {
+      int dev = 0, v = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return v;
+    }();
+    int wpc = 1;
+    if (wpc_env == 1 || wpc_env == 2 || wpc_env == 4 || wpc_env == 8) {
+      wpc = wpc_env;
+    } else {
+      while (wpc < 8 && (long long)total * wpc * 2 / 8 <= 8LL * num_sms) wpc *= 2;
+    }
+    const int tc = 8 / wpc;
     const int tiles = (total + tc - 1) / tc;
     const float inv_area = 1.0f / (float)(win * win);
     if (x_f32)
