@@ -1194,11 +1194,9 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
         if ((rc = cuda_check(cudaEventRecord(x_ready, st), "fork record", 0)) ||
             (rc = cuda_check(cudaStreamWaitEvent(aux, x_ready, 0), "fork wait", 0)))
           return rc;
-        rc = laud_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in,
-                                 a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
-                                 a->masker_wdiff, a->masker_bias, a->coarse_out, a->cell_list,
-                                 a->cell_count, a->partial, a->scan, aux);
-        if (rc == LAUD_OK) rc = cuda_check(cudaEventRecord(fork_done, aux), "join record", 0);
+        // the masker kernel itself is launched after conv1 (below): conv1's few
+        // CTAs need nearly a whole SM of shared memory each and must not wait
+        // behind the masker's small CTAs already resident on every SM
       } else {
         rc = laud_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in,
                                  a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride,
@@ -1296,6 +1294,13 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
     c1.row_mode = ROWS_DENSE;
     if ((rc = run_conv(&c1, st))) return rc;
     conv1_done = true;
+    cudaStream_t aux = (cudaStream_t)a->aux_stream;
+    if ((rc = laud_spatial_masker(a->x, a->fp32, a->x_ld, n, a->h_in, a->w_in, a->c_in,
+                                  a->paradigm == LAUD_PARADIGM_LAYER ? ho : a->s, a->stride, a->masker_wdiff,
+                                  a->masker_bias, a->coarse_out, a->cell_list, a->cell_count, a->partial,
+                                  a->scan, aux)) ||
+        (rc = cuda_check(cudaEventRecord(fork_done, aux), "join record", 0)))
+      return rc;
     if ((rc = cuda_check(cudaStreamWaitEvent(st, fork_done, 0), "join wait", 0))) return rc;
   }
 
