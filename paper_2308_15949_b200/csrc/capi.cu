@@ -556,6 +556,30 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
   const bool pair_ok = pair_env && bn == 256 && p.a_tile && !a->sample_rows && !a->chan_count && !a->b_gather &&
                        !a->b_batched && p.groups == 1 && pair_tiles >= num_sms() / 2;
   const int pair = (!pair_ok || ad) ? 0 : (kw >= 1024 ? 1 : (kw <= 512 && (pair_env & 2) ? 2 : 0));
+  // small grids (latency_split): cluster split-K for the plain epilogues — the
+  // KS CTAs of a cluster take K slices of one tile, partials reduced over DSMEM
+  {
+    static const int gks_env = [] {
+      const char* e = getenv("LAUD_GEMM_KSPLIT_MAX");
+      return e ? atoi(e) : 8;
+    }();
+    // the split is sized as for a batch of at least 8, so every batch of up to 8
+    // images runs the same K slices: the per-row arithmetic (and so the masker
+    // decisions downstream) does not depend on how images are batched
+    const long long rows_b8 = a->batch > 0 && a->batch < 8 ? (long long)a->rows_max / a->batch * 8 : a->rows_max;
+    const long long g_tiles = ((rows_b8 + 127) / 128) * ((a->n_out + bn - 1) / bn);
+    const int g_kb = a->ksize * a->ksize * (p.kpad / 64);
+    const int npad = (a->n_out + bn - 1) / bn * bn;
+    const bool plain = !a->out_f32 && !a->scale && !a->col_index && !a->ymask_coarse && !a->mdot_w &&
+                       !a->ymask_channel && !a->relu_inactive_coarse && npad <= 12 * bn;
+    if (gks_env > 1 && a->latency_split && !pair && !ad && plain && !a->b_gather && !a->chan_count &&
+        !a->sample_rows && p.groups == 1)
+      for (int k = gks_env >= 8 ? 8 : gks_env >= 4 ? 4 : 2; k >= 2; k >>= 1)
+        if (g_tiles * k <= num_sms() && g_kb >= 2 * k) {
+          p.ksplit = k;
+          break;
+        }
+  }
   if (ad) {  // fused masker readers need single-CTA tiles with contiguous (TMA box) A rows
     if (!p.a_tile) return LAUD_ADOT_UNAVAILABLE;
     p.adot_w = ad->w;
@@ -1261,6 +1285,7 @@ int laud_block_forward(const laud_block_args* a, void* stream) {
   c1.out = a->h1;
   c1.out_ld = a->c_mid;
   c1.rows_max = n * a->h_in * a->w_in;
+  c1.latency_split = a->latency_split;
   bool conv1_done = false;
   if (fuse_masker) {
     // per-pixel masker dots stored by conv1's readers, then decisions + the

@@ -23,6 +23,8 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
                npad <= 12 * bn && (p.n_out % bn == 0 || !p.ymask_channel) &&
                (!p.adot_out || npad + p.kpad <= 12 * bn);  // + masker weights in smem
   c.relu_all = p.relu && !p.relu_inactive_coarse;
+  if (p.ksplit > 1 && (!c.ep_plain || pair || p.adot_out || p.ymask_channel || p.relu_inactive_coarse))
+    return cudaErrorInvalidValue;  // split-K runs only the plain epilogues (host-checked)
   c.am = p.a_tile ? (p.adot_out ? AM_TILE_DOT : AM_TILE) : p.a_box ? AM_BOX : p.a_tma ? AM_G4 : AM_ANY;
   if (pair) {
     if (bn != 256) return cudaErrorInvalidValue;

@@ -98,6 +98,7 @@ __device__ __forceinline__ bool map_row_raw(const ConvParams& p, int m, int nval
 // Per-tile schedule shared by every warp role (all roles skip the same tiles).
 struct TileInfo {
   int m0, n0, sample, kpt, num_kb, kc;
+  int kb_lo, kb_hi;  // this CTA's k-blocks (all; or its slice under cluster split-K)
   int c_lo;  // first input channel of the tile's K window (grouped convs)
   bool skip;
 };
@@ -119,6 +120,13 @@ __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int t, int n_
     ti.kpt = ((g1 - g0) * p.gw_in + BK - 1) / BK;
   }
   ti.num_kb = p.ksize * p.ksize * ti.kpt;
+  ti.kb_lo = 0;
+  ti.kb_hi = ti.num_kb;
+  if (!PAIR && p.ksplit > 1) {  // small grids: CTA ks of the cluster takes K slice ks
+    const int ks = (int)cluster_ctarank();
+    ti.kb_lo = ks * ti.num_kb / p.ksplit;
+    ti.kb_hi = (ks + 1) * ti.num_kb / p.ksplit;
+  }
   return ti;
 }
 
@@ -172,8 +180,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // tcgen05.mma.cta_group::2 issued by the leader (rank 0); each CTA loads
   // its 128 A rows and half of B, so per-SM operand traffic per MMA halves.
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
-  const int t_begin = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  // cluster split-K (small grids, plain epilogues): the KS CTAs of a cluster
+  // share one tile, each a slice of its k-blocks; fp32 partials are reduced
+  // through distributed shared memory after the role loops
+  constexpr bool kSplitOK = !PAIR && EP != EP_ANY && BM * (BN + 4) * 4 <= L::STG_OFF;  // partials fit the stages
+  const int KS = (kSplitOK && p.ksplit > 1) ? p.ksplit : 1;
+  const int t_begin = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / KS;
+  const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x / KS;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base_u32 = (raw_u32 + 1023u) & ~1023u;
@@ -267,7 +280,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (ti.skip) continue;
         float aa[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};  // 4-way ILP per row
         const bool dots = ti.n0 == 0;  // every N tile re-reads the rows: dot them once
-        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+        for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&full[stage], phase);
@@ -326,7 +339,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int row0 = p.sample_rows > 0
                                ? ti.sample * p.out_h * p.out_w + (ti.m0 - ti.sample * p.sample_rows)
                                : ti.m0;
-          for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+          for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
             const int stage = it % STAGES;
             const uint32_t phase = (it / STAGES) & 1;
             mbar_wait(&empty[stage], phase ^ 1);
@@ -363,7 +376,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           by = ci * p.patch_h * p.stride - p.pad;
           bx = cj * p.patch_w * p.stride - p.pad;
         }
-        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+        for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -387,7 +400,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         RowPos rp;
         bool fp;
         const bool rv = map_row(p, m0 + tid, nvalid, rp, fp);
-        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+        for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -435,7 +448,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         bool fp;
         rv[i] = map_row(p, m0 + rsub + 16 * i, nvalid, rp[i], fp);
       }
-      for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+      for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
         const int stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
         mbar_wait(&empty[stage], phase ^ 1);
@@ -480,10 +493,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (ti.skip) continue;
         const int* idx = p.b_index + (size_t)ti.sample * p.b_index_ld;
         const bool gn = p.b_gather == B_GATHER_N;
-        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+        for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
-          if (gn ? kb == 0 : true) {
+          if (gn ? kb == ti.kb_lo : true) {
             // N gather: the tile's BN rows once per tile; K gather: this k-block's 64 K rows
             __syncwarp();
             const int cnt = gn ? BN : BK, off = gn ? ti.n0 : kb * BK;
@@ -524,7 +537,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = t_begin; t < tiles; t += t_step) {
         const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
         if (ti.skip) continue;
-        for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+        for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -570,7 +583,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
-      for (int kb = 0; kb < ti.num_kb; ++kb, ++it) {
+      for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb, ++it) {
         const int stage = it % STAGES;
         const uint32_t phase = (it / STAGES) & 1;
         mbar_wait(&full[stage], phase);
@@ -584,11 +597,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             if constexpr (PAIR)
               umma_bf16_pair(tmem_d, umma_sdesc_sw128(sA + k * 32), umma_sdesc_sw128(sB + k * 32), idesc,
-                             (kb | k) != 0);
+                             kb != ti.kb_lo || k != 0);
             else
               umma_bf16(tmem_d, umma_sdesc_sw128(sA + k * 32),
                         b_mn ? umma_sdesc_sw128_mn(sB + k * 2048, 8192) : umma_sdesc_sw128(sB + k * 32), idesc,
-                        (kb | k) != 0);
+                        kb != ti.kb_lo || k != 0);
           }
           if constexpr (PAIR)
             umma_commit_pair(&empty[stage]);  // frees the stage in both CTAs
@@ -645,7 +658,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool staged = !p.out_f32;
     constexpr bool kRes = EP == EP_PLAIN_RES || EP == EP_PLAIN_RES_RELU;
     constexpr bool kReluAll = EP == EP_PLAIN_RELU || EP == EP_PLAIN_RES_RELU;
-    const bool pre = EP != EP_ANY ? kRes : (staged && resid != nullptr);
+    const bool pre = (EP != EP_ANY ? kRes : (staged && resid != nullptr)) && KS == 1;  // split-K: resid in the reduction
     const bool has_scale = p.scale != nullptr || p.col_index != nullptr;
     // the common epilogues (bias [+ residual] [+ ReLU]) take a branch-free path
     constexpr bool kPlain = EP != EP_ANY;  // host: plain && cached && full slices
@@ -802,6 +815,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (tma_out) bulk_wait_read<0>();  // staging rows of an earlier TMA store are free
       __syncwarp();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col0;
+      if (KS > 1) {
+        // split-K: this CTA's fp32 partial of its rows -> its own operand smem
+        // (every MMA of the tile has completed); reduced after the role loops
+        float* prow = reinterpret_cast<float*>(base + L::A_OFF) + (size_t)(q * 32 + lane) * (BN + 4) + col0;
+#pragma unroll 1
+        for (int j = 0; j < EW_COLS / CH; ++j) {
+          uint32_t r[CH];
+          tmem_ld_32x32b<CH>(tbase + j * CH, r);
+#pragma unroll
+          for (int e = 0; e < CH; e += 4)
+            *reinterpret_cast<float4*>(prow + j * CH + e) = make_float4(
+                __uint_as_float(r[e]), __uint_as_float(r[e + 1]), __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+        }
+        break;  // one tile per cluster
+      }
       auto slot_of = [&](int cl) { return reinterpret_cast<uint4*>(stg + soff(lane, cl >> 3)); };
       // generic 8-column step: affine, masks, residual, ReLU, store
       auto finish8 = [&](const uint32_t* rv, int cl) {
@@ -918,7 +946,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int j = 0; j < EW_COLS / CH; ++j) {
         if (j * CH >= nch) break;
         uint32_t r[CH];
-        if (ti.num_kb > 0 && !(p.dbg & 4)) {
+        if (ti.kb_hi > ti.kb_lo && !(p.dbg & 4)) {
           tmem_ld_32x32b<CH>(tbase + j * CH, r);
         } else {  // empty K (no channel kept): y = 0
 #pragma unroll
@@ -1013,6 +1041,73 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (tma_out) bulk_wait_all();  // stores done before the CTA's shared memory goes away
   }
 
+  if (KS > 1) {
+    // split-K reduction through distributed shared memory: CTA ks finishes rows
+    // [ks*BM/KS, (ks+1)*BM/KS) of the cluster's tile, adding the KS partials in
+    // rank order (deterministic), then bias [+ residual] [+ ReLU] and the store
+    cluster_sync();
+    const int t = t_begin;
+    if (warp >= FIRST_EPI && t < tiles) {
+      const TileInfo ti = tile_info<BN, PAIR>(p, t, n_tiles, rank);
+      const int ks = (int)cluster_ctarank();
+      const int rows = BM / KS, r0 = ks * rows;
+      const float* bias_cache = reinterpret_cast<const float*>(base + L::VEC_OFF);
+      const __nv_bfloat16* resid = reinterpret_cast<const __nv_bfloat16*>(p.resid);
+      __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(p.out);
+      constexpr bool kRes = EP == EP_PLAIN_RES || EP == EP_PLAIN_RES_RELU;
+      const bool relu = EP == EP_PLAIN_RELU || EP == EP_PLAIN_RES_RELU || p.relu != 0;
+      const uint32_t part0 = base_u32 + L::A_OFF;
+      for (int item = threadIdx.x - FIRST_EPI * 32; item < rows * (BN / 8); item += NUM_EPI_WARPS * 32) {
+        const int r = r0 + item / (BN / 8), c8 = item % (BN / 8);
+        const int col = ti.n0 + c8 * 8;
+        if (col >= p.n_out) continue;
+        const int m = ti.m0 + r;
+        RowPos rp;
+        bool fp;
+        if (!map_row_raw(p, m, nvalid, row_fetch(p, m), rp, fp)) continue;
+        long long dst = m;
+        if (p.out_mode != OUT_ROW) {
+          int y = rp.y;
+          if (p.misplace_first && fp) y = (y + p.patch_h) % p.out_h;
+          dst = (long long)(rp.n * p.out_h + y) * p.out_w + rp.x;
+        }
+        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const uint32_t off = (uint32_t)((r * (BN + 4) + c8 * 8) * 4);
+        for (int k = 0; k < KS; ++k) {
+          float4 a, b;
+          const uint32_t ad = mapa_shared(part0 + off, (uint32_t)k);
+          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(ad));
+          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "r"(ad + 16u));
+          v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+          v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += bias_cache[col + e];
+        if (kRes) {
+          const uint4 rr = *reinterpret_cast<const uint4*>(resid + dst * p.resid_ld + col);
+          float2 f;
+          f = unpack_bf16x2(rr.x); v[0] += f.x; v[1] += f.y;
+          f = unpack_bf16x2(rr.y); v[2] += f.x; v[3] += f.y;
+          f = unpack_bf16x2(rr.z); v[4] += f.x; v[5] += f.y;
+          f = unpack_bf16x2(rr.w); v[6] += f.x; v[7] += f.y;
+        }
+        if (relu) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+        }
+        uint4 w;
+        w.x = pack_bf16x2(v[0], v[1]);
+        w.y = pack_bf16x2(v[2], v[3]);
+        w.z = pack_bf16x2(v[4], v[5]);
+        w.w = pack_bf16x2(v[6], v[7]);
+        *reinterpret_cast<uint4*>(outp + dst * p.out_ld + col) = w;
+      }
+    }
+    cluster_sync();  // peers done reading this CTA's partials
+  }
+
   tc_fence_before();
   if constexpr (PAIR)
     cluster_sync();  // the peer's smem / barriers must outlive the leader's last use
@@ -1053,6 +1148,25 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   int grid = tiles_max < units ? tiles_max : units;
   if (grid_env > 0 && grid > grid_env) grid = grid_env;
   if (grid < 1) grid = 1;
+  if (!PAIR && p.ksplit > 1) {  // cluster split-K: one tile per cluster of ksplit CTAs
+    if (EP == EP_ANY || BM * (BN + 4) * 4 > L::STG_OFF || tiles_max * p.ksplit > num_sms)
+      return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tiles_max * p.ksplit, 1, 1);
+    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = L::ALLOC;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.ksplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kern, tmap_a, tmap, tmap_o, p);
+  }
   if constexpr (PAIR) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * grid, 1, 1);

@@ -130,6 +130,51 @@ def test_patch_conv_halo_smem(s, cin, cout, n, h, density, split):
     assert err < 6e-3, float(err)
 
 
+@pytest.mark.parametrize("kind,cin,cout,k,stride,n,h", [
+    ("dense", 2048, 512, 1, 1, 1, 7), ("dense", 1024, 256, 1, 1, 1, 14), ("resid", 128, 512, 1, 1, 1, 7),
+    ("dense", 256, 512, 3, 2, 1, 14), ("dense", 128, 128, 3, 2, 2, 28), ("pixels", 512, 512, 3, 1, 1, 7),
+    ("pixels", 256, 256, 3, 1, 2, 14), ("dense", 64, 64, 3, 1, 1, 8)])
+@pytest.mark.parametrize("split", [0, 1])
+def test_engine_cluster_split_k(kind, cin, cout, k, stride, n, h, split):
+    """Small-grid cluster split-K of the implicit-GEMM engine (latency_split, plain
+    epilogues): the K slices' fp32 partials reduced over distributed shared memory
+    then bias [+ residual] + ReLU — dense 1x1 / strided 3x3 rows and an active-pixel
+    list (S = 1 patches, the stage-4 LAUD conv2), vs torch fp32; split and unsplit agree."""
+    CH, D = _engine()
+    g = torch.Generator().manual_seed(cin + cout + k + n + h)
+    x = torch.randn(n, h, h, cin, generator=g).cuda().to(torch.bfloat16)
+    w = (torch.randn(cout, cin, k, k, generator=g) / np.sqrt(k * k * cin)).to(torch.bfloat16).float()
+    bi = torch.randn(cout, generator=g) * 0.1
+    pad = k // 2
+    ho = (h + 2 * pad - k) // stride + 1
+    ref = _torch_conv_nhwc(x, w.cuda(), stride, pad) + bi.cuda()
+    kw = dict(act=x, in_hw=(h, h), in_c=cin, in_ld=cin, weight=D.pack_weight(w, cin), n_out=cout, out_ld=cout,
+              out_hw=(ho, ho), batch=n, ksize=k, stride=stride, pad=pad, bias=bi.cuda(), relu=1,
+              latency_split=split)
+    if kind == "pixels":
+        rng = np.random.default_rng(h)
+        pix = np.flatnonzero(rng.random(n * ho * ho) < 0.5).astype(np.int32)
+        lst = torch.from_numpy(np.concatenate([pix, np.zeros(4, np.int32)])).cuda()
+        cnt = torch.tensor([len(pix)], dtype=torch.int32, device="cuda")
+        out = torch.full((len(pix), cout), 7.0, dtype=torch.bfloat16, device="cuda")
+        CH.conv(out=out, row_mode=CH.ROWS_PATCH, rows_max=n * ho * ho, lst=lst, count=cnt, patch=(1, 1),
+                cells=(ho, ho), out_mode=CH.OUT_ROW, **kw)
+        exp = torch.relu(ref).reshape(-1, cout)[torch.from_numpy(pix.astype(np.int64)).cuda()]
+    else:
+        out = torch.empty(n, ho, ho, cout, dtype=torch.bfloat16, device="cuda")
+        if kind == "resid":
+            res = (torch.randn(n, ho, ho, cout, generator=g) * 0.5).cuda().to(torch.bfloat16)
+            out.copy_(res)
+            CH.conv(out=out, resid=out, resid_ld=cout, **kw)
+            exp = torch.relu(ref + res.float())
+        else:
+            CH.conv(out=out, **kw)
+            exp = torch.relu(ref)
+    torch.cuda.synchronize()
+    err = (out.float() - exp).norm() / exp.norm()
+    assert err < 6e-3, float(err)
+
+
 def test_compaction_matches_argwhere():
     from paper_2308_15949_b200 import reference as R
     rng = np.random.default_rng(0)
