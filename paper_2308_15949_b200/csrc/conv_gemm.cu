@@ -15,13 +15,13 @@ cudaError_t launch_conv_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   c.num_sms = num_sms;
   c.stream = stream;
   // EP_PLAIN*: bf16 out, no per-channel scale / coarse mask / masker-dot, bias
-  // vector fits the smem cache (12 * BN floats)
+  // vector fits the smem cache (VEC_CACHE_FLOATS)
   // (a partial last N tile is fine — its extra columns are never stored —
   // except under the per-sample channel mask, read per column)
   const int npad = n_tiles * bn;
   c.ep_plain = !p.out_f32 && !p.scale && !p.col_index && !p.ymask_coarse && !p.mdot_w &&
-               npad <= 12 * bn && (p.n_out % bn == 0 || !p.ymask_channel) &&
-               (!p.adot_out || npad + p.kpad <= 12 * bn);  // + masker weights in smem
+               npad <= VEC_CACHE_FLOATS && (p.n_out % bn == 0 || !p.ymask_channel) &&
+               (!p.adot_out || npad + p.kpad <= VEC_CACHE_FLOATS);  // + masker weights in smem
   c.relu_all = p.relu && !p.relu_inactive_coarse;
   if (p.ksplit > 1 && (!c.ep_plain || pair || p.adot_out || p.ymask_channel || p.relu_inactive_coarse))
     return cudaErrorInvalidValue;  // split-K runs only the plain epilogues (host-checked)

@@ -41,6 +41,9 @@ constexpr int WARP_MMA = 5;
 constexpr int FIRST_EPI = 6;
 constexpr int NUM_EPI_WARPS = LAUD_EPI_WARPS;  // warps 6 .. 6 + NUM_EPI_WARPS - 1
 constexpr int NUM_THREADS = (FIRST_EPI + NUM_EPI_WARPS) * 32;
+// floats of the per-kernel smem vector cache (bias; + masker weights): the
+// epilogue vector region, 3 x 64 floats per epilogue warp for every tile width
+constexpr int VEC_CACHE_FLOATS = NUM_EPI_WARPS * 3 * 64;
 
 // Raw list entry row m depends on (fetched early; map_row_raw resolves it).
 __device__ __forceinline__ int row_fetch(const ConvParams& p, int m) {
@@ -153,6 +156,7 @@ struct Smem {
   static constexpr int VEC_OFF = STG_OFF + NSTG * STG_BUF;  // per-warp scale/bias slices
   static constexpr int EW_COLS = EW_COLS0;  // columns per epilogue warp
   static constexpr int VEC_BYTES = NUM_EPI_WARPS * 3 * EW_COLS * 4;  // scale, bias, next wdiff
+  static_assert(VEC_BYTES / 4 >= VEC_CACHE_FLOATS, "vector cache size");
   static constexpr int BAR_OFF = VEC_OFF + VEC_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 2 * NACC;
   static constexpr int TMEM_SLOT_OFF = BAR_OFF + NUM_BARS * 8;
