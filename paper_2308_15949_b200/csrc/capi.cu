@@ -572,7 +572,7 @@ int run_conv(const laud_conv_args* a, cudaStream_t st, const AdotArgs* ad = null
     const int npad = (a->n_out + bn - 1) / bn * bn;
     const bool plain = !a->out_f32 && !a->scale && !a->col_index && !a->ymask_coarse && !a->mdot_w &&
                        !a->ymask_channel && !a->relu_inactive_coarse && npad <= 3072;  // VEC_CACHE_FLOATS
-    if (gks_env > 1 && a->latency_split && !pair && !ad && plain && !a->b_gather && !a->chan_count &&
+    if (gks_env > 1 && bn == 64 && a->latency_split && !pair && !ad && plain && !a->b_gather && !a->chan_count &&
         !a->sample_rows && p.groups == 1)
       for (int k = gks_env >= 8 ? 8 : gks_env >= 4 ? 4 : 2; k >= 2; k >>= 1)
         if (g_tiles * k <= num_sms() && g_kb >= 2 * k) {

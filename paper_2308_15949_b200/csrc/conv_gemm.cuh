@@ -125,7 +125,7 @@ __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int t, int n_
   ti.num_kb = p.ksize * p.ksize * ti.kpt;
   ti.kb_lo = 0;
   ti.kb_hi = ti.num_kb;
-  if (!PAIR && p.ksplit > 1) {  // small grids: CTA ks of the cluster takes K slice ks
+  if (BN == 64 && !PAIR && p.ksplit > 1) {  // small grids: CTA ks of the cluster takes K slice ks
     const int ks = (int)cluster_ctarank();
     ti.kb_lo = ks * ti.num_kb / p.ksplit;
     ti.kb_hi = (ks + 1) * ti.num_kb / p.ksplit;
@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // cluster split-K (small grids, plain epilogues): the KS CTAs of a cluster
   // share one tile, each a slice of its k-blocks; fp32 partials are reduced
   // through distributed shared memory after the role loops
-  constexpr bool kSplitOK = !PAIR && EP != EP_ANY && BM * (BN + 4) * 4 <= L::STG_OFF;  // partials fit the stages
+  // (64-wide tiles only: the small-grid tile width; wider instantiations carry no split code)
+  constexpr bool kSplitOK = BN == 64 && !PAIR && EP != EP_ANY && BM * (BN + 4) * 4 <= L::STG_OFF;
   const int KS = (kSplitOK && p.ksplit > 1) ? p.ksplit : 1;
   const int t_begin = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / KS;
   const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x / KS;
@@ -1153,7 +1154,7 @@ static cudaError_t launch_bn(const CUtensorMap& tmap_a, const CUtensorMap& tmap,
   if (grid_env > 0 && grid > grid_env) grid = grid_env;
   if (grid < 1) grid = 1;
   if (!PAIR && p.ksplit > 1) {  // cluster split-K: one tile per cluster of ksplit CTAs
-    if (EP == EP_ANY || BM * (BN + 4) * 4 > L::STG_OFF || tiles_max * p.ksplit > num_sms)
+    if (BN != 64 || EP == EP_ANY || BM * (BN + 4) * 4 > L::STG_OFF || tiles_max * p.ksplit > num_sms)
       return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tiles_max * p.ksplit, 1, 1);
