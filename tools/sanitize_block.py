@@ -4,7 +4,8 @@
 Round 2 adds: the small-grid cluster split-K of the halo conv2 (latency_split),
 the masker forked onto a second stream, the grouped halo conv2 (RegNet), the
 gathered-weight channel schedule (LAUD_CH_GATHER=1), both fused stems and the
-split SE FC kernels."""
+split SE FC kernels, the GEMM engine's small-grid split-K (batch-1 static / S = 1 blocks)
+and the TMA-store epilogue."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -16,7 +17,7 @@ from paper_2308_15949_b200.network import make_params
 def main():
     torch.cuda.set_device(0)
     for arch, stage, index, s in (("resnet50", 3, 1, 2), ("resnet50", 2, 0, 2), ("resnet50", 1, 1, 4),
-                                  ("regnety-1.6gf", 3, 1, 2)):
+                                  ("resnet50", 4, 1, 1), ("regnety-1.6gf", 3, 1, 2)):
         bp = [b for b in make_params(arch, 0)["blocks"] if b["stage"] == stage and b["index"] == index][0]
         blk = bp["block"]
         ep = D.Epilogue(s1=bp["s1"], b1=bp["b1"], relu1=True, s2=bp["s2"], b2=bp["b2"], relu2=True,
@@ -31,6 +32,7 @@ def main():
             db.forward(x.clone(), "spatial", s, conv1_dense=dense)
         aux = torch.cuda.Stream()
         db.forward(x[:1].clone(), "spatial", s, conv1_dense=True, aux_stream=aux, latency_split=True)
+        db.forward(x[:1].clone(), "static", latency_split=True)  # GEMM-engine split-K (small grids)
         db.forward(x.clone(), "static")
         db.forward(x.clone(), "layer", coarse=torch.tensor([1, 0], dtype=torch.uint8, device="cuda"))
         db.enable_grouped_channel()  # EXT for grouped conv2 (no-op otherwise)
