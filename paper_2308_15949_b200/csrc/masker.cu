@@ -113,6 +113,57 @@ __global__ void __launch_bounds__(256) cell_dot_kernel(
   if (lane == 0) partial[item] = acc;
 }
 
+// Layer masker (one cell = the whole image; contiguous NHWC rows, C = 256 P):
+// a split is 1024 consecutive 16-byte chunks of the image, so lane l always
+// meets channel chunk l + 32 j at step j mod P — the weights stay in
+// registers, no index arithmetic per load, P independent accumulators added
+// in j order at the end (deterministic).
+template <int P>
+__global__ void __launch_bounds__(256) cell_dot_contig_kernel(const __nv_bfloat16* __restrict__ x, int cell_chunks,
+                                                              const float* __restrict__ wdiff, int splits,
+                                                              float* __restrict__ partial, long long items) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * 8 + warp;
+  if (item >= items) return;
+  const long long cell = item / splits;
+  const int split = (int)(item - cell * splits);
+  float wv[P][8];
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(wdiff + (lane + 32 * j) * 8));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(wdiff + (lane + 32 * j) * 8 + 4));
+    wv[j][0] = a.x; wv[j][1] = a.y; wv[j][2] = a.z; wv[j][3] = a.w;
+    wv[j][4] = b.x; wv[j][5] = b.y; wv[j][6] = b.z; wv[j][7] = b.w;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(x) + cell * cell_chunks + (long long)split * 1024;
+  const int nq = min(1024, cell_chunks - split * 1024);
+  float acc[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) acc[j] = 0.f;
+#pragma unroll 2
+  for (int q0 = lane; q0 < nq; q0 += 32 * P) {
+    uint4 v[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = q0 + 32 * j < nq ? __ldg(src + q0 + 32 * j) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      float2 f;
+      f = unpack_bf16x2(v[j].x); acc[j] = fmaf(f.x, wv[j][0], acc[j]); acc[j] = fmaf(f.y, wv[j][1], acc[j]);
+      f = unpack_bf16x2(v[j].y); acc[j] = fmaf(f.x, wv[j][2], acc[j]); acc[j] = fmaf(f.y, wv[j][3], acc[j]);
+      f = unpack_bf16x2(v[j].z); acc[j] = fmaf(f.x, wv[j][4], acc[j]); acc[j] = fmaf(f.y, wv[j][5], acc[j]);
+      f = unpack_bf16x2(v[j].w); acc[j] = fmaf(f.x, wv[j][6], acc[j]); acc[j] = fmaf(f.y, wv[j][7], acc[j]);
+    }
+  }
+  float a = 0.f;
+#pragma unroll
+  for (int j = 0; j < P; ++j) a += acc[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) partial[item] = a;
+}
+
 // Same as cell_dot_kernel for cells of <= 32*NPL chunks (one split): every
 // lane issues all of its NPL 16-byte loads before the first FMA, so a warp
 // keeps a whole cell (up to 8 KiB) in flight.
@@ -632,6 +683,28 @@ cudaError_t launch_spatial_masker(const void* x, int x_f32, int ld, int n, int h
   const long long items = (long long)total * splits;
   const int blocks = (int)((items + 7) / 8);
   const int cell_chunks = win * win * (c / 8);
+  // layer masker (one cell per image, contiguous rows): the register-weight kernel
+  static const int contig_env = [] {
+    const char* e = getenv("LAUD_CELL_DOT_CONTIG");
+    return e ? atoi(e) : 1;
+  }();
+  const int P = c / 256;
+  if (contig_env && !x_f32 && !dn && cells_h == 1 && cells_w == 1 && win == h && win == w && ld == c &&
+      c % 256 == 0 && (P == 1 || P == 2 || P == 4 || P == 8) && splits == (cell_chunks + 1023) / 1024) {
+    auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+    if (P == 1)
+      launch_k(cell_dot_contig_kernel<1>, dim3(blocks), dim3(256), 0, stream, xb, cell_chunks, wdiff, splits, partial, items);
+    else if (P == 2)
+      launch_k(cell_dot_contig_kernel<2>, dim3(blocks), dim3(256), 0, stream, xb, cell_chunks, wdiff, splits, partial, items);
+    else if (P == 4)
+      launch_k(cell_dot_contig_kernel<4>, dim3(blocks), dim3(256), 0, stream, xb, cell_chunks, wdiff, splits, partial, items);
+    else
+      launch_k(cell_dot_contig_kernel<8>, dim3(blocks), dim3(256), 0, stream, xb, cell_chunks, wdiff, splits, partial, items);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    MaskerFlag f{partial, splits, 1.0f / (float)(win * win), bias, coarse};
+    return launch_compact(f, total, list, count, scan, stream);
+  }
   if (false && !x_f32 && splits == 1 && cell_chunks <= 512) {  // measured slower (occupancy)
     auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
     const size_t sm = c * sizeof(float);
