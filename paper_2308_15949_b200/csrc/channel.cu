@@ -65,6 +65,25 @@ __global__ void __launch_bounds__(CM_THREADS) channel_masker_kernel(
       const int grp = cpp > (int)blockDim.x ? 0 : tid / cpp;
       float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       int px = grp;
+      if constexpr (sizeof(T) == 2) {
+        // bf16: eight raw 16-byte loads in flight per thread (4 registers each;
+        // 1024-thread CTAs leave 64 registers per thread), then accumulated in
+        // pixel order
+        for (; px + 7 * groups < hw; px += 8 * groups) {
+          uint4 r[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            r[u] = __ldg(reinterpret_cast<const uint4*>(xs + (size_t)(px + u * groups) * ld + chunk * 8));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            float2 f;
+            f = unpack_bf16x2(r[u].x); a[0] += f.x; a[1] += f.y;
+            f = unpack_bf16x2(r[u].y); a[2] += f.x; a[3] += f.y;
+            f = unpack_bf16x2(r[u].z); a[4] += f.x; a[5] += f.y;
+            f = unpack_bf16x2(r[u].w); a[6] += f.x; a[7] += f.y;
+          }
+        }
+      }
       // four independent 16-byte loads in flight per thread (the pass is HBM-bound)
       for (; px + 3 * groups < hw; px += 4 * groups) {
         float v0[8], v1[8], v2[8], v3[8];
