@@ -29,7 +29,7 @@ def test_fitted_constants_and_monotonicity():
 
 
 def test_predictor_tracks_measured_b200_blocks():
-    data = json.loads((ROOT / "profiles" / "r01_block_latency_b200.json").read_text())
+    data = json.loads((ROOT / "profiles" / "r02m_block_latency_b200.json").read_text())
     m = P.B200Predictor()
     nets = {}
     ape = []

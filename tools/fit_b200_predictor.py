@@ -102,7 +102,7 @@ def main():
     out_hw = ROOT / "paper_2308_15949_b200" / "data" / "b200.hw"
     out_hw.parent.mkdir(exist_ok=True)
     out_hw.write_text("# NVIDIA B200 (sm_100a), recalibrated on measured LAUD block latencies\n"
-                      "# (profiles/r01_block_latency_b200.json, tools/fit_b200_predictor.py).\n"
+                      f"# (profiles/{Path(sys.argv[1]).name}, tools/fit_b200_predictor.py).\n"
                       "# fp32_per_pe carries the fitted tensor-core MAC rate per SM and cycle.\n"
                       + core.format_hardware(hw))
     by_para = {}

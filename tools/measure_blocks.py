@@ -84,7 +84,8 @@ def main():
                 # in-place residual for identity-skip blocks, as in the network executor
                 out_t = (x if not blk.has_downsample else
                          torch.empty(n, o.height, o.width, db.cout_p, dtype=torch.bfloat16, device="cuda"))
-                add("static", timed(lambda: db.forward(x, "static", out=out_t, ws=ws), flush), r=1.0)
+                add("static", timed(lambda: db.forward(x, "static", out=out_t, ws=ws, latency_split=True), flush),
+                    r=1.0)
                 for s in s_opts:
                     cells = (o.height // s) * (o.width // s)
                     for r in ratios:
